@@ -1,0 +1,147 @@
+/* sk_poisson.h — C ABI of the B200-native DFS spectral Poisson solver.
+ *
+ * This is the drop-in boundary for the reference's Poisson entry points
+ * (namespace spherekit, /root/reference/proj/include/spherekit/poisson.hpp):
+ *
+ *   reference (C++)                                      here (C ABI)
+ *   -------------------------------------------------    ----------------------------
+ *   PoissonSolution solve(const PoissonProblem&)         sk_solve_coeffs
+ *       poisson.hpp:47, poisson.cpp:121-161
+ *   ResidualReport residual(const PoissonProblem&,       sk_residual
+ *       const PoissonSolution&)  poisson.hpp:54, .cpp:163-186
+ *   sample_dfs -> analyze_2d -> Msin^2 -> solve ->       sk_solve_grid
+ *       sample_grid (the grid-level composition:
+ *       sphere_domain.cpp:46-52, fourier.cpp:170-209,
+ *       poisson.cpp:61-71, :121-161)
+ *   test helper real_sph_harmonic sums                   sk_shgen (input generator)
+ *       (tests/support/helpers.hpp:18-27)
+ *
+ * Layouts (bit-exact contract):
+ *   coefficient matrices F, X: row-major M x N complex double, interleaved
+ *     (re, im) — std::complex<double> layout (types.hpp:17-41); row i is theta
+ *     mode j = i - M/2, column kc is lambda mode k = kc - N/2;
+ *   physical grids f, u: row-major (M/2+1) x N real double; row p is
+ *     theta_p = 2 pi p / M (p = 0 and p = M/2 are the poles), column q is
+ *     lambda_q = -pi + 2 pi q / N.  The doubled grid of sample_dfs is never
+ *     materialised (its rows j < M/2 are the glide reflection of row M/2 - j).
+ *
+ * Errors: every call returns an sk_status; sk_last_error() describes the last
+ * failure on the calling thread.  The C++ shim (spherekit/poisson_b200.hpp)
+ * rethrows SK_ERR_SIZE as spherekit::size_error, SK_ERR_PRECONDITION as
+ * precondition_error and SK_ERR_SINGULAR as structure_error, as the reference
+ * throws them (poisson.cpp:123-124, :115-116; banded.cpp:132, :306).
+ *
+ * Threading: a plan owns device buffers and a stream; one plan must not be
+ * used from two threads at once; distinct plans are independent.  There is no
+ * CPU fallback: without a usable sm_100 device every compute call fails with
+ * SK_ERR_CUDA.
+ */
+#ifndef SK_POISSON_H
+#define SK_POISSON_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sk_status {
+    SK_OK = 0,
+    SK_ERR_SIZE = 1,          /* non-positive or odd sizes (reference size_error)     */
+    SK_ERR_PRECONDITION = 2,  /* right-hand side with nonzero surface mean            */
+    SK_ERR_SINGULAR = 3,      /* numerically singular band system (structure_error)  */
+    SK_ERR_CUDA = 4,          /* CUDA runtime / launch failure, or no device          */
+    SK_ERR_UNSUPPORTED = 5,   /* size outside this build's FFT / on-chip limits       */
+    SK_ERR_ARGUMENT = 6,      /* null pointer, bad flag, wrong plan kind              */
+    SK_ERR_NCCL = 7           /* reserved for the collective layer                    */
+} sk_status;
+
+typedef struct sk_plan_s* sk_plan_t;
+
+/* flags for data arguments */
+#define SK_HOST 0u     /* pointers are host memory (copies inside the call)   */
+#define SK_DEVICE 1u   /* pointers are device memory on the plan's device    */
+#define SK_ASYNC 2u    /* do not synchronise the plan stream before returning
+                          (device pointers only; errors that need a host-side
+                          check, e.g. the mean precondition, are then reported
+                          by the next sk_sync) */
+
+/* Create a plan for an M x N problem (M = doubled theta count, N = lambda
+ * count, both even) with `nrhs` independent right-hand sides on CUDA device
+ * `device`.  Grid-path sizes must factor into 2,3,5,7 with M/2 and N/2 within
+ * the on-chip limits reported by sk_plan_info (else SK_ERR_UNSUPPORTED; the
+ * coefficient-space solve accepts any even sizes).  Replaces the per-call
+ * operator construction of poisson.cpp:127-128 / fourier.cpp:22-35. */
+sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* plan);
+sk_status sk_plan_destroy(sk_plan_t plan);
+/* Use an external CUDA stream (cudaStream_t) for all work of this plan. */
+sk_status sk_plan_set_stream(sk_plan_t plan, void* stream);
+sk_status sk_sync(sk_plan_t plan);
+
+/* Coefficient-space solve, the drop-in for spherekit::solve(PoissonProblem):
+ * X = solution of the N decoupled banded systems with the (j=0,k=0) row
+ * replaced by 2 pi w^T X_0 = 0.  Bit-identical to the reference for every
+ * k != 0 column (ascending Thomas on the four exact-zero-decoupled chains,
+ * IEEE mul/sub/div in the reference's order, no FMA); k = 0 agrees to
+ * rounding.  Checks the nonzero-mean precondition like check_mean_zero
+ * (poisson.cpp:101-117).  F and X: nrhs consecutive M x N complex matrices. */
+sk_status sk_solve_coeffs(sk_plan_t plan, const double* F, double* X, unsigned flags);
+
+/* Residual report (poisson.cpp:163-186) for one right-hand side:
+ * out[0] = interior max |(lap - k^2) X_k - F_k| over all equations but
+ * (j=0,k=0); out[1] = that replaced equation's |defect|; out[2] = |2 pi w^T X_0|. */
+sk_status sk_residual(sk_plan_t plan, const double* F, const double* X, double out[3], unsigned flags);
+
+/* Grid-level solve: physical samples f -> physical solution u of
+ * Lap u = f with integral(u) = 0, through DFS doubling, the 2D trigonometric
+ * transforms, Msin^2, the per-mode banded solves and the inverse transforms.
+ * f and u: nrhs consecutive (M/2+1) x N real grids (may alias).
+ * If X_half != NULL it receives the solution coefficients for lambda modes
+ * k = 0..N/2 as an (N/2+1) x M complex array, X_half[k][i] = X[i][k + N/2]
+ * (the k < 0 half is its complex conjugate, reflected: real data). */
+sk_status sk_solve_grid(sk_plan_t plan, const double* f, double* u, double* X_half, unsigned flags);
+
+/* Surface mean 2 pi w^T f~_0 of the last grid solve's right-hand side and
+ * max|F| of its coefficients (for callers that want the precondition data). */
+sk_status sk_last_mean(sk_plan_t plan, double out[3]);
+
+/* Seeded spherical-harmonic input generator (untimed helper):
+ * phys = sum_{l=1..L} sum_{|m|<=l} coeffs[l*l+l+m] Y_l^m on the plan's
+ * physical grid, Y as in the reference tests (helpers.hpp:18-27).
+ * coeffs: (L+1)^2 doubles; phys: (M/2+1) x N real; both device pointers. */
+sk_status sk_shgen(sk_plan_t plan, int L, const double* coeffs_dev, double* phys_dev);
+
+/* Stage entry points for the slab-decomposed multi-GPU solve (one plan per
+ * rank; the transposes between them are collectives run by the caller).
+ * Spectrum blocks use the all-to-all layout described in DESIGN.md §5:
+ *   sk_stage_lambda_fwd: rows [r0, r1) of f -> send buffer, blocks per
+ *     destination d ordered [d][k - k0_d][p - r0] (complex);
+ *   sk_stage_theta:      columns [k0, k1) read from the receive buffer,
+ *     blocks per source s ordered [s][k - k0][p - r0_s], solved in place;
+ *   sk_stage_lambda_inv: rows [r0, r1) of u from the returned blocks.
+ * row_bounds[P+1] and col_bounds[P+1] give every rank's slab. */
+sk_status sk_stage_lambda_fwd(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
+                              const double* f_rows_dev, double* send_dev);
+sk_status sk_stage_theta(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
+                         double* recv_dev);
+sk_status sk_stage_lambda_inv(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
+                              const double* back_dev, double* u_rows_dev);
+
+/* Plan facts: info[0] = M, [1] = N, [2] = nrhs, [3] = device,
+ * [4] = grid path supported (1/0), [5] = spectrum leading dimension,
+ * [6] = theta-stage split (CTAs per column), [7] = theta-stage threads,
+ * [8] = lambda-stage threads, [9] = kernels launched by the last call. */
+sk_status sk_plan_info(sk_plan_t plan, long long info[16]);
+
+/* Time one launch of each stage (device events, ms): t[0] lambda_fwd,
+ * t[1] theta, t[2] lambda_inv, t[3] coeff solve (last measured). */
+sk_status sk_stage_times(sk_plan_t plan, double t[4]);
+sk_status sk_enable_stage_timing(sk_plan_t plan, int on);
+
+const char* sk_last_error(void);
+const char* sk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SK_POISSON_H */

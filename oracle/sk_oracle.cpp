@@ -1,0 +1,789 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY — see sk_oracle.h.
+//
+// A from-the-algorithm restatement of the reference hot path; each function
+// cites the reference lines it follows.  Plain IEEE double (the Makefile does
+// not enable FMA contraction), std::complex arithmetic as in the reference so
+// that the coefficient-space solve is bit-comparable with it.
+#include "sk_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "skfft.h"
+
+namespace {
+
+using cplx = std::complex<double>;
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr double kTwoPi = 2.0 * kPi;
+
+enum { OK = 0, E_SIZE = 1, E_PRECOND = 2, E_STRUCT = 3, E_OTHER = 9 };
+struct size_err : std::runtime_error { using std::runtime_error::runtime_error; };
+struct precond_err : std::runtime_error { using std::runtime_error::runtime_error; };
+struct struct_err : std::runtime_error { using std::runtime_error::runtime_error; };
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return OK;
+    } catch (const size_err& e) {
+        g_err = e.what();
+        return E_SIZE;
+    } catch (const precond_err& e) {
+        g_err = e.what();
+        return E_PRECOND;
+    } catch (const struct_err& e) {
+        g_err = e.what();
+        return E_STRUCT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return E_OTHER;
+    }
+}
+
+const cplx* as_c(const double* p) { return reinterpret_cast<const cplx*>(p); }
+cplx* as_c(double* p) { return reinterpret_cast<cplx*>(p); }
+
+// ---------------------------------------------------------------- band matrix
+// Square complex band matrix, storage a[i*(kl+ku+1) + (j-i+kl)]
+// (banded.hpp:11-41).
+struct Band {
+    int n = 0, kl = 0, ku = 0;
+    std::vector<cplx> a;
+    Band() = default;
+    Band(int n_, int kl_, int ku_) : n(n_), kl(kl_), ku(ku_), a(static_cast<size_t>(n_) * (kl_ + ku_ + 1)) {}
+    bool in(int i, int j) const { return j - i >= -kl && j - i <= ku && j >= 0 && j < n; }
+    cplx get(int i, int j) const { return in(i, j) ? a[static_cast<size_t>(i) * (kl + ku + 1) + (j - i + kl)] : cplx{}; }
+    cplx& at(int i, int j) { return a[static_cast<size_t>(i) * (kl + ku + 1) + (j - i + kl)]; }
+    // banded.cpp:8-19: ascending-j accumulation, exact zeros included.
+    std::vector<cplx> apply(const cplx* x) const {
+        std::vector<cplx> y(n);
+        for (int i = 0; i < n; ++i) {
+            cplx acc{};
+            for (int j = std::max(0, i - kl); j <= std::min(n - 1, i + ku); ++j) acc += get(i, j) * x[j];
+            y[i] = acc;
+        }
+        return y;
+    }
+};
+
+// The theta operators of poisson.cpp:15-40, restated from their closed form.
+// msin: (i,i+1) = +i/2, (i,i-1) = -i/2; mcos: 1/2 on both; Dm = diag(i j).
+// lap = Msin (Msin Dm) Dm + Mcos (Msin Dm); with the square truncation its
+// entries are the real dyadic numbers below (every product in band_mul is
+// exact, so this equals the reference bit for bit; tests pin it).
+Band lap_band(int m) {
+    Band L(m, 2, 2);
+    const int h = m / 2;
+    for (int i = 0; i < m; ++i) {
+        const double j = i - h;
+        if (i - 2 >= 0) L.at(i, i - 2) = cplx((j - 2) * (j - 1) / 4.0, 0.0);
+        if (i + 2 < m) L.at(i, i + 2) = cplx((j + 2) * (j + 1) / 4.0, 0.0);
+        if (i - 1 >= 0) L.at(i, i - 1) = cplx(0.0, 0.0);
+        if (i + 1 < m) L.at(i, i + 1) = cplx(0.0, 0.0);
+        double d = -j * j / 2.0;
+        if (i == 0) d = -j * (j - 1) / 4.0;          // j = -M/2: only the (j+1) term survives
+        if (i == m - 1) d = -j * (j + 1) / 4.0;      // j = M/2-1
+        L.at(i, i) = cplx(d, 0.0);
+    }
+    return L;
+}
+
+// Msin^2 = band_mul(msin, msin): (-1/4, 1/2, -1/4) at offsets (-2,0,+2), 1/4 on
+// the first and last diagonal entries, exact zeros at +-1 (poisson.cpp:61).
+Band msin2_band(int m) {
+    Band S(m, 2, 2);
+    for (int i = 0; i < m; ++i) {
+        if (i - 2 >= 0) S.at(i, i - 2) = cplx(-0.25, 0.0);
+        if (i + 2 < m) S.at(i, i + 2) = cplx(-0.25, 0.0);
+        if (i - 1 >= 0) S.at(i, i - 1) = cplx(0.0, 0.0);
+        if (i + 1 < m) S.at(i, i + 1) = cplx(0.0, 0.0);
+        S.at(i, i) = cplx((i == 0 || i == m - 1) ? 0.25 : 0.5, 0.0);
+    }
+    return S;
+}
+
+std::vector<cplx> weights(int m) {  // poisson.cpp:42-50
+    std::vector<cplx> w(m);
+    for (int i = 0; i < m; ++i) {
+        const int k = i - m / 2;
+        if (k % 2 != 0) continue;
+        w[i] = 2.0 / (1.0 - static_cast<double>(k) * k);
+    }
+    return w;
+}
+
+// ------------------------------------------------------------- band solvers
+// Gaussian elimination with partial pivoting inside the band, restated from
+// banded.cpp:101-158.  Each row keeps a window of `width` = 2 kl + ku + 1
+// entries starting at global column base[r]; a row is shifted left (aligned)
+// before it is used at column c, exactly as banded.cpp:89-97 does.
+struct Win {
+    int base = 0, len = 0;
+    cplx* e = nullptr;
+    cplx val(int col) const {
+        const int t = col - base;
+        return (t >= 0 && t < len) ? e[t] : cplx{};
+    }
+    void align(int col, int width) {
+        if (base >= col) return;
+        const int sh = col - base;
+        const int keep = std::max(0, len - sh);
+        for (int t = 0; t < keep; ++t) e[t] = e[t + sh];
+        for (int t = keep; t < width; ++t) e[t] = cplx{};
+        base = col;
+        len = width;
+    }
+};
+
+std::vector<cplx> band_solve(const Band& A, const cplx* b) {
+    const int n = A.n, kl = A.kl, ku = A.ku;
+    const int width = 2 * kl + ku + 1;
+    std::vector<cplx> store(static_cast<size_t>(n) * width);
+    std::vector<Win> row(n);
+    std::vector<cplx> rhs(b, b + n);
+    std::vector<int> perm(n);
+    for (int i = 0; i < n; ++i) {
+        perm[i] = i;
+        row[i].base = std::max(0, i - kl);
+        row[i].len = width;
+        row[i].e = store.data() + static_cast<size_t>(i) * width;
+        for (int j = row[i].base; j <= std::min(n - 1, i + ku); ++j) row[i].e[j - row[i].base] = A.get(i, j);
+    }
+    for (int c = 0; c < n; ++c) {
+        const int last = std::min(n - 1, c + kl);
+        int piv = c;
+        double best = std::abs(row[perm[c]].val(c));
+        for (int r = c + 1; r <= last; ++r) {
+            const double v = std::abs(row[perm[r]].val(c));
+            if (v > best) {  // strict: ties keep the earlier row
+                best = v;
+                piv = r;
+            }
+        }
+        if (best < 1e-300) throw struct_err("band_solve: matrix is numerically singular");
+        std::swap(perm[c], perm[piv]);
+        Win& P = row[perm[c]];
+        P.align(c, width);
+        const cplx pv = P.e[0];
+        for (int r = c + 1; r <= last; ++r) {
+            Win& R = row[perm[r]];
+            const cplx v = R.val(c);
+            if (v == cplx{}) continue;
+            R.align(c, width);
+            const cplx f = v / pv;
+            R.e[0] = cplx{};
+            for (int t = 1; t < width; ++t) R.e[t] -= f * P.e[t];
+            rhs[perm[r]] -= f * rhs[perm[c]];
+        }
+    }
+    std::vector<cplx> x(n);
+    for (int c = n - 1; c >= 0; --c) {
+        const Win& P = row[perm[c]];
+        cplx acc = rhs[perm[c]];
+        for (int j = c + 1; j <= std::min(n - 1, c + width - 1); ++j) acc -= P.val(j) * x[j];
+        x[c] = acc / P.e[c - P.base];
+    }
+    return x;
+}
+
+// Bordered solve restated from banded.cpp:160-328: the band rows (minus
+// skip_row) plus one dense row.  Band rows are admitted to the active set in
+// order of their first column; at each column the largest band candidate is
+// preferred unless it is below 1e-10 times the largest dense candidate, in
+// which case a dense row pivots and any band rows it touches are promoted to
+// dense rows.  Back substitution runs over the recorded pivot rows.
+std::vector<cplx> band_solve_dense(const Band& A, int skip, const cplx* w, cplx wrhs, const cplx* b) {
+    const int n = A.n, kl = A.kl, ku = A.ku;
+    const int width = 2 * kl + ku + 1;
+    struct BR {
+        Win win;
+        cplx rhs;
+        bool used = false;
+    };
+    struct DR {
+        std::vector<cplx> e;
+        cplx rhs;
+        bool used = false;
+    };
+    std::vector<cplx> store(static_cast<size_t>(n) * width);
+    std::vector<BR> band;
+    band.reserve(n);
+    for (int i = 0; i < n; ++i) {
+        if (i == skip) continue;
+        BR r;
+        r.win.base = std::max(0, i - kl);
+        r.win.len = width;
+        r.win.e = store.data() + band.size() * width;
+        for (int j = r.win.base; j <= std::min(n - 1, i + ku); ++j) r.win.e[j - r.win.base] = A.get(i, j);
+        r.rhs = b[i];
+        band.push_back(r);
+    }
+    std::vector<int> order(band.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+    std::stable_sort(order.begin(), order.end(), [&](int p, int q) { return band[p].win.base < band[q].win.base; });
+    std::vector<DR> dense;
+    dense.push_back({std::vector<cplx>(w, w + n), wrhs, false});
+    struct Up {
+        bool dense = false;
+        int idx = -1;
+    };
+    std::vector<Up> up(n);
+    std::vector<int> active;
+    size_t next = 0;
+    for (int c = 0; c < n; ++c) {
+        while (next < order.size() && band[order[next]].win.base <= c) active.push_back(order[next++]);
+        int bb = -1;
+        double bb_abs = 0;
+        for (int idx : active) {
+            if (band[idx].used) continue;
+            const double v = std::abs(band[idx].win.val(c));
+            if (v > bb_abs) {
+                bb_abs = v;
+                bb = idx;
+            }
+        }
+        int bd = -1;
+        double bd_abs = 0;
+        for (size_t d = 0; d < dense.size(); ++d) {
+            if (dense[d].used) continue;
+            const double v = std::abs(dense[d].e[c]);
+            if (v > bd_abs) {
+                bd_abs = v;
+                bd = static_cast<int>(d);
+            }
+        }
+        if (bb >= 0 && bb_abs >= 1e-10 * bd_abs && bb_abs >= 1e-300) {
+            BR& P = band[bb];
+            P.used = true;
+            P.win.align(c, width);
+            up[c] = {false, bb};
+            const cplx pv = P.win.e[0];
+            for (int idx : active) {
+                BR& R = band[idx];
+                if (R.used) continue;
+                const cplx v = R.win.val(c);
+                if (v == cplx{}) continue;
+                R.win.align(c, width);
+                const cplx f = v / pv;
+                R.win.e[0] = cplx{};
+                for (int t = 1; t < width; ++t) R.win.e[t] -= f * P.win.e[t];
+                R.rhs -= f * P.rhs;
+            }
+            for (DR& D : dense) {
+                if (D.used) continue;
+                const cplx v = D.e[c];
+                if (v == cplx{}) continue;
+                const cplx f = v / pv;
+                D.e[c] = cplx{};
+                for (int t = 1; t < width && c + t < n; ++t) D.e[c + t] -= f * P.win.e[t];
+                D.rhs -= f * P.rhs;
+            }
+        } else if (bd >= 0 && bd_abs >= 1e-300) {
+            dense[bd].used = true;
+            up[c] = {true, bd};
+            const std::vector<cplx> pe = dense[bd].e;  // copy: `dense` may grow
+            const cplx prhs = dense[bd].rhs;
+            const cplx pv = pe[c];
+            for (int idx : active) {
+                BR& R = band[idx];
+                if (R.used) continue;
+                const cplx v = R.win.val(c);
+                if (v == cplx{}) continue;
+                DR pr;
+                pr.e.assign(n, cplx{});
+                for (int t = 0; t < R.win.len; ++t) {
+                    const int col = R.win.base + t;
+                    if (col >= 0 && col < n) pr.e[col] = R.win.e[t];
+                }
+                pr.rhs = R.rhs;
+                const cplx f = v / pv;
+                for (int j = c; j < n; ++j) pr.e[j] -= f * pe[j];
+                pr.e[c] = cplx{};
+                pr.rhs -= f * prhs;
+                R.used = true;
+                dense.push_back(std::move(pr));
+            }
+            for (size_t d = 0; d < dense.size(); ++d) {
+                DR& D = dense[d];
+                if (D.used || static_cast<int>(d) == bd) continue;
+                const cplx v = D.e[c];
+                if (v == cplx{}) continue;
+                const cplx f = v / pv;
+                for (int j = c; j < n; ++j) D.e[j] -= f * pe[j];
+                D.e[c] = cplx{};
+                D.rhs -= f * prhs;
+            }
+        } else {
+            throw struct_err("band_solve_with_dense_row: singular bordered system");
+        }
+    }
+    std::vector<cplx> x(n);
+    for (int c = n - 1; c >= 0; --c) {
+        cplx acc, pv;
+        if (up[c].dense) {
+            const DR& r = dense[up[c].idx];
+            acc = r.rhs;
+            for (int j = c + 1; j < n; ++j) acc -= r.e[j] * x[j];
+            pv = r.e[c];
+        } else {
+            const BR& r = band[up[c].idx];
+            acc = r.rhs;
+            for (int j = c + 1; j <= std::min(n - 1, r.win.base + r.win.len - 1); ++j) acc -= r.win.val(j) * x[j];
+            pv = r.win.val(c);
+        }
+        x[c] = acc / pv;
+    }
+    return x;
+}
+
+std::vector<cplx> div_sin(const std::vector<cplx>& c) {  // fourier.cpp:92-103
+    const int n = static_cast<int>(c.size());
+    if (n == 0) throw size_err("div_sin: empty input");
+    Band ms(n, 1, 1);
+    for (int i = 0; i < n; ++i) {
+        if (i + 1 < n) ms.at(i, i + 1) = cplx(0, 0.5);
+        if (i - 1 >= 0) ms.at(i, i - 1) = cplx(0, -0.5);
+    }
+    return band_solve(ms, c.data());
+}
+
+double max_abs(const cplx* a, size_t len) {
+    double m = 0;
+    for (size_t i = 0; i < len; ++i) m = std::max(m, std::abs(a[i]));
+    return m;
+}
+
+// poisson.cpp:101-117
+void check_mean_zero(int m, int n, const cplx* F) {
+    std::vector<cplx> f0(m);
+    for (int i = 0; i < m; ++i) f0[i] = F[static_cast<size_t>(i) * n + n / 2];
+    const double fscale = max_abs(F, static_cast<size_t>(m) * n);
+    if (fscale == 0.0) return;
+    if (m % 2 != 0) throw size_err("CoeffVec: length must be even");
+    const std::vector<cplx> a = div_sin(div_sin(f0));
+    const std::vector<cplx> w = weights(m);
+    cplx mean{};
+    for (int i = 0; i < m; ++i) mean += w[i] * a[i];
+    mean *= kTwoPi;
+    if (std::abs(mean) > 1e-6 * 4.0 * kPi * fscale)
+        throw precond_err("poisson solve: right-hand side has a nonzero surface mean");
+}
+
+void solve_impl(int m, int n, const cplx* F, cplx* X, int threads) {
+    if (m <= 0 || n <= 0 || m % 2 != 0 || n % 2 != 0) throw size_err("poisson solve: sizes must be positive and even");
+    check_mean_zero(m, n, F);
+    const Band lap = lap_band(m);
+    const std::vector<cplx> w = weights(m);
+    auto column = [&](int kc) {
+        const int k = kc - n / 2;
+        std::vector<cplx> rhs(m);
+        for (int i = 0; i < m; ++i) rhs[i] = F[static_cast<size_t>(i) * n + kc];
+        std::vector<cplx> x;
+        if (k != 0) {
+            Band a = lap;
+            for (int i = 0; i < m; ++i) a.at(i, i) += cplx(-static_cast<double>(k) * k, 0.0);
+            x = band_solve(a, rhs.data());
+        } else {
+            x = band_solve_dense(lap, m / 2, w.data(), cplx{}, rhs.data());
+        }
+        for (int i = 0; i < m; ++i) X[static_cast<size_t>(i) * n + kc] = x[i];
+    };
+    unsigned hw = std::thread::hardware_concurrency();
+    if (hw == 0) hw = 1;
+    if (threads >= 1) hw = std::min<unsigned>(hw, static_cast<unsigned>(threads));
+    const int T = n < 64 ? 1 : static_cast<int>(std::min<unsigned>(hw, 16));
+    if (T <= 1) {
+        for (int kc = 0; kc < n; ++kc) column(kc);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (int kc = t; kc < n; kc += T) column(kc);
+            });
+        for (auto& th : pool) th.join();
+    }
+}
+
+// ----------------------------------------------------------------- transforms
+void fft_inplace(std::vector<cplx>& v, int sign) {
+    skfft_plan* p = skfft_plan_create(static_cast<int>(v.size()), sign);
+    skfft_execute(p, reinterpret_cast<double*>(v.data()), reinterpret_cast<double*>(v.data()));
+    skfft_destroy(p);
+}
+
+// fourier.cpp:39-53: c_k = (1/n) (-1)^k F_{(k+n) mod n}, ascending k.
+std::vector<cplx> analyze_1d(const cplx* s, int n) {
+    if (n <= 0 || n % 2 != 0) throw size_err("analyze_1d: sample count must be even");
+    std::vector<cplx> w(s, s + n);
+    fft_inplace(w, -1);
+    std::vector<cplx> out(n);
+    for (int k = -n / 2; k < n / 2; ++k) {
+        const double sg = (k % 2 == 0) ? 1.0 : -1.0;
+        out[k + n / 2] = sg / n * w[(k + n) % n];
+    }
+    return out;
+}
+
+// fourier.cpp:55-66: zero-pad / truncate, (-1)^k, backward FFT (unnormalised).
+std::vector<cplx> synthesize_1d(const cplx* c, int nc, int n_out) {
+    if (n_out <= 0 || n_out % 2 != 0) throw size_err("synthesize_1d: output size must be even");
+    std::vector<cplx> g(n_out, cplx{});
+    const int kmin = -nc / 2;
+    const int lo = std::max(kmin, -n_out / 2), hi = std::min(-kmin, n_out / 2);
+    for (int k = lo; k < hi; ++k) {
+        const double sg = (k % 2 == 0) ? 1.0 : -1.0;
+        g[(k + n_out) % n_out] += sg * c[k - kmin];
+    }
+    fft_inplace(g, +1);
+    return g;
+}
+
+void analyze_2d(int m, int n, const cplx* grid, cplx* X) {  // fourier.cpp:170-188
+    if (m <= 0 || n <= 0 || m % 2 || n % 2) throw size_err("BMCGrid: sample counts must be positive and even");
+    std::vector<cplx> half(static_cast<size_t>(m) * n), col(m), row(n);
+    for (int k = 0; k < n; ++k) {
+        for (int j = 0; j < m; ++j) col[j] = grid[static_cast<size_t>(j) * n + k];
+        const std::vector<cplx> c = analyze_1d(col.data(), m);
+        for (int j = 0; j < m; ++j) half[static_cast<size_t>(j) * n + k] = c[j];
+    }
+    for (int j = 0; j < m; ++j) {
+        const std::vector<cplx> c = analyze_1d(half.data() + static_cast<size_t>(j) * n, n);
+        std::copy(c.begin(), c.end(), X + static_cast<size_t>(j) * n);
+    }
+}
+
+void sample_grid(int rows, int cols, const cplx* X, int m, int n, cplx* g) {  // fourier.cpp:190-209
+    if (m % 2 != 0 || n % 2 != 0) throw size_err("sample_grid: output sizes must be even");
+    std::vector<cplx> half(static_cast<size_t>(m) * cols), c(rows);
+    for (int k = 0; k < cols; ++k) {
+        for (int j = 0; j < rows; ++j) c[j] = X[static_cast<size_t>(j) * cols + k];
+        const std::vector<cplx> v = synthesize_1d(c.data(), rows, m);
+        for (int j = 0; j < m; ++j) half[static_cast<size_t>(j) * cols + k] = v[j];
+    }
+    for (int j = 0; j < m; ++j) {
+        const std::vector<cplx> v = synthesize_1d(half.data() + static_cast<size_t>(j) * cols, cols, n);
+        std::copy(v.begin(), v.end(), g + static_cast<size_t>(j) * n);
+    }
+}
+
+// DFS doubling of physical samples: the index map of sphere_domain.cpp:19-26
+// evaluated on the grid of :46-52 — theta_i >= 0 (i >= M/2) reads physical
+// row i - M/2; theta_i < 0 reads row M/2 - i at longitude shifted by pi,
+// i.e. column (q + N/2) mod N.
+void dfs_double(int m, int n, const double* phys, cplx* g) {
+    for (int i = 0; i < m; ++i)
+        for (int q = 0; q < n; ++q) {
+            double v;
+            if (i >= m / 2) v = phys[static_cast<size_t>(i - m / 2) * n + q];
+            else v = phys[static_cast<size_t>(m / 2 - i) * n + (q + n / 2) % n];
+            g[static_cast<size_t>(i) * n + q] = cplx(v, 0.0);
+        }
+}
+
+// ------------------------------------------------------ spherical harmonics
+// Orthonormal associated Legendre P~_l^m(cos th) (no Condon-Shortley phase,
+// matching std::assoc_legendre in tests/support/helpers.hpp:18-27) by the
+// standard stable recurrences, with an extended exponent so that
+// sin(th)^m does not underflow for large m.
+void legendre_row(int L, int mm, double x, double s, std::vector<double>& out) {
+    // out[l - mm] = P~_l^mm(x) for l = mm..L
+    const double big = std::ldexp(1.0, 400), small = std::ldexp(1.0, -400);
+    double pmm = 1.0 / std::sqrt(4.0 * kPi);
+    int e = 0;
+    for (int i = 1; i <= mm; ++i) {
+        pmm *= std::sqrt((2.0 * i + 1.0) / (2.0 * i)) * s;
+        if (pmm != 0.0 && std::fabs(pmm) < small) {
+            pmm *= big;
+            e -= 400;
+        }
+    }
+    out.assign(L - mm + 1, 0.0);
+    if (pmm == 0.0) return;
+    auto emit = [&](int l, double v) { out[l - mm] = std::ldexp(v, e); };
+    double p2 = pmm;  // P_{l-2}
+    emit(mm, p2);
+    if (mm == L) return;
+    double p1 = std::sqrt(2.0 * mm + 3.0) * x * pmm;  // P_{mm+1}
+    emit(mm + 1, p1);
+    for (int l = mm + 2; l <= L; ++l) {
+        const double ll = l, m2 = static_cast<double>(mm) * mm;
+        const double a = std::sqrt((4.0 * ll * ll - 1.0) / (ll * ll - m2));
+        const double b = std::sqrt(((ll - 1.0) * (ll - 1.0) - m2) / (4.0 * (ll - 1.0) * (ll - 1.0) - 1.0));
+        const double p = a * (x * p1 - b * p2);
+        p2 = p1;
+        p1 = p;
+        if (std::fabs(p1) > big) {
+            p1 *= small;
+            p2 *= small;
+            e += 400;
+        }
+        emit(l, p1);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sko_last_error(void) { return g_err.c_str(); }
+
+int sko_build_lap(int m, double* lap) {
+    return guarded([&] {
+        if (m <= 0 || m % 2 != 0) throw size_err("build_operators: m must be positive and even");
+        const Band L = lap_band(m);
+        for (int i = 0; i < m; ++i)
+            for (int d = -2; d <= 2; ++d) lap[i * 5 + d + 2] = L.get(i, i + d).real();
+    });
+}
+
+int sko_integration_weights(int m, double* w) {
+    return guarded([&] {
+        const std::vector<cplx> v = weights(m);
+        for (int i = 0; i < m; ++i) w[i] = v[i].real();
+    });
+}
+
+int sko_band_solve(int n, int kl, int ku, const double* band, const double* b, double* x) {
+    return guarded([&] {
+        Band A(n, kl, ku);
+        std::memcpy(static_cast<void*>(A.a.data()), band, sizeof(cplx) * A.a.size());
+        const std::vector<cplx> r = band_solve(A, as_c(b));
+        std::memcpy(x, static_cast<const void*>(r.data()), sizeof(cplx) * n);
+    });
+}
+
+int sko_band_solve_dense_row(int n, int kl, int ku, const double* band, int skip_row, const double* w,
+                             double wrhs_re, double wrhs_im, const double* b, double* x) {
+    return guarded([&] {
+        Band A(n, kl, ku);
+        std::memcpy(static_cast<void*>(A.a.data()), band, sizeof(cplx) * A.a.size());
+        const std::vector<cplx> r = band_solve_dense(A, skip_row, as_c(w), cplx(wrhs_re, wrhs_im), as_c(b));
+        std::memcpy(x, static_cast<const void*>(r.data()), sizeof(cplx) * n);
+    });
+}
+
+int sko_div_sin(int n, const double* c, double* out) {
+    return guarded([&] {
+        if (n % 2 != 0) throw size_err("CoeffVec: length must be even");
+        const std::vector<cplx> u = div_sin(std::vector<cplx>(as_c(c), as_c(c) + n));
+        std::memcpy(out, static_cast<const void*>(u.data()), sizeof(cplx) * n);
+    });
+}
+
+int sko_solve(int m, int n, const double* F, double* X, int threads) {
+    return guarded([&] { solve_impl(m, n, as_c(F), as_c(X), threads); });
+}
+
+int sko_residual(int m, int n, const double* Fd, const double* Xd, double* out) {  // poisson.cpp:163-186
+    return guarded([&] {
+        const cplx* F = as_c(Fd);
+        const cplx* X = as_c(Xd);
+        const Band lap = lap_band(m);
+        double interior = 0, replaced = 0;
+        std::vector<cplx> xk(m);
+        for (int kc = 0; kc < n; ++kc) {
+            const int k = kc - n / 2;
+            for (int i = 0; i < m; ++i) xk[i] = X[static_cast<size_t>(i) * n + kc];
+            std::vector<cplx> r = lap.apply(xk.data());
+            for (int i = 0; i < m; ++i) {
+                r[i] -= static_cast<double>(k) * k * xk[i] + F[static_cast<size_t>(i) * n + kc];
+                if (k == 0 && i == m / 2) replaced = std::abs(r[i]);
+                else interior = std::max(interior, std::abs(r[i]));
+            }
+        }
+        const std::vector<cplx> w = weights(m);
+        cplx c{};
+        for (int i = 0; i < m; ++i) c += w[i] * X[static_cast<size_t>(i) * n + n / 2];
+        out[0] = interior;
+        out[1] = replaced;
+        out[2] = std::abs(kTwoPi * c);
+    });
+}
+
+int sko_msin2_columns(int m, int n, const double* Xd, double* Fd) {
+    return guarded([&] {
+        const Band S = msin2_band(m);
+        std::vector<cplx> col(m);
+        for (int k = 0; k < n; ++k) {
+            for (int i = 0; i < m; ++i) col[i] = as_c(Xd)[static_cast<size_t>(i) * n + k];
+            const std::vector<cplx> y = S.apply(col.data());
+            for (int i = 0; i < m; ++i) as_c(Fd)[static_cast<size_t>(i) * n + k] = y[i];
+        }
+    });
+}
+
+int sko_analyze_1d(int n, const double* s, double* c) {
+    return guarded([&] {
+        const std::vector<cplx> v = analyze_1d(as_c(s), n);
+        std::memcpy(c, static_cast<const void*>(v.data()), sizeof(cplx) * n);
+    });
+}
+
+int sko_synthesize_1d(int n, const double* c, int n_out, double* g) {
+    return guarded([&] {
+        if (n % 2 != 0) throw size_err("CoeffVec: length must be even");
+        const std::vector<cplx> v = synthesize_1d(as_c(c), n, n_out);
+        std::memcpy(g, static_cast<const void*>(v.data()), sizeof(cplx) * n_out);
+    });
+}
+
+int sko_analyze_2d(int m, int n, const double* grid, double* X) {
+    return guarded([&] { analyze_2d(m, n, as_c(grid), as_c(X)); });
+}
+
+int sko_sample_grid(int rows, int cols, const double* X, int m_out, int n_out, double* grid) {
+    return guarded([&] { sample_grid(rows, cols, as_c(X), m_out, n_out, as_c(grid)); });
+}
+
+int sko_dfs_double(int m, int n, const double* phys, double* grid) {
+    return guarded([&] {
+        if (m <= 0 || n <= 0 || m % 2 || n % 2) throw size_err("BMCGrid: sample counts must be positive and even");
+        dfs_double(m, n, phys, as_c(grid));
+    });
+}
+
+int sko_grid_pipeline(int m, int n, const double* phys, double* Xout, double* u_doubled, double* u_phys,
+                      int threads, double* mean_out) {
+    return guarded([&] {
+        if (m <= 0 || n <= 0 || m % 2 || n % 2) throw size_err("sizes must be positive and even");
+        const size_t mn = static_cast<size_t>(m) * n;
+        std::vector<cplx> g(mn), A(mn), F(mn), X(mn), U(mn);
+        dfs_double(m, n, phys, g.data());
+        analyze_2d(m, n, g.data(), A.data());
+        if (mean_out) {  // the surface mean 2 pi w^T a_0 of f~ (poisson.cpp:101-117)
+            const std::vector<cplx> w = weights(m);
+            cplx mu{};
+            for (int i = 0; i < m; ++i) mu += w[i] * A[static_cast<size_t>(i) * n + n / 2];
+            mean_out[0] = (kTwoPi * mu).real();
+            mean_out[1] = (kTwoPi * mu).imag();
+        }
+        const Band S = msin2_band(m);
+        std::vector<cplx> col(m);
+        for (int k = 0; k < n; ++k) {
+            for (int i = 0; i < m; ++i) col[i] = A[static_cast<size_t>(i) * n + k];
+            const std::vector<cplx> y = S.apply(col.data());
+            for (int i = 0; i < m; ++i) F[static_cast<size_t>(i) * n + k] = y[i];
+        }
+        solve_impl(m, n, F.data(), X.data(), threads);
+        sample_grid(m, n, X.data(), m, n, U.data());
+        if (Xout) std::memcpy(Xout, static_cast<const void*>(X.data()), sizeof(cplx) * mn);
+        if (u_doubled) std::memcpy(u_doubled, static_cast<const void*>(U.data()), sizeof(cplx) * mn);
+        if (u_phys) {
+            for (int p = 0; p <= m / 2; ++p) {
+                const int i = p < m / 2 ? m / 2 + p : 0;
+                for (int q = 0; q < n; ++q) u_phys[static_cast<size_t>(p) * n + q] = U[static_cast<size_t>(i) * n + q].real();
+            }
+        }
+    });
+}
+
+int sko_bench_problem(int nsizes, const int* sizes, double* F_last) {  // poisson.cpp:190-216
+    return guarded([&] {
+        std::mt19937_64 rng(0x5eedu);
+        std::uniform_real_distribution<double> unit(-1.0, 1.0);
+        for (int si = 0; si < nsizes; ++si) {
+            const int s = sizes[si];
+            if (s < 16 || s % 2 != 0) throw size_err("bench_poisson: sizes must be even and >= 16");
+            const Band S = msin2_band(s);
+            const std::vector<cplx> w = weights(s);
+            const int band = std::max(2, s / 8);
+            std::vector<cplx> col(s);
+            for (int kc = 0; kc < s; ++kc) {
+                const int k = kc - s / 2;
+                std::fill(col.begin(), col.end(), cplx{});
+                if (std::abs(k) <= band)
+                    for (int i = 0; i < s; ++i)
+                        if (std::abs(i - s / 2) <= band) col[i] = cplx(unit(rng), unit(rng));
+                if (k == 0) {
+                    cplx mean{};
+                    for (int i = 0; i < s; ++i) mean += w[i] * col[i];
+                    col[s / 2] -= mean / w[s / 2];
+                }
+                const std::vector<cplx> y = S.apply(col.data());
+                if (si == nsizes - 1)
+                    for (int i = 0; i < s; ++i) as_c(F_last)[static_cast<size_t>(i) * s + kc] = y[i];
+            }
+        }
+    });
+}
+
+int sko_random_mean_zero_problem(int m, int n, unsigned seed, double* Fd) {  // poisson_oracle.hpp:119-154
+    return guarded([&] {
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> unit(-1.0, 1.0);
+        const Band S = msin2_band(m);
+        const std::vector<cplx> w = weights(m);
+        const int bt = m / 4, bl = n / 4;
+        std::vector<cplx> col(m);
+        for (int kc = 0; kc < n; ++kc) {
+            const int k = kc - n / 2;
+            std::fill(col.begin(), col.end(), cplx{});
+            if (std::abs(k) <= bl) {
+                const double sg = k % 2 == 0 ? 1.0 : -1.0;
+                for (int j = 1; j <= bt; ++j) {
+                    const cplx v(unit(rng), unit(rng));
+                    col[m / 2 + j] = v;
+                    col[m / 2 - j] = sg * v;
+                }
+                if (k % 2 == 0) col[m / 2] = cplx(unit(rng), unit(rng));
+            }
+            if (k == 0) {
+                cplx mean{};
+                for (int i = 0; i < m; ++i) mean += w[i] * col[i];
+                col[m / 2] -= mean / w[m / 2];
+            }
+            const std::vector<cplx> y = S.apply(col.data());
+            for (int i = 0; i < m; ++i) as_c(Fd)[static_cast<size_t>(i) * n + kc] = y[i];
+        }
+    });
+}
+
+int sko_shgen(int m, int n, int L, const double* coeffs, double* phys, int threads) {
+    return guarded([&] {
+        const int rows = m / 2 + 1;
+        const int T = std::max(1, threads);
+        auto work = [&](int t) {
+            std::vector<double> P, A(2 * L + 1);
+            for (int p = t; p < rows; p += T) {
+                const double th = kTwoPi * p / m;
+                const double x = std::cos(th), s = std::sin(th);
+                std::fill(A.begin(), A.end(), 0.0);
+                for (int mm = 0; mm <= L; ++mm) {
+                    legendre_row(L, mm, x, s, P);
+                    for (int l = std::max(mm, 1); l <= L; ++l) {
+                        const double pl = P[l - mm];
+                        A[L + mm] += coeffs[static_cast<size_t>(l) * l + l + mm] * pl;
+                        if (mm > 0) A[L - mm] += coeffs[static_cast<size_t>(l) * l + l - mm] * pl;
+                    }
+                }
+                for (int q = 0; q < n; ++q) {
+                    double acc = A[L];
+                    for (int mm = 1; mm <= L; ++mm) {
+                        // m * lambda_q = m(-pi + 2 pi q/N): exact index reduction
+                        const long r = (static_cast<long>(mm) * q) % n;
+                        const double a = kTwoPi * static_cast<double>(r) / n;
+                        const double sg = (mm % 2 == 0) ? 1.0 : -1.0;
+                        acc += std::sqrt(2.0) * sg * (A[L + mm] * std::cos(a) + A[L - mm] * std::sin(a));
+                    }
+                    phys[static_cast<size_t>(p) * n + q] = acc;
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+    });
+}
+
+}  // extern "C"

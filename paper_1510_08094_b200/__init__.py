@@ -1,0 +1,11 @@
+"""B200-native DFS spectral Poisson solver on the unit sphere (sm_100a).
+
+The compute path is libsk_poisson.so (hand-written CUDA, C ABI declared in
+include/sk_poisson.h); this package is the host-side mirror of the
+reference's spherekit Poisson interface (poisson.hpp) on top of it.
+"""
+from .poisson import (  # noqa: F401
+    BenchRow, DeviceError, Plan, PoissonProblem, PoissonSolution, ResidualReport, UnsupportedError, bench_poisson,
+    integration_weights, precondition_error, residual, size_error, solve, solve_grid, structure_error)
+
+__version__ = "0.1.0"

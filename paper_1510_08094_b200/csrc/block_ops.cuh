@@ -1,0 +1,145 @@
+// Block-wide scans and reductions (warp shuffles + one shared-memory slot per
+// warp).  Used by the partitioned tridiagonal solve of the theta stage.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sk {
+
+struct V4 {
+    double a, b, c, d;
+};
+
+__device__ __forceinline__ V4 shfl_up4(V4 v, int delta) {
+    V4 r;
+    r.a = __shfl_up_sync(0xffffffffu, v.a, delta);
+    r.b = __shfl_up_sync(0xffffffffu, v.b, delta);
+    r.c = __shfl_up_sync(0xffffffffu, v.c, delta);
+    r.d = __shfl_up_sync(0xffffffffu, v.d, delta);
+    return r;
+}
+__device__ __forceinline__ V4 shfl_down4(V4 v, int delta) {
+    V4 r;
+    r.a = __shfl_down_sync(0xffffffffu, v.a, delta);
+    r.b = __shfl_down_sync(0xffffffffu, v.b, delta);
+    r.c = __shfl_down_sync(0xffffffffu, v.c, delta);
+    r.d = __shfl_down_sync(0xffffffffu, v.d, delta);
+    return r;
+}
+
+// Exclusive scan over the CTA in thread order (REV = false) or reverse thread
+// order (REV = true).  Op::combine(earlier, later) composes two elements,
+// Op::identity() is its neutral element.  blockDim.x must be a multiple of 32
+// and <= 1024; `wsc` needs 32 V4 slots.  Ends with a barrier.
+template <class Op, bool REV>
+__device__ V4 block_exclusive_scan(V4 v, V4* wsc) {
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int nw = nthr >> 5;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    // position of this thread in scan order
+    const int vlane = REV ? 31 - lane : lane;
+    const int vwarp = REV ? nw - 1 - warp : warp;
+    // inclusive warp scan in scan order
+    V4 inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const V4 o = REV ? shfl_down4(inc, off) : shfl_up4(inc, off);
+        if (vlane >= off) inc = Op::combine(o, inc);
+    }
+    if (vlane == 31) wsc[vwarp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        V4 t = lane < nw ? wsc[lane] : Op::identity();
+        // inclusive scan of warp totals (natural lane order = scan order here)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const V4 o = shfl_up4(t, off);
+            if (lane >= off) t = Op::combine(o, t);
+        }
+        // exclusive warp prefixes
+        const V4 prev = shfl_up4(t, 1);
+        if (lane < nw) wsc[lane] = lane == 0 ? Op::identity() : prev;
+    }
+    __syncthreads();
+    const V4 wpre = wsc[vwarp];
+    // exclusive within the warp
+    V4 ex = REV ? shfl_down4(inc, 1) : shfl_up4(inc, 1);
+    if (vlane == 0) ex = Op::identity();
+    const V4 res = Op::combine(wpre, ex);
+    __syncthreads();
+    return res;
+}
+
+// 2x2 Moebius matrices [[a, b], [c, d]]; later * earlier, rescaled.
+struct MobOp {
+    __device__ static V4 identity() { return V4{1.0, 0.0, 0.0, 1.0}; }
+    __device__ static V4 combine(V4 e, V4 l) {
+        V4 r{l.a * e.a + l.b * e.c, l.a * e.b + l.b * e.d, l.c * e.a + l.d * e.c, l.c * e.b + l.d * e.d};
+        const double m = fmax(fmax(fabs(r.a), fabs(r.b)), fmax(fabs(r.c), fabs(r.d)));
+        if (m > 0.0 && (m > 1e150 || m < 1e-150)) {
+            const double s = 1.0 / m;
+            r.a *= s;
+            r.b *= s;
+            r.c *= s;
+            r.d *= s;
+        }
+        return r;
+    }
+};
+
+// Affine maps x -> a x + (b + i c) with real a: later o earlier.
+struct AffOp {
+    __device__ static V4 identity() { return V4{1.0, 0.0, 0.0, 0.0}; }
+    __device__ static V4 combine(V4 e, V4 l) { return V4{l.a * e.a, fma(l.a, e.b, l.b), fma(l.a, e.c, l.c), 0.0}; }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+// Sum of (x, y) pairs over the CTA; result valid in every thread. `red` needs
+// 64 doubles.  Ends with a barrier.
+__device__ __forceinline__ double2 block_sum2(double2 v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    if (lane == 0) {
+        red[2 * warp] = v.x;
+        red[2 * warp + 1] = v.y;
+    }
+    __syncthreads();
+    double2 t = make_double2(0.0, 0.0);
+    for (int w = 0; w < nw; ++w) {
+        t.x += red[2 * w];
+        t.y += red[2 * w + 1];
+    }
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t = fmax(t, red[w]);
+    __syncthreads();
+    return t;
+}
+
+// atomic max of a non-negative double (IEEE order == unsigned order)
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace sk

@@ -1,0 +1,257 @@
+// Coefficient-space kernels (sm_100a), compiled with --fmad=false:
+//
+//   K5 coeff_solve — drop-in for spherekit::solve (poisson.cpp:121-161).
+//   K6 residual    — spherekit::residual (poisson.cpp:163-186).
+//   check_mean     — check_mean_zero (poisson.cpp:101-117).
+//
+// Layout: F, X row-major M x N complex (types.hpp:17-41); a lambda-mode column
+// is strided by N, so a warp owns 32 consecutive columns and every row access
+// of the warp is one contiguous 512-byte segment.
+//
+// Why four independent real recurrences reproduce the reference bit for bit:
+// lap (poisson.cpp:35-38) has exact-zero +-1 offsets and real entries, its
+// entries lap[+-2][0] and lap[+-1][-+1] are exact zeros, so for k != 0 the
+// system splits into the chains {even, odd} x {j < 0, j > 0} plus the row
+// j = 0, which couples x_0 to x_-2 and x_2 only.  The matrix is strictly
+// column diagonally dominant for k != 0, so band_solve's partial pivoting
+// (banded.cpp:121-133) never swaps and its elimination is the ascending Thomas
+// recurrence.  Each complex operation of the reference has a zero imaginary
+// part in the operator, so it decomposes into the real IEEE mul/sub/div used
+// here, in the same order and without FMA contraction.
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "params.h"
+
+namespace sk {
+
+
+// lap entries (exact dyadic values; see oracle/sk_oracle.cpp lap_band)
+__device__ __forceinline__ double lapc_lower(int i, int M) {  // lap[i][i-2]
+    const double j = i - M / 2;
+    return __dmul_rn(__dmul_rn(j - 2.0, j - 1.0), 0.25);
+}
+__device__ __forceinline__ double lapc_upper(int i, int M) {  // lap[i][i+2]
+    const double j = i - M / 2;
+    return __dmul_rn(__dmul_rn(j + 2.0, j + 1.0), 0.25);
+}
+__device__ __forceinline__ double lapc_diag(int i, int M) {
+    const double j = i - M / 2;
+    if (i == 0) return -__dmul_rn(__dmul_rn(j, j - 1.0), 0.25);
+    if (i == M - 1) return -__dmul_rn(__dmul_rn(j, j + 1.0), 0.25);
+    return -__dmul_rn(__dmul_rn(j, j), 0.5);
+}
+
+// warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0
+__global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
+    __shared__ double2 s_rm2[32];   // r'_{-2}
+    __shared__ double s_dm2[32];    // d'_{-2}
+    __shared__ double2 s_x2[32];    // x_2
+    const int M = P.M, N = P.N, h = M / 2;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int kc = blockIdx.x * 32 + lane;
+    const int rhs = blockIdx.y;
+    const bool live = kc < N;
+    const size_t off = static_cast<size_t>(rhs) * M * N;
+    const double2* F = P.F + off;
+    double2* X = P.X + off;
+    double* D = P.D + off;
+    const int k = kc - N / 2;
+    const double negk2 = __dmul_rn(-static_cast<double>(k), static_cast<double>(k));  // -static_cast<double>(k) * k
+    // chain rows (storage index i, ascending)
+    const int even_lo = (h & 1) ? 1 : 0;  // i with j = i - h even
+    int i0, i1;
+    if (w == 0) { i0 = even_lo; i1 = h - 2; }
+    else if (w == 1) { i0 = 1 - even_lo; i1 = h - 1; }
+    else if (w == 2) { i0 = h + 2; i1 = ((M - 1 - (h + 2)) / 2) * 2 + h + 2; }
+    else { i0 = h + 1; i1 = ((M - 1 - (h + 1)) / 2) * 2 + h + 1; }
+    if (i1 > M - 1) i1 -= 2;
+    double fmx = 0.0;
+    int bad = 0;
+    // ---- forward elimination: d'_i = b_i - (a_i/d'_{i-2}) c_{i-2}; r_i = F_i - l r_{i-2}
+    double dprev = 0.0;
+    double2 rprev = make_double2(0.0, 0.0);
+    if (live && i0 <= i1) {
+        for (int i = i0; i <= i1; i += 2) {
+            const double2 f = F[static_cast<size_t>(i) * N + kc];
+            fmx = fmax(fmx, hypot(f.x, f.y));
+            const double b = __dadd_rn(lapc_diag(i, M), negk2);
+            double d = b;
+            double2 r = f;
+            if (i > i0) {
+                const double a = lapc_lower(i, M);
+                if (a != 0.0) {
+                    if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
+                    const double l = __ddiv_rn(a, dprev);
+                    d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
+                    r = make_double2(__dsub_rn(f.x, __dmul_rn(l, rprev.x)), __dsub_rn(f.y, __dmul_rn(l, rprev.y)));
+                }
+            }
+            if (fabs(d) < 1e-300) bad += 1 << 20;
+            X[static_cast<size_t>(i) * N + kc] = r;
+            D[static_cast<size_t>(i) * N + kc] = d;
+            dprev = d;
+            rprev = r;
+        }
+    }
+    if (w == 0 && live) {
+        s_rm2[lane] = rprev;  // chain ends at j = -2
+        s_dm2[lane] = dprev;
+    }
+    // ---- back substitution: x_i = (r_i - c_i x_{i+2}) / d'_i
+    double2 xnext = make_double2(0.0, 0.0);
+    if (live && i0 <= i1) {
+        for (int i = i1; i >= i0; i -= 2) {
+            const double2 r = X[static_cast<size_t>(i) * N + kc];
+            const double d = D[static_cast<size_t>(i) * N + kc];
+            double2 acc = r;
+            if (i + 2 <= M - 1) {
+                const double c = lapc_upper(i, M);
+                if (c != 0.0)
+                    acc = make_double2(__dsub_rn(acc.x, __dmul_rn(c, xnext.x)), __dsub_rn(acc.y, __dmul_rn(c, xnext.y)));
+            }
+            const double2 x = make_double2(__ddiv_rn(acc.x, d), __ddiv_rn(acc.y, d));
+            X[static_cast<size_t>(i) * N + kc] = x;
+            xnext = x;
+        }
+    }
+    if (w == 2 && live) s_x2[lane] = xnext;  // chain starts at j = 2
+    __syncthreads();
+    // ---- row j = 0
+    if (w == 0 && live) {
+        const double2 f0 = F[static_cast<size_t>(h) * N + kc];
+        fmx = fmax(fmx, hypot(f0.x, f0.y));
+        const bool has_m2 = (h - 2) >= 0;
+        const bool has_p2 = (h + 2) <= M - 1;
+        if (k != 0) {
+            double2 r0 = f0;
+            if (has_m2) {  // eliminate with pivot row j = -2: f = lap[0][-2] / d'_{-2}
+                const double l = __ddiv_rn(lapc_lower(h, M), s_dm2[lane]);
+                r0 = make_double2(__dsub_rn(r0.x, __dmul_rn(l, s_rm2[lane].x)), __dsub_rn(r0.y, __dmul_rn(l, s_rm2[lane].y)));
+            }
+            if (has_p2) {
+                const double c = lapc_upper(h, M);
+                r0 = make_double2(__dsub_rn(r0.x, __dmul_rn(c, s_x2[lane].x)), __dsub_rn(r0.y, __dmul_rn(c, s_x2[lane].y)));
+            }
+            const double d0 = __dadd_rn(lapc_diag(h, M), negk2);
+            X[static_cast<size_t>(h) * N + kc] = make_double2(__ddiv_rn(r0.x, d0), __ddiv_rn(r0.y, d0));
+        }
+    }
+    __syncthreads();
+    if (k == 0 && live && w == 0) {
+        // constraint row 2 pi w^T X_0 = 0 replaces row j = 0:
+        // x_0 = -(sum_{j != 0, j even} w_j x_j) / w_0, w_j = 2 / (1 - j^2)
+        double2 s = make_double2(0.0, 0.0);
+        for (int i = even_lo; i < M; i += 2) {
+            if (i == h) continue;
+            const double j = i - h;
+            const double wj = 2.0 / (1.0 - j * j);
+            const double2 x = X[static_cast<size_t>(i) * N + kc];
+            s = make_double2(__dadd_rn(s.x, __dmul_rn(wj, x.x)), __dadd_rn(s.y, __dmul_rn(wj, x.y)));
+        }
+        X[static_cast<size_t>(h) * N + kc] = make_double2(-__ddiv_rn(s.x, 2.0), -__ddiv_rn(s.y, 2.0));
+    }
+    // stats
+    const double fm = warp_max(live ? fmx : 0.0);
+    if (lane == 0) atomic_max_nonneg(P.stats + 4 * rhs + 2, fm);
+    if (bad) atomicAdd(P.stats + 4 * rhs + 3, static_cast<double>(bad));
+}
+
+// check_mean_zero (poisson.cpp:101-117): the reference computes
+// 2 pi w^T div_sin(div_sin(F_0)); with Msin^T = -Msin this equals
+// 2 pi z^T F_0 for z = Msin^-1 Msin^-1 w, precomputed per plan.
+__global__ void __launch_bounds__(256) mean_kernel(CoeffParams P) {
+    __shared__ double red[64];
+    const int rhs = blockIdx.x;
+    const double2* F = P.F + static_cast<size_t>(rhs) * P.M * P.N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < P.M; i += blockDim.x) {
+        const double2 f = F[static_cast<size_t>(i) * P.N + P.N / 2];
+        const double2 z = P.z[i];
+        acc.x += z.x * f.x - z.y * f.y;
+        acc.y += z.x * f.y + z.y * f.x;
+    }
+    acc = block_sum2(acc, red);
+    if (threadIdx.x == 0) {
+        const double twopi = 6.283185307179586476925286766559;
+        P.stats[4 * rhs + 0] = twopi * acc.x;
+        P.stats[4 * rhs + 1] = twopi * acc.y;
+    }
+}
+
+
+// residual (poisson.cpp:163-186): r = lap x_k - (k^2 x_k + F_k) per column.
+__global__ void __launch_bounds__(128) residual_kernel(ResidualParams P) {
+    const int M = P.M, N = P.N, h = M / 2;
+    const int kc = blockIdx.x * blockDim.x + threadIdx.x;
+    double imax = 0.0;
+    if (kc < N) {
+        const double k = kc - N / 2;
+        const double k2 = k * k;
+        double2 xw[5];  // x_{i-2} .. x_{i+2}
+        for (int q = 0; q < 5; ++q) {
+            const int i = q - 2;
+            xw[q] = (i >= 0 && i < M) ? P.X[static_cast<size_t>(i) * N + kc] : make_double2(0.0, 0.0);
+        }
+        double2 wsum = make_double2(0.0, 0.0);
+        for (int i = 0; i < M; ++i) {
+            double2 r = make_double2(0.0, 0.0);
+            if (i - 2 >= 0) {
+                const double a = lapc_lower(i, M);
+                r.x += a * xw[0].x;
+                r.y += a * xw[0].y;
+            }
+            {
+                const double b = lapc_diag(i, M);
+                r.x += b * xw[2].x;
+                r.y += b * xw[2].y;
+            }
+            if (i + 2 < M) {
+                const double c = lapc_upper(i, M);
+                r.x += c * xw[4].x;
+                r.y += c * xw[4].y;
+            }
+            const double2 f = P.F[static_cast<size_t>(i) * N + kc];
+            r.x -= k2 * xw[2].x + f.x;
+            r.y -= k2 * xw[2].y + f.y;
+            const double ab = hypot(r.x, r.y);
+            if (kc == N / 2 && i == h) {
+                P.out[1] = ab;
+            } else {
+                imax = fmax(imax, ab);
+            }
+            if (kc == N / 2) {
+                const int j = i - h;
+                if ((j & 1) == 0) {
+                    const double wj = 2.0 / (1.0 - static_cast<double>(j) * j);
+                    wsum.x += wj * xw[2].x;
+                    wsum.y += wj * xw[2].y;
+                }
+            }
+            for (int q = 0; q < 4; ++q) xw[q] = xw[q + 1];
+            xw[4] = (i + 3 < M) ? P.X[static_cast<size_t>(i + 3) * N + kc] : make_double2(0.0, 0.0);
+        }
+        if (kc == N / 2) {
+            P.out[2] = wsum.x;
+            P.out[3] = wsum.y;
+        }
+    }
+    const double m = warp_max(imax);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(P.out, m);
+}
+
+cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st) {
+    if (P.z) {
+        mean_kernel<<<P.nrhs, 256, 0, st>>>(P);
+    }
+    dim3 grid((P.N + 31) / 32, P.nrhs);
+    coeff_solve_kernel<<<grid, 128, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st) {
+    residual_kernel<<<(P.N + 127) / 128, 128, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

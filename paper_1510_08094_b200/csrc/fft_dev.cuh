@@ -1,0 +1,241 @@
+// Device-side FFT engine: in-place mixed-radix Cooley-Tukey in shared memory.
+//
+// Replaces the FFTW calls of fourier.cpp:22-35 (run_fft, one plan per 1D
+// transform under a global mutex).  Here a whole CTA transforms one sequence
+// resident in shared memory: forward stages are decimation-in-frequency
+// (natural order in, digit-reversed out), inverse stages decimation-in-time
+// (digit-reversed in, natural out), so a forward + pointwise/solve + inverse
+// sequence never needs a reordering pass.  Each butterfly reads and writes the
+// same R slots, so stages need no ping-pong buffer and only R complex values
+// per thread live in registers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "sk_internal.h"
+
+namespace sk {
+
+struct cd {
+    double x, y;
+};
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
+// multiply by (sign * i)
+template <int SIGN>
+__device__ __forceinline__ double2 mul_si(double2 a) {
+    return SIGN < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+// Twiddle table access (exp(-2 pi i m / 2L)), tables staged in shared memory.
+struct Tw {
+    const double2* hi;
+    const double2* lo;
+    int shift;
+    int mask;
+    __device__ __forceinline__ double2 operator()(int m) const { return cmul(hi[m >> shift], lo[m & mask]); }
+};
+
+// ---------------------------------------------------------------- radix DFTs
+// y_s = sum_q x_q exp(SIGN 2 pi i q s / R), in place.
+template <int SIGN>
+__device__ __forceinline__ void dft2(double2* x) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(double2* x) {
+    const double2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+    const double2 t2 = cadd(x[1], x[3]), t3 = mul_si<SIGN>(csub(x[1], x[3]));
+    x[0] = cadd(t0, t2);
+    x[2] = csub(t0, t2);
+    x[1] = cadd(t1, t3);
+    x[3] = csub(t1, t3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft8(double2* x) {
+    constexpr double r = 0.70710678118654752440084436210484903928;
+    double2 e[4] = {x[0], x[2], x[4], x[6]};
+    double2 o[4] = {x[1], x[3], x[5], x[7]};
+    dft4<SIGN>(e);
+    dft4<SIGN>(o);
+    // W^1 = r (1 + SIGN i), W^2 = SIGN i, W^3 = r (-1 + SIGN i)
+    const double2 w1o = make_double2(r * (o[1].x - SIGN * o[1].y), r * (o[1].y + SIGN * o[1].x));
+    const double2 w2o = mul_si<SIGN>(o[2]);
+    const double2 w3o = make_double2(r * (-o[3].x - SIGN * o[3].y), r * (-o[3].y + SIGN * o[3].x));
+    x[0] = cadd(e[0], o[0]);
+    x[4] = csub(e[0], o[0]);
+    x[1] = cadd(e[1], w1o);
+    x[5] = csub(e[1], w1o);
+    x[2] = cadd(e[2], w2o);
+    x[6] = csub(e[2], w2o);
+    x[3] = cadd(e[3], w3o);
+    x[7] = csub(e[3], w3o);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft3(double2* x) {
+    constexpr double s3 = 0.86602540378443864676372317075293618347;  // sin(2pi/3)
+    const double2 t1 = cadd(x[1], x[2]);
+    const double2 t2 = make_double2(x[0].x - 0.5 * t1.x, x[0].y - 0.5 * t1.y);
+    const double2 t3 = mul_si<SIGN>(cscale(csub(x[1], x[2]), s3));
+    x[0] = cadd(x[0], t1);
+    x[1] = cadd(t2, t3);
+    x[2] = csub(t2, t3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft5(double2* x) {
+    constexpr double c1 = 0.30901699437494742410229341718281905886;   // cos(2pi/5)
+    constexpr double c2 = -0.80901699437494742410229341718281905886;  // cos(4pi/5)
+    constexpr double s1 = 0.95105651629515357211643933337938214340;   // sin(2pi/5)
+    constexpr double s2 = 0.58778525229247312916870595463907276860;   // sin(4pi/5)
+    const double2 t1 = cadd(x[1], x[4]), t2 = cadd(x[2], x[3]);
+    const double2 t3 = csub(x[1], x[4]), t4 = csub(x[2], x[3]);
+    const double2 a1 = make_double2(x[0].x + c1 * t1.x + c2 * t2.x, x[0].y + c1 * t1.y + c2 * t2.y);
+    const double2 a2 = make_double2(x[0].x + c2 * t1.x + c1 * t2.x, x[0].y + c2 * t1.y + c1 * t2.y);
+    const double2 b1 = mul_si<SIGN>(make_double2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y));
+    const double2 b2 = mul_si<SIGN>(make_double2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y));
+    x[0] = make_double2(x[0].x + t1.x + t2.x, x[0].y + t1.y + t2.y);
+    x[1] = cadd(a1, b1);
+    x[4] = csub(a1, b1);
+    x[2] = cadd(a2, b2);
+    x[3] = csub(a2, b2);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft7(double2* x) {
+    // c[q][s] = cos(2 pi q s / 7), sn[q][s] = sin(2 pi q s / 7), q,s = 1..3
+    constexpr double C1 = 0.62348980185873353052500488400423981063;
+    constexpr double C2 = -0.22252093395631440428890256449679475947;
+    constexpr double C3 = -0.90096886790241912623610231950744505116;
+    constexpr double S1 = 0.78183148246802980870844452667405775023;
+    constexpr double S2 = 0.97492791218182360701813168299393121723;
+    constexpr double S3 = 0.43388373911755812047576833284835875461;
+    const double2 p1 = cadd(x[1], x[6]), p2 = cadd(x[2], x[5]), p3 = cadd(x[3], x[4]);
+    const double2 m1 = csub(x[1], x[6]), m2 = csub(x[2], x[5]), m3 = csub(x[3], x[4]);
+    const double2 x0 = x[0];
+    auto A = [&](double a, double b, double c) {
+        return make_double2(x0.x + a * p1.x + b * p2.x + c * p3.x, x0.y + a * p1.y + b * p2.y + c * p3.y);
+    };
+    auto B = [&](double a, double b, double c) {
+        return mul_si<SIGN>(make_double2(a * m1.x + b * m2.x + c * m3.x, a * m1.y + b * m2.y + c * m3.y));
+    };
+    const double2 a1 = A(C1, C2, C3), b1 = B(S1, S2, S3);
+    const double2 a2 = A(C2, C3, C1), b2 = B(S2, -S3, -S1);
+    const double2 a3 = A(C3, C1, C2), b3 = B(S3, -S1, S2);
+    x[0] = make_double2(x0.x + p1.x + p2.x + p3.x, x0.y + p1.y + p2.y + p3.y);
+    x[1] = cadd(a1, b1);
+    x[6] = csub(a1, b1);
+    x[2] = cadd(a2, b2);
+    x[5] = csub(a2, b2);
+    x[3] = cadd(a3, b3);
+    x[4] = csub(a3, b3);
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(double2* x) {
+    if constexpr (R == 2) dft2<SIGN>(x);
+    else if constexpr (R == 3) dft3<SIGN>(x);
+    else if constexpr (R == 4) dft4<SIGN>(x);
+    else if constexpr (R == 5) dft5<SIGN>(x);
+    else if constexpr (R == 7) dft7<SIGN>(x);
+    else dft8<SIGN>(x);
+}
+
+// ------------------------------------------------------------------- stages
+// Forward DIF stage: x_q = a[base + q span]; y = DFT_R(x); y_q *= w^(q j).
+template <int R>
+__device__ __forceinline__ void dif_stage(double2* a, int L, int span, int tw, const Tw& T, int tid, int nthr) {
+    const int nb = L / R;
+    for (int b = tid; b < nb; b += nthr) {
+        const int g = b / span;
+        const int j = b - g * span;
+        const int base = g * span * R + j;
+        double2 x[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = a[base + q * span];
+        dft<R, -1>(x);
+        a[base] = x[0];
+        const int step = j * tw;
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+            const double2 w = T(q * step);
+            a[base + q * span] = j == 0 ? x[q] : cmul(x[q], w);
+        }
+    }
+}
+
+// Inverse DIT stage: x_q = a[base + q span] * conj(w)^(q j); y = DFT^+_R(x).
+template <int R>
+__device__ __forceinline__ void dit_stage(double2* a, int L, int span, int tw, const Tw& T, int tid, int nthr) {
+    const int nb = L / R;
+    for (int b = tid; b < nb; b += nthr) {
+        const int g = b / span;
+        const int j = b - g * span;
+        const int base = g * span * R + j;
+        double2 x[R];
+        x[0] = a[base];
+        const int step = j * tw;
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+            const double2 v = a[base + q * span];
+            x[q] = j == 0 ? v : cmulc(v, T(q * step));
+        }
+        dft<R, +1>(x);
+#pragma unroll
+        for (int q = 0; q < R; ++q) a[base + q * span] = x[q];
+    }
+}
+
+// Whole transforms; callers must __syncthreads() before (data ready) — the
+// routines end with a barrier.
+__device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
+    for (int s = 0; s < d.nst; ++s) {
+        switch (d.R[s]) {
+            case 2: dif_stage<2>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 3: dif_stage<3>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 4: dif_stage<4>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 5: dif_stage<5>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 7: dif_stage<7>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            default: dif_stage<8>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
+    for (int s = d.nst - 1; s >= 0; --s) {
+        switch (d.R[s]) {
+            case 2: dit_stage<2>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 3: dit_stage<3>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 4: dit_stage<4>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 5: dit_stage<5>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 7: dit_stage<7>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            default: dit_stage<8>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+        }
+        __syncthreads();
+    }
+}
+
+// Stage the 2L-th-root twiddle tables of `d` into shared memory.
+__device__ __forceinline__ Tw load_tw(const FftDesc& d, double2* s_hi, double2* s_lo, int tid, int nthr) {
+    for (int i = tid; i < d.nhi; i += nthr) s_hi[i] = d.hi[i];
+    for (int i = tid; i < d.nlo; i += nthr) s_lo[i] = d.lo[i];
+    return Tw{s_hi, s_lo, d.shift, (1 << d.shift) - 1};
+}
+
+}  // namespace sk

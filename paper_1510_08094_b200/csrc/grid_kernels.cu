@@ -1,0 +1,530 @@
+// Grid-path kernels of the DFS spectral Poisson solve (sm_100a).
+//
+//   K1 lambda_fwd  — DFS doubling + forward lambda transform of each physical
+//                    row (replaces sample_dfs sphere_domain.cpp:46-52 and the
+//                    row stage of analyze_2d fourier.cpp:181-186);
+//   K3 theta_stage — per lambda mode: theta transform (column stage of
+//                    analyze_2d :174-180), Msin^2 (poisson.cpp:61-71), the
+//                    banded solve with the k=0 constraint (solve :121-161,
+//                    band_solve banded.cpp:101-158, band_solve_with_dense_row
+//                    :160-328), inverse theta transform (sample_grid :194-200);
+//   K4 lambda_inv  — inverse lambda transform per physical row (sample_grid
+//                    :202-207);
+//   K7 shgen       — seeded spherical-harmonic input generator (untimed).
+//
+// Data in HBM between the kernels is the half spectrum S[k][p], k = 0..N/2
+// (real data: the k < 0 half is its Hermitian mirror), p = 0..M/2 (physical
+// rows only: the doubled rows j < M/2 are (-1)^k times row M/2-j in lambda-
+// spectral space, so the doubled grid is never stored).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "fft_dev.cuh"
+#include "params.h"
+#include "sk_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace sk {
+
+// ------------------------------------------------------------------ layout
+// Element (kl, p) of a lambda-mode column on the theta rank: pieces from each
+// source rank s are [kl][p - row_b[s]] blocks of ncols x rows_s, concatenated.
+__device__ __forceinline__ size_t theta_addr(const Slabs& sl, int ncols, int kl, int p) {
+    int s = 0;
+    while (s + 1 < sl.P && p >= sl.row_b[s + 1]) ++s;
+    const int r0 = sl.row_b[s];
+    const int rows_s = sl.row_b[s + 1] - r0;
+    return static_cast<size_t>(ncols) * r0 + static_cast<size_t>(kl) * rows_s + (p - r0);
+}
+
+
+// One CTA per physical row: load the real row as N/2 complex pairs, forward
+// DIF FFT, split into the N/2+1 modes of the real transform, apply
+// analyze_1d's (-1)^k / N (fourier.cpp:44-51), store transposed.
+__global__ void __launch_bounds__(512) lambda_fwd_kernel(LambdaParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = P.fd.L;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + L;
+    double2* s_lo = s_hi + P.fd.nhi;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int row = blockIdx.x % P.rows_local;
+    const int rhs = blockIdx.x / P.rows_local;
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    const double2* src =
+        reinterpret_cast<const double2*>(P.f + rhs * P.in_rhs_stride + static_cast<long long>(row) * P.g.N);
+    for (int j = tid; j < L; j += nthr) a[j] = __ldg(src + j);
+    __syncthreads();
+    fft_forward(a, P.fd, T, tid, nthr);
+    const double invN = 1.0 / P.g.N;
+    double2* out = P.spec + rhs * P.out_rhs_stride;
+    const int* rev = P.fd.rev;
+    for (int k = tid; k <= L / 2; k += nthr) {
+        const int km = L - k;  // partner mode
+        const double2 z = a[__ldg(rev + k)];
+        const double2 zp = a[__ldg(rev + (km == L ? 0 : km))];
+        // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
+        const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
+        const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
+        const double2 Xk = cadd(A, cmul(T(k), B));
+        const double2 Xm = cadd(conjd(A), cmul(T(km), conjd(B)));
+        const double sk = (k & 1) ? -invN : invN;
+        const double sm = (km & 1) ? -invN : invN;
+        out[static_cast<size_t>(k) * P.rows_local + row] = cscale(Xk, sk);
+        if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = cscale(Xm, sm);
+    }
+}
+
+// Inverse: gather the N/2+1 modes of a physical row, apply sample_grid's
+// (-1)^k (fourier.cpp:61-62), pack into N/2 complex, inverse DIT FFT, store
+// the real row (unnormalised backward transform, as FFTW_BACKWARD).
+__global__ void __launch_bounds__(512) lambda_inv_kernel(LambdaParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = P.fd.L;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + L;
+    double2* s_lo = s_hi + P.fd.nhi;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int row = blockIdx.x % P.rows_local;
+    const int rhs = blockIdx.x / P.rows_local;
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    const double2* in = P.spec + rhs * P.in_rhs_stride;
+    const int* rev = P.fd.rev;
+    for (int k = tid; k <= L / 2; k += nthr) {
+        const int km = L - k;
+        double2 v = in[static_cast<size_t>(k) * P.rows_local + row];
+        double2 w = in[static_cast<size_t>(km) * P.rows_local + row];
+        if (k & 1) v = make_double2(-v.x, -v.y);
+        if (km & 1) w = make_double2(-w.x, -w.y);
+        if (k == 0) {  // DC and Nyquist of a real signal are real
+            v.y = 0.0;
+            w.y = 0.0;
+        }
+        // Z_k = E_k + i O_k, E_k = V_k + conj V_{L-k}, O_k = (V_k - conj V_{L-k}) conj(T(k))
+        {
+            const double2 E = make_double2(v.x + w.x, v.y - w.y);
+            const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
+            a[__ldg(rev + k)] = make_double2(E.x - O.y, E.y + O.x);
+        }
+        if (k != 0 && km != k) {
+            const double2 E = make_double2(w.x + v.x, w.y - v.y);
+            const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
+            a[__ldg(rev + km)] = make_double2(E.x - O.y, E.y + O.x);
+        }
+    }
+    __syncthreads();
+    fft_inverse(a, P.fd, T, tid, nthr);
+    double2* dst = reinterpret_cast<double2*>(P.u + rhs * P.out_rhs_stride + static_cast<long long>(row) * P.g.N);
+    for (int j = tid; j < L; j += nthr) dst[j] = a[j];
+}
+
+// -------------------------------------------------------------- theta stage
+
+// theta-mode index of natural FFT index tau in parity class par (t = 2 tau + par
+// folded into [-M/2, M/2)).
+__device__ __forceinline__ int t_of(int tau, int par, int L) {
+    const int t = 2 * tau + par;
+    return t < L ? t : t - 2 * L;
+}
+
+struct Chain {
+    int n;       // length
+    int tau0;    // natural FFT index of element 0
+    int dtau;    // +1 (t > 0 chain) or -1 (t < 0 chain)
+    int t0;      // theta mode of element 0
+    int dt;      // +2 or -2
+};
+
+// Coefficients of row t of (lap - k^2) (poisson.cpp:15-40 closed form; the
+// +-1 offsets are exact zeros): lower = lap[t][t-2], upper = lap[t][t+2].
+__device__ __forceinline__ double lap_lower(int t, int L) {
+    return (t - 2 >= -L) ? (double)(t - 2) * (double)(t - 1) * 0.25 : 0.0;
+}
+__device__ __forceinline__ double lap_upper(int t, int L) {
+    return (t + 2 <= L - 1) ? (double)(t + 2) * (double)(t + 1) * 0.25 : 0.0;
+}
+__device__ __forceinline__ double lap_diag(int t, int L) {
+    const double tt = t;
+    if (t == -L) return -tt * (tt - 1.0) * 0.25;
+    if (t == L - 1) return -tt * (tt + 1.0) * 0.25;
+    return -tt * tt * 0.5;
+}
+// Msin^2 diagonal (poisson.cpp:61; 1/4 on the first and last rows)
+__device__ __forceinline__ double msin2_diag(int t, int L) { return (t == -L || t == L - 1) ? 0.25 : 0.5; }
+
+// Solves one chain of the per-mode system in place.  The chain's rows are
+// a_i x_{i-1} + b_i x_i + c_i x_{i+1} = F_i with F = Msin^2 X computed on the
+// fly from the transform output.  Each thread owns a contiguous segment; the
+// Thomas recurrences (pivots d'_i, forward r'_i, backward x_i) are evaluated
+// as segment-local passes joined by three block scans (Moebius composition of
+// the pivot recurrence, affine compositions of the two sweeps), so the result
+// equals a sequential Thomas sweep up to rounding.
+__device__ void solve_chain(double2* a, const int* rev, double* inv, V4* wsc, const Chain& ch, int L, double k2,
+                            double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int n = ch.n;
+    const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
+    const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
+    const bool up = ch.dt > 0;
+    auto tt = [&](int i) { return ch.t0 + ch.dt * i; };
+    auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
+    auto A = [&](int i) { return up ? lap_lower(tt(i), L) : lap_upper(tt(i), L); };
+    auto C = [&](int i) { return (i < 0) ? 0.0 : (up ? lap_upper(tt(i), L) : lap_lower(tt(i), L)); };
+    auto B = [&](int i) { return lap_diag(tt(i), L) - k2; };
+    // boundary neighbours (original transform values) before anyone writes
+    double2 xlo = make_double2(0.0, 0.0), xhi = make_double2(0.0, 0.0);
+    if (s < e) {
+        xlo = (s == 0) ? inner : a[pos(s - 1)];
+        xhi = (e < n) ? a[pos(e)] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+
+    // ---- pass A: Moebius product of the pivot recurrence over the segment
+    V4 mob = MobOp::identity();
+    for (int i = s; i < e; ++i) {
+        const V4 Mi{B(i), -A(i) * C(i - 1), 1.0, 0.0};
+        mob = MobOp::combine(mob, Mi);
+    }
+    const V4 min = block_exclusive_scan<MobOp, false>(mob, wsc);
+    // state [p; q] = min * [1; 0]; 1/d'_{s-1} = q / p
+    double inv_prev = (min.a != 0.0) ? min.c / min.a : 0.0;
+
+    // ---- pass B: pivots (stored as reciprocals) and the local forward sweep
+    auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
+        const int t = tt(i);
+        const double d2 = msin2_diag(t, L);
+        return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+    };
+    V4 aff = AffOp::identity();
+    {
+        double2 xm = xlo;
+        double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
+        double ip = inv_prev;
+        for (int i = s; i < e; ++i) {
+            const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
+            const double2 F = Fof(xm, x0, xp, i);
+            const double d = B(i) - A(i) * C(i - 1) * ip;
+            const double iv = 1.0 / d;
+            inv[i] = iv;
+            const double al = -A(i) * ip;
+            aff = AffOp::combine(aff, V4{al, F.x, F.y, 0.0});
+            ip = iv;
+            xm = x0;
+            x0 = xp;
+        }
+    }
+    const V4 rin = block_exclusive_scan<AffOp, false>(aff, wsc);  // r'_{s-1} = rin.(b, c)
+
+    // ---- pass C: forward sweep with the true incoming value, r' in place
+    double2 bsum_x = make_double2(0.0, 0.0);
+    {
+        double2 rp = make_double2(rin.b, rin.c);
+        double ip = (s > 0) ? inv[s - 1] : 0.0;
+        double2 xm = xlo;
+        double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
+        for (int i = s; i < e; ++i) {
+            const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
+            const double2 F = Fof(xm, x0, xp, i);
+            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+            const double al = -A(i) * ip;
+            rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
+            a[pos(i)] = rp;
+            ip = inv[i];
+            xm = x0;
+            x0 = xp;
+        }
+    }
+    __syncthreads();
+
+    // ---- pass D: local backward summary x_s = P x_e + xt
+    V4 baff = AffOp::identity();
+    for (int i = e - 1; i >= s; --i) {
+        const double iv = inv[i];
+        const double2 r = a[pos(i)];
+        baff = AffOp::combine(baff, V4{-C(i) * iv, r.x * iv, r.y * iv, 0.0});
+    }
+    const V4 xin = block_exclusive_scan<AffOp, true>(baff, wsc);  // x_e
+
+    // ---- pass E: back substitution, x in place
+    {
+        double2 x = make_double2(xin.b, xin.c);
+        for (int i = e - 1; i >= s; --i) {
+            const double iv = inv[i];
+            const double2 r = a[pos(i)];
+            const double c = -C(i) * iv;
+            x = make_double2(fma(c, x.x, r.x * iv), fma(c, x.y, r.y * iv));
+            a[pos(i)] = x;
+            if (want_wsum) {
+                const double t = tt(i);
+                const double w = 2.0 / (1.0 - t * t);
+                bsum_x.x = fma(w, x.x, bsum_x.x);
+                bsum_x.y = fma(w, x.y, bsum_x.y);
+            }
+            if (i == 0) *x_first = x;
+        }
+    }
+    wsum.x += bsum_x.x;
+    wsum.y += bsum_x.y;
+    __syncthreads();
+}
+
+
+// One 2-CTA cluster per lambda mode k: CTA `par` (0/1) owns the theta modes
+// of parity par.  Folding the DFS-symmetric column onto the two parity
+// classes is the first radix-2 step of the length-M theta transform; each CTA
+// then runs a length-M/2 transform, the chains of its parity (the +-1 band
+// offsets of lap are exact zeros, so even and odd modes never couple), and the
+// inverse transform.  The two halves are recombined through distributed
+// shared memory.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(ThetaParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int L = P.fd.L;  // M/2
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + L;
+    double2* s_lo = s_hi + P.fd.nhi;
+    double* inv = reinterpret_cast<double*>(s_lo + P.fd.nlo);
+    V4* wsc = reinterpret_cast<V4*>(inv + (L / 2 + 2));
+    double2* misc = reinterpret_cast<double2*>(wsc + 32);
+    double* red = reinterpret_cast<double*>(misc + 16);
+
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int par = static_cast<int>(cluster.block_rank());
+    const int col = blockIdx.x >> 1;
+    const int rhs = col / P.ncols;
+    const int kl = col - rhs * P.ncols;
+    const int kg = P.k0 + kl;  // global lambda mode, 0..N/2
+    const double k2 = static_cast<double>(kg) * static_cast<double>(kg);
+    const double sgn = (kg & 1) ? -1.0 : 1.0;
+    const int* rev = P.fd.rev;
+    double2* colbase = P.buf + rhs * P.rhs_stride;
+
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    __syncthreads();
+
+    // ---- load + DFS fold (first radix-2 step), scaled by 1/M
+    const double invM = 1.0 / P.g.M;
+    for (int r = tid; r <= L / 2; r += nthr) {
+        const int rm = L - r;
+        const double2 ar = colbase[theta_addr(P.sl, P.ncols, kl, r)];
+        const double2 am = colbase[theta_addr(P.sl, P.ncols, kl, rm)];
+        if (par == 0) {
+            // e_r = a_r + s a_{L-r}
+            a[r] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
+            if (rm < L && rm != r) a[rm] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
+        } else {
+            // o_r = (a_r - s a_{L-r}) w_M^{-r}
+            a[r] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
+            if (rm < L && rm != r)
+                a[rm] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
+        }
+    }
+    __syncthreads();
+    fft_forward(a, P.fd, T, tid, nthr);
+
+    // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
+    double* st = P.stats + 4 * rhs;
+    if (kg == 0 && par == 0) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int tau = tid; tau < L; tau += nthr) {
+            const double t = t_of(tau, 0, L);
+            const double w = 2.0 / (1.0 - t * t);
+            const double2 x = a[__ldg(rev + tau)];
+            acc.x = fma(w, x.x, acc.x);
+            acc.y = fma(w, x.y, acc.y);
+        }
+        acc = block_sum2(acc, red);
+        if (tid == 0) {
+            const double twopi = 6.283185307179586476925286766559;
+            st[0] = twopi * acc.x;
+            st[1] = twopi * acc.y;
+        }
+    }
+
+    // ---- chains
+    Chain cp, cm;
+    if (par == 0) {
+        cp = Chain{(L - 1 >= 2) ? (L - 1 - 2) / 2 + 1 : 0, 1, +1, 2, +2};
+        cm = Chain{(L >= 2) ? (L - 2) / 2 + 1 : 0, L - 1, -1, -2, -2};
+    } else {
+        cp = Chain{(L - 1 >= 1) ? (L - 1 - 1) / 2 + 1 : 0, 0, +1, 1, +2};
+        cm = Chain{(L >= 1) ? (L - 1) / 2 + 1 : 0, L - 1, -1, -1, -2};
+    }
+    // inner neighbours and the j = 0 row data, read before any chain writes
+    if (tid == 0) {
+        if (par == 0) {
+            const double2 x0 = a[__ldg(rev + 0)];
+            const double2 xp2 = cp.n > 0 ? a[__ldg(rev + 1)] : make_double2(0.0, 0.0);
+            const double2 xm2 = cm.n > 0 ? a[__ldg(rev + L - 1)] : make_double2(0.0, 0.0);
+            misc[0] = x0;
+            misc[1] = x0;
+            // F_0 = -1/4 X_{-2} + d2(0) X_0 - 1/4 X_2
+            const double d2 = msin2_diag(0, L);
+            misc[2] = make_double2(d2 * x0.x - 0.25 * (xm2.x + xp2.x), d2 * x0.y - 0.25 * (xm2.y + xp2.y));
+        } else {
+            misc[0] = cm.n > 0 ? a[__ldg(rev + L - 1)] : make_double2(0.0, 0.0);  // X_{-1}: inner of t>0 chain
+            misc[1] = cp.n > 0 ? a[__ldg(rev + 0)] : make_double2(0.0, 0.0);      // X_{+1}: inner of t<0 chain
+            misc[2] = make_double2(0.0, 0.0);
+        }
+        misc[3] = make_double2(0.0, 0.0);
+        misc[4] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const double2 inner_p = misc[0], inner_m = misc[1], F0 = misc[2];
+    double fmax_acc = (par == 0) ? sqrt(F0.x * F0.x + F0.y * F0.y) : 0.0;
+    double2 wsum = make_double2(0.0, 0.0);
+    const bool want_wsum = (kg == 0 && par == 0);
+    __syncthreads();
+    solve_chain(a, rev, inv, wsc, cp, L, k2, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    solve_chain(a, rev, inv, wsc, cm, L, k2, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    if (want_wsum) wsum = block_sum2(wsum, red);
+    if (par == 0 && tid == 0) {
+        double2 x0;
+        if (kg != 0) {
+            // row j = 0: 1/2 x_{-2} - k^2 x_0 + 1/2 x_2 = F_0
+            const double2 xp2 = misc[3], xm2 = misc[4];
+            x0 = make_double2((F0.x - 0.5 * xm2.x - 0.5 * xp2.x) / (-k2), (F0.y - 0.5 * xm2.y - 0.5 * xp2.y) / (-k2));
+        } else {
+            // constraint row 2 pi w^T X_0 = 0 replaces row j = 0 (w_0 = 2)
+            x0 = make_double2(-0.5 * wsum.x, -0.5 * wsum.y);
+        }
+        a[__ldg(rev + 0)] = x0;
+    }
+    const double fm = block_max(fmax_acc, red);
+    if (tid == 0) atomic_max_nonneg(st + 2, fm);
+    __syncthreads();
+
+    // optional: export the solution coefficients of this parity class
+    if (P.xhalf) {
+        double2* xo = P.xhalf + static_cast<long long>(rhs) * (P.g.N / 2 + 1) * P.g.M +
+                      static_cast<long long>(kg) * P.g.M;
+        for (int tau = tid; tau < L; tau += nthr) {
+            const int t = t_of(tau, par, L);
+            xo[t + L] = a[__ldg(rev + tau)];
+        }
+    }
+    __syncthreads();
+
+    fft_inverse(a, P.fd, T, tid, nthr);
+
+    // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
+    cluster.sync();
+    const double2* ve = par == 0 ? a : cluster.map_shared_rank(a, 0);
+    const double2* vo = par == 1 ? a : cluster.map_shared_rank(a, 1);
+    const int half = L / 2;
+    const int p_lo = par == 0 ? 0 : half;
+    const int p_hi = par == 0 ? half : L + 1;
+    for (int p = p_lo + tid; p < p_hi; p += nthr) {
+        const int pm = p == L ? 0 : p;
+        const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
+        colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
+    }
+    cluster.sync();
+}
+
+// ------------------------------------------------------------------ shgen
+
+// One CTA per physical latitude: per order m the orthonormal associated
+// Legendre recurrence (no Condon-Shortley phase, as std::assoc_legendre in
+// tests/support/helpers.hpp:18-27) accumulates A_m = sum_l c_lm P_l^m and
+// A_-m; the lambda synthesis is the inverse lambda transform (K4) applied to
+// v_m = (A_m - i A_-m)/sqrt(2), v_0 = A_0.  An extended exponent keeps
+// sin^m(theta) from underflowing at large m.
+__global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
+    const int p = blockIdx.x;
+    const double th = 6.283185307179586476925286766559 * p / P.g.M;
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const int L = P.L;
+    const double big = 0x1p400, small = 0x1p-400;
+    const double inv_sqrt2 = 0.70710678118654752440084436210484903928;
+    for (int m = threadIdx.x; m <= P.g.N / 2; m += blockDim.x) {
+        double Ap = 0.0, Am = 0.0;
+        if (m <= L) {
+            double pmm = 0.28209479177387814347403972578038629292;  // 1/sqrt(4 pi)
+            int e = 0;
+            for (int i = 1; i <= m; ++i) {
+                pmm *= sqrt((2.0 * i + 1.0) / (2.0 * i)) * sn;
+                if (pmm != 0.0 && fabs(pmm) < small) {
+                    pmm *= big;
+                    e -= 400;
+                }
+            }
+            if (pmm != 0.0) {
+                auto emit = [&](int l, double v) {
+                    if (l >= 1) {
+                        const double val = ldexp(v, e);
+                        Ap = fma(P.coeffs[(long long)l * l + l + m], val, Ap);
+                        if (m > 0) Am = fma(P.coeffs[(long long)l * l + l - m], val, Am);
+                    }
+                };
+                double p2 = pmm;
+                emit(m, p2);
+                if (m < L) {
+                    double p1 = sqrt(2.0 * m + 3.0) * cs * pmm;
+                    emit(m + 1, p1);
+                    const double m2 = static_cast<double>(m) * m;
+                    for (int l = m + 2; l <= L; ++l) {
+                        const double ll = l;
+                        const double aa = sqrt((4.0 * ll * ll - 1.0) / (ll * ll - m2));
+                        const double bb = sqrt(((ll - 1.0) * (ll - 1.0) - m2) / (4.0 * (ll - 1.0) * (ll - 1.0) - 1.0));
+                        const double pl = aa * (cs * p1 - bb * p2);
+                        p2 = p1;
+                        p1 = pl;
+                        if (fabs(p1) > big) {
+                            p1 *= small;
+                            p2 *= small;
+                            e += 400;
+                        }
+                        emit(l, p1);
+                    }
+                }
+            }
+        }
+        double2 v;
+        if (m == 0) v = make_double2(Ap, 0.0);
+        else v = make_double2(Ap * inv_sqrt2, -Am * inv_sqrt2);
+        P.spec[static_cast<size_t>(m) * P.rows + p] = v;
+    }
+}
+
+// --------------------------------------------------------- host launchers
+cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(lambda_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    lambda_fwd_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lambda_inv(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(lambda_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    lambda_inv_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr = true;
+    }
+    theta_kernel<<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st) {
+    shgen_kernel<<<P.rows, 256, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

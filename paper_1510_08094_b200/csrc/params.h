@@ -1,0 +1,76 @@
+// Kernel parameter blocks and launchers shared by the host plan code
+// (sk_poisson.cu) and the kernels (grid_kernels.cu, coeff_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "sk_internal.h"
+
+namespace sk {
+
+struct LambdaParams {
+    GridGeom g;
+    FftDesc fd;
+    int rows_local;     // physical rows on this rank
+    int nrhs;
+    long long in_rhs_stride;   // doubles (fwd) or complex (inv) per rhs in the input
+    long long out_rhs_stride;  // complex (fwd) or doubles (inv) per rhs in the output
+    const double* f;    // fwd: real rows; inv: unused
+    double2* spec;      // fwd: output [k][p_local]; inv: input
+    double* u;          // inv: real rows
+};
+
+struct ThetaParams {
+    GridGeom g;
+    FftDesc fd;       // length M/2, twiddles of the M-th roots
+    Slabs sl;
+    double2* buf;     // receive buffer, solved in place
+    int ncols;        // lambda modes on this rank
+    int k0;           // first lambda mode of this rank
+    int nrhs;
+    long long rhs_stride;  // complex per rhs in buf
+    double* stats;    // per rhs: [0..1] mean (re, im), [2] max|F|, [3] unused
+    double2* xhalf;   // optional: solution coefficients X[k][i], (N/2+1) x M per rhs
+};
+
+struct ShgenParams {
+    GridGeom g;
+    int L;                 // max degree
+    const double* coeffs;  // (L+1)^2, index l*l + l + m
+    double2* spec;         // [m][p] (rows = M/2+1), modes m = 0..N/2
+    int rows;
+};
+
+struct CoeffParams {
+    int M, N, nrhs;
+    const double2* F;
+    double2* X;
+    double* D;          // scratch pivots, M x N per rhs
+    double* stats;      // per rhs: [0..1] mean, [2] max|F|, [3] pivot-order violations
+    const double2* z;   // Msin^-1 Msin^-1 w (check_mean_zero), length M
+};
+
+struct ResidualParams {
+    int M, N;
+    const double2* F;
+    const double2* X;
+    double* out;  // [0] interior max, [1] replaced-row abs, [2..3] constraint sum (re, im)
+};
+
+// Dynamic shared memory of theta_kernel (bytes).
+__host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
+    const size_t chain_max = static_cast<size_t>(L / 2 + 2);
+    return static_cast<size_t>(L) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
+           16 * 16 + 64 * 8;
+}
+
+cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_inv(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
+cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
+cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
+
+}  // namespace sk

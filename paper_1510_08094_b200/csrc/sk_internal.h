@@ -1,0 +1,53 @@
+// Internal declarations shared by the host plan code and the CUDA kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sk {
+
+constexpr int kMaxStages = 24;
+constexpr int kMaxRanks = 16;
+
+// In-place mixed-radix Cooley-Tukey FFT of length L in shared memory:
+// forward = decimation in frequency (natural in -> digit-reversed out),
+// inverse = decimation in time (digit-reversed in -> natural out).
+// Stage s has radix R[s], sub-block size sz[s] = L/(R[0]..R[s-1]) and
+// span[s] = sz[s]/R[s]; its twiddles are omega_sz^(q j) = table index
+// q*j*tw[s] of the 2L-th roots (tw[s] = 2L/sz[s]).
+struct FftDesc {
+    int L = 0;
+    int nst = 0;
+    int R[kMaxStages] = {};
+    int span[kMaxStages] = {};
+    int tw[kMaxStages] = {};
+    // twiddle table for the 2L-th roots exp(-2 pi i m / 2L), m in [0, 2L):
+    // T(m) = hi[m >> shift] * lo[m & (B-1)], B = 1 << shift
+    int shift = 0;
+    int nhi = 0;
+    int nlo = 0;
+    const double2* hi = nullptr;  // device, nhi entries
+    const double2* lo = nullptr;  // device, nlo entries
+    const int* rev = nullptr;     // device, L entries: natural index -> DIF output position
+};
+
+// Slab decomposition of one right-hand side over P ranks (P = 1 on a single
+// GPU).  Physical rows p in [0, M/2] are split by row_b, lambda modes
+// k in [0, N/2] by col_b.
+struct Slabs {
+    int P = 1;
+    int rank = 0;
+    int row_b[kMaxRanks + 1] = {};
+    int col_b[kMaxRanks + 1] = {};
+};
+
+struct GridGeom {
+    int M = 0, N = 0;
+    int Lt = 0;   // theta FFT length M/2
+    int Ll = 0;   // lambda FFT length N/2
+    int rows = 0; // M/2 + 1 physical rows
+    int cols = 0; // N/2 + 1 lambda modes (k >= 0)
+};
+
+}  // namespace sk

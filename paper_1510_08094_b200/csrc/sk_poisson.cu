@@ -1,0 +1,710 @@
+// Host side of the C ABI (include/sk_poisson.h): plans, device buffers, FFT
+// tables, launches and the error contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sk_poisson.h"
+#include "params.h"
+#include "sk_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+sk_status fail(sk_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CU(call)                                                                                       \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) return fail(SK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+bool factor_radices(int L, std::vector<int>& R) {
+    R.clear();
+    if (L < 1) return false;
+    int m = L;
+    int p2 = 0;
+    while (m % 2 == 0) {
+        m /= 2;
+        ++p2;
+    }
+    while (p2 >= 3) {
+        if (p2 == 4) {
+            R.push_back(4);
+            R.push_back(4);
+            p2 = 0;
+            break;
+        }
+        R.push_back(8);
+        p2 -= 3;
+    }
+    if (p2 == 2) R.push_back(4);
+    if (p2 == 1) R.push_back(2);
+    for (int q : {5, 3, 7}) {
+        while (m % q == 0) {
+            R.push_back(q);
+            m /= q;
+        }
+    }
+    return m == 1 && static_cast<int>(R.size()) <= sk::kMaxStages;
+}
+
+struct DevFft {
+    sk::FftDesc d;
+    double2* hi = nullptr;
+    double2* lo = nullptr;
+    int* rev = nullptr;
+};
+
+// exp(-2 pi i m / n) with exact index reduction and long double arithmetic.
+void root(long long m, long long n, double& c, double& s) {
+    m %= n;
+    if (m < 0) m += n;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const long double a = 2.0L * pi * static_cast<long double>(m) / static_cast<long double>(n);
+    c = static_cast<double>(cosl(a));
+    s = static_cast<double>(-sinl(a));
+}
+
+sk_status build_fft(int L, DevFft& out) {
+    std::vector<int> R;
+    if (!factor_radices(L, R)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
+    sk::FftDesc& d = out.d;
+    d.L = L;
+    d.nst = static_cast<int>(R.size());
+    int sz = L;
+    for (int s = 0; s < d.nst; ++s) {
+        d.R[s] = R[s];
+        d.span[s] = sz / R[s];
+        d.tw[s] = 2 * L / sz;
+        sz /= R[s];
+    }
+    const long long n2 = 2LL * L;
+    int shift = 0;
+    while ((1LL << (2 * shift)) < n2) ++shift;  // B = 2^shift >= sqrt(2L)
+    const int B = 1 << shift;
+    d.shift = shift;
+    d.nlo = B;
+    d.nhi = static_cast<int>((n2 + B - 1) / B);
+    std::vector<double2> hi(d.nhi), lo(d.nlo);
+    for (int h = 0; h < d.nhi; ++h) root(static_cast<long long>(h) * B, n2, hi[h].x, hi[h].y);
+    for (int l = 0; l < d.nlo; ++l) root(l, n2, lo[l].x, lo[l].y);
+    std::vector<int> rev(L);
+    for (int k = 0; k < L; ++k) {
+        int kk = k, pos = 0;
+        for (int s = 0; s < d.nst; ++s) {
+            pos += (kk % d.R[s]) * d.span[s];
+            kk /= d.R[s];
+        }
+        rev[k] = pos;
+    }
+    CU(cudaMalloc(&out.hi, sizeof(double2) * d.nhi));
+    CU(cudaMalloc(&out.lo, sizeof(double2) * d.nlo));
+    CU(cudaMalloc(&out.rev, sizeof(int) * L));
+    CU(cudaMemcpy(out.hi, hi.data(), sizeof(double2) * d.nhi, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(out.lo, lo.data(), sizeof(double2) * d.nlo, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(out.rev, rev.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    d.hi = out.hi;
+    d.lo = out.lo;
+    d.rev = out.rev;
+    return SK_OK;
+}
+
+void free_fft(DevFft& f) {
+    cudaFree(f.hi);
+    cudaFree(f.lo);
+    cudaFree(f.rev);
+    f = DevFft{};
+}
+
+int round_threads(long long want, int lo, int hi) {
+    long long t = ((want + 31) / 32) * 32;
+    if (t < lo) t = lo;
+    if (t > hi) t = hi;
+    return static_cast<int>(t);
+}
+
+}  // namespace
+
+namespace {
+
+// z = Msin^-1 Msin^-1 w for the mean check (see coeff_kernels.cu mean_kernel),
+// via the pivoted tridiagonal solve of div_sin (fourier.cpp:92-103).
+std::vector<std::complex<double>> div_sin_host(const std::vector<std::complex<double>>& c) {
+    // Msin (i,i+1) = +i/2, (i,i-1) = -i/2: general partial-pivoting tridiagonal
+    // solve (row-permuted, width-3 windows).
+    using C = std::complex<double>;
+    const int n = static_cast<int>(c.size());
+    std::vector<std::vector<C>> row(n, std::vector<C>(4, C{}));  // cols base..base+3
+    std::vector<int> base(n);
+    std::vector<C> rhs(c);
+    for (int i = 0; i < n; ++i) {
+        base[i] = std::max(0, i - 1);
+        for (int j = base[i]; j <= std::min(n - 1, i + 1); ++j) {
+            C v{};
+            if (j == i + 1) v = C(0, 0.5);
+            if (j == i - 1) v = C(0, -0.5);
+            row[i][j - base[i]] = v;
+        }
+    }
+    std::vector<int> perm(n);
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    auto val = [&](int r, int col) {
+        const int t = col - base[r];
+        return (t >= 0 && t < 4) ? row[r][t] : C{};
+    };
+    auto align = [&](int r, int col) {
+        const int sh = col - base[r];
+        if (sh <= 0) return;
+        for (int t = 0; t < 4; ++t) row[r][t] = (t + sh < 4) ? row[r][t + sh] : C{};
+        base[r] = col;
+    };
+    for (int cc = 0; cc < n; ++cc) {
+        const int last = std::min(n - 1, cc + 1);
+        int piv = cc;
+        double best = std::abs(val(perm[cc], cc));
+        for (int r = cc + 1; r <= last; ++r)
+            if (std::abs(val(perm[r], cc)) > best) {
+                best = std::abs(val(perm[r], cc));
+                piv = r;
+            }
+        std::swap(perm[cc], perm[piv]);
+        align(perm[cc], cc);
+        const C pv = row[perm[cc]][0];
+        for (int r = cc + 1; r <= last; ++r) {
+            const C v = val(perm[r], cc);
+            if (v == C{}) continue;
+            align(perm[r], cc);
+            const C f = v / pv;
+            row[perm[r]][0] = C{};
+            for (int t = 1; t < 4; ++t) row[perm[r]][t] -= f * row[perm[cc]][t];
+            rhs[perm[r]] -= f * rhs[perm[cc]];
+        }
+    }
+    std::vector<C> x(n);
+    for (int cc = n - 1; cc >= 0; --cc) {
+        C acc = rhs[perm[cc]];
+        for (int j = cc + 1; j <= std::min(n - 1, cc + 3); ++j) acc -= val(perm[cc], j) * x[j];
+        x[cc] = acc / val(perm[cc], cc);
+    }
+    return x;
+}
+
+std::vector<std::complex<double>> mean_weights(int m) {
+    std::vector<std::complex<double>> w(m);
+    for (int i = 0; i < m; ++i) {
+        const int k = i - m / 2;
+        if (k % 2 != 0) continue;
+        w[i] = 2.0 / (1.0 - static_cast<double>(k) * k);
+    }
+    return div_sin_host(div_sin_host(w));
+}
+
+}  // namespace
+
+struct sk_plan_s {
+    int M = 0, N = 0, nrhs = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool grid_ok = false;
+    std::string grid_why;
+    sk::GridGeom g;
+    DevFft ft, fl;
+    int thr_theta = 0, thr_lambda = 0;
+    size_t smem_theta = 0, smem_lambda = 0;
+    double2* spec = nullptr;   // nrhs * cols * rows complex
+    double* stats = nullptr;   // 4 * nrhs
+    double2* z = nullptr;      // mean weights, M complex
+    double* D = nullptr;       // coefficient-solve pivot scratch
+    double2* hF = nullptr;     // staging for host-pointer coefficient calls
+    double2* hX = nullptr;
+    double* hf = nullptr;      // staging for host-pointer grid calls
+    double* hu = nullptr;
+    double* rbuf = nullptr;    // residual output (4)
+    double2* coef_stage = nullptr;  // shgen coefficients
+    long long last_launches = 0;
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    double times[4] = {0, 0, 0, 0};
+    std::vector<double> host_stats;
+};
+
+namespace {
+
+sk_status ensure(void** p, size_t bytes) {
+    if (*p) return SK_OK;
+    CU(cudaMalloc(p, bytes));
+    return SK_OK;
+}
+
+sk_status check_plan(sk_plan_t p) {
+    if (!p) return fail(SK_ERR_ARGUMENT, "null plan");
+    CU(cudaSetDevice(p->device));
+    return SK_OK;
+}
+
+sk_status check_precondition(sk_plan_t p, int nrhs) {
+    // poisson.cpp:111-116: |2 pi w^T f0| > 1e-6 * 4 pi * max|F|
+    p->host_stats.resize(4 * nrhs);
+    CU(cudaMemcpyAsync(p->host_stats.data(), p->stats, sizeof(double) * 4 * nrhs, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    const double fourpi = 12.566370614359172953850573533118;
+    for (int r = 0; r < nrhs; ++r) {
+        const double* s = &p->host_stats[4 * r];
+        if (s[3] >= double(1 << 20))
+            return fail(SK_ERR_SINGULAR, "band_solve: matrix is numerically singular");
+        const double fscale = s[2];
+        if (fscale == 0.0) continue;
+        const double mean = std::hypot(s[0], s[1]);
+        if (mean > 1e-6 * fourpi * fscale)
+            return fail(SK_ERR_PRECONDITION, "poisson solve: right-hand side has a nonzero surface mean");
+    }
+    return SK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+const char* sk_version(void) { return "sk_poisson 0.1 (sm_100a)"; }
+
+sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
+    if (!out) return fail(SK_ERR_ARGUMENT, "null output plan pointer");
+    *out = nullptr;
+    if (M <= 0 || N <= 0 || M % 2 != 0 || N % 2 != 0)
+        return fail(SK_ERR_SIZE, "poisson solve: sizes must be positive and even");
+    if (nrhs < 1) return fail(SK_ERR_ARGUMENT, "nrhs must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SK_ERR_CUDA, "no CUDA device available (the solver has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(SK_ERR_ARGUMENT, "bad device ordinal");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(SK_ERR_CUDA, "this build targets sm_100a (Blackwell); device is sm_" +
+                                                      std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* p = new sk_plan_s;
+    p->M = M;
+    p->N = N;
+    p->nrhs = nrhs;
+    p->device = device;
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete p;
+        return fail(SK_ERR_CUDA, "stream creation failed");
+    }
+    p->own_stream = true;
+    p->g.M = M;
+    p->g.N = N;
+    p->g.Lt = M / 2;
+    p->g.Ll = N / 2;
+    p->g.rows = M / 2 + 1;
+    p->g.cols = N / 2 + 1;
+    sk_status s;
+    if ((s = ensure(reinterpret_cast<void**>(&p->stats), sizeof(double) * 4 * nrhs)) != SK_OK) {
+        sk_plan_destroy(p);
+        return s;
+    }
+    // mean weights
+    {
+        const auto z = mean_weights(M);
+        if ((s = ensure(reinterpret_cast<void**>(&p->z), sizeof(double2) * M)) != SK_OK) {
+            sk_plan_destroy(p);
+            return s;
+        }
+        if (cudaMemcpy(p->z, z.data(), sizeof(double2) * M, cudaMemcpyHostToDevice) != cudaSuccess) {
+            sk_plan_destroy(p);
+            return fail(SK_ERR_CUDA, "copy of mean weights failed");
+        }
+    }
+    // grid path: FFT plans + on-chip limits
+    p->grid_ok = true;
+    if (M < 8 || N < 4) {
+        p->grid_ok = false;
+        p->grid_why = "grid path needs M >= 8 and N >= 4";
+    }
+    if (p->grid_ok && (s = build_fft(M / 2, p->ft)) != SK_OK) {
+        p->grid_ok = false;
+        p->grid_why = g_err;
+    }
+    if (p->grid_ok && (s = build_fft(N / 2, p->fl)) != SK_OK) {
+        p->grid_ok = false;
+        p->grid_why = g_err;
+    }
+    if (p->grid_ok) {
+        const int Lt = M / 2, Ll = N / 2;
+        p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
+        p->smem_lambda = static_cast<size_t>(Ll) * 16 + static_cast<size_t>(p->fl.d.nhi + p->fl.d.nlo) * 16;
+        const size_t cap = 227 * 1024;
+        if (p->smem_theta > cap || p->smem_lambda > cap) {
+            p->grid_ok = false;
+            p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +
+                          " exceeds the on-chip (shared memory) limit of this build";
+        }
+        p->thr_theta = round_threads(Lt / 8, 64, 512);
+        p->thr_lambda = round_threads(Ll / 8, 64, 512);
+    }
+    if (p->grid_ok) {
+        const size_t n = static_cast<size_t>(nrhs) * p->g.rows * p->g.cols;
+        if ((s = ensure(reinterpret_cast<void**>(&p->spec), sizeof(double2) * n)) != SK_OK) {
+            sk_plan_destroy(p);
+            return s;
+        }
+    }
+    *out = p;
+    return SK_OK;
+}
+
+sk_status sk_plan_destroy(sk_plan_t p) {
+    if (!p) return SK_OK;
+    cudaSetDevice(p->device);
+    free_fft(p->ft);
+    free_fft(p->fl);
+    for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
+                    static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
+                    static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
+                    static_cast<void*>(p->coef_stage)})
+        if (q) cudaFree(q);
+    for (auto& e : p->ev)
+        if (e) cudaEventDestroy(e);
+    if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+    return SK_OK;
+}
+
+sk_status sk_plan_set_stream(sk_plan_t p, void* stream) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+    p->stream = static_cast<cudaStream_t>(stream);
+    p->own_stream = false;
+    return SK_OK;
+}
+
+sk_status sk_sync(sk_plan_t p) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+sk_status sk_enable_stage_timing(sk_plan_t p, int on) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (on && !p->ev[0])
+        for (auto& e : p->ev) CU(cudaEventCreate(&e));
+    p->timing = on != 0;
+    return SK_OK;
+}
+
+sk_status sk_stage_times(sk_plan_t p, double t[4]) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!t) return fail(SK_ERR_ARGUMENT, "null output");
+    for (int i = 0; i < 4; ++i) t[i] = p->times[i];
+    return SK_OK;
+}
+
+sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
+    if (!p || !info) return fail(SK_ERR_ARGUMENT, "null argument");
+    for (int i = 0; i < 16; ++i) info[i] = 0;
+    info[0] = p->M;
+    info[1] = p->N;
+    info[2] = p->nrhs;
+    info[3] = p->device;
+    info[4] = p->grid_ok ? 1 : 0;
+    info[5] = p->g.rows;
+    info[6] = 2;
+    info[7] = p->thr_theta;
+    info[8] = p->thr_lambda;
+    info[9] = p->last_launches;
+    info[10] = static_cast<long long>(p->smem_theta);
+    info[11] = static_cast<long long>(p->smem_lambda);
+    return SK_OK;
+}
+
+sk_status sk_solve_coeffs(sk_plan_t p, const double* F, double* X, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!F || !X) return fail(SK_ERR_ARGUMENT, "null F or X");
+    const size_t n = static_cast<size_t>(p->nrhs) * p->M * p->N;
+    const double2* dF;
+    double2* dX;
+    if (flags & SK_DEVICE) {
+        dF = reinterpret_cast<const double2*>(F);
+        dX = reinterpret_cast<double2*>(X);
+    } else {
+        if ((s = ensure(reinterpret_cast<void**>(&p->hF), sizeof(double2) * n)) != SK_OK) return s;
+        if ((s = ensure(reinterpret_cast<void**>(&p->hX), sizeof(double2) * n)) != SK_OK) return s;
+        CU(cudaMemcpyAsync(p->hF, F, sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+        dF = p->hF;
+        dX = p->hX;
+    }
+    if ((s = ensure(reinterpret_cast<void**>(&p->D), sizeof(double) * n)) != SK_OK) return s;
+    CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4 * p->nrhs, p->stream));
+    sk::CoeffParams cp{p->M, p->N, p->nrhs, dF, dX, p->D, p->stats, p->z};
+    if (p->timing) CU(cudaEventRecord(p->ev[6], p->stream));
+    CU(sk::launch_coeff_solve(cp, p->stream));
+    if (p->timing) CU(cudaEventRecord(p->ev[7], p->stream));
+    p->last_launches = 2;
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(X, dX, sizeof(double2) * n, cudaMemcpyDeviceToHost, p->stream));
+    if ((flags & SK_ASYNC) && (flags & SK_DEVICE)) return SK_OK;
+    s = check_precondition(p, p->nrhs);
+    if (p->timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p->ev[6], p->ev[7]);
+        p->times[3] = ms;
+    }
+    return s;
+}
+
+sk_status sk_residual(sk_plan_t p, const double* F, const double* X, double out[3], unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!F || !X || !out) return fail(SK_ERR_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(p->M) * p->N;
+    const double2 *dF, *dX;
+    if (flags & SK_DEVICE) {
+        dF = reinterpret_cast<const double2*>(F);
+        dX = reinterpret_cast<const double2*>(X);
+    } else {
+        if ((s = ensure(reinterpret_cast<void**>(&p->hF), sizeof(double2) * n * p->nrhs)) != SK_OK) return s;
+        if ((s = ensure(reinterpret_cast<void**>(&p->hX), sizeof(double2) * n * p->nrhs)) != SK_OK) return s;
+        CU(cudaMemcpyAsync(p->hF, F, sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+        CU(cudaMemcpyAsync(p->hX, X, sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+        dF = p->hF;
+        dX = p->hX;
+    }
+    if ((s = ensure(reinterpret_cast<void**>(&p->rbuf), sizeof(double) * 4)) != SK_OK) return s;
+    CU(cudaMemsetAsync(p->rbuf, 0, sizeof(double) * 4, p->stream));
+    sk::ResidualParams rp{p->M, p->N, dF, dX, p->rbuf};
+    CU(sk::launch_residual(rp, p->stream));
+    p->last_launches = 1;
+    double h[4];
+    CU(cudaMemcpyAsync(h, p->rbuf, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    out[0] = h[0];
+    out[1] = h[1];
+    out[2] = 6.283185307179586476925286766559 * std::hypot(h[2], h[3]);
+    return SK_OK;
+}
+
+static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int ncols_local, int k0,
+                          const double* f_dev, double2* spec, double* u_dev, double2* xhalf, int stages) {
+    // stages bit 0: lambda fwd, bit 1: theta, bit 2: lambda inv
+    sk::LambdaParams lp{};
+    lp.g = p->g;
+    lp.fd = p->fl.d;
+    lp.rows_local = rows_local;
+    lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
+    if (stages & 1) {
+        lp.in_rhs_stride = static_cast<long long>(rows_local) * p->N;
+        lp.out_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
+        lp.f = f_dev;
+        lp.spec = spec;
+        if (p->timing) CU(cudaEventRecord(p->ev[0], p->stream));
+        CU(sk::launch_lambda_fwd(lp, p->thr_lambda, p->smem_lambda, p->stream));
+        if (p->timing) CU(cudaEventRecord(p->ev[1], p->stream));
+        p->last_launches += 1;
+    }
+    if (stages & 2) {
+        sk::ThetaParams tp{};
+        tp.g = p->g;
+        tp.fd = p->ft.d;
+        tp.sl = sl;
+        tp.buf = spec;
+        tp.ncols = ncols_local;
+        tp.k0 = k0;
+        tp.nrhs = (sl.P == 1) ? p->nrhs : 1;
+        tp.rhs_stride = static_cast<long long>(p->g.rows) * ncols_local;
+        tp.stats = p->stats;
+        tp.xhalf = xhalf;
+        if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
+        CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
+        if (p->timing) CU(cudaEventRecord(p->ev[3], p->stream));
+        p->last_launches += 1;
+    }
+    if (stages & 4) {
+        lp.in_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
+        lp.out_rhs_stride = static_cast<long long>(rows_local) * p->N;
+        lp.f = nullptr;
+        lp.spec = spec;
+        lp.u = u_dev;
+        if (p->timing) CU(cudaEventRecord(p->ev[4], p->stream));
+        CU(sk::launch_lambda_inv(lp, p->thr_lambda, p->smem_lambda, p->stream));
+        if (p->timing) CU(cudaEventRecord(p->ev[5], p->stream));
+        p->last_launches += 1;
+    }
+    return SK_OK;
+}
+
+static void collect_times(sk_plan_t p, int stages) {
+    if (!p->timing) return;
+    cudaStreamSynchronize(p->stream);
+    float ms = 0;
+    if (stages & 1) {
+        cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]);
+        p->times[0] = ms;
+    }
+    if (stages & 2) {
+        cudaEventElapsedTime(&ms, p->ev[2], p->ev[3]);
+        p->times[1] = ms;
+    }
+    if (stages & 4) {
+        cudaEventElapsedTime(&ms, p->ev[4], p->ev[5]);
+        p->times[2] = ms;
+    }
+}
+
+sk_status sk_solve_grid(sk_plan_t p, const double* f, double* u, double* X_half, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    if (!f || !u) return fail(SK_ERR_ARGUMENT, "null f or u");
+    const size_t ng = static_cast<size_t>(p->nrhs) * p->g.rows * p->N;
+    const double* df;
+    double* du;
+    if (flags & SK_DEVICE) {
+        df = f;
+        du = u;
+    } else {
+        if ((s = ensure(reinterpret_cast<void**>(&p->hf), sizeof(double) * ng)) != SK_OK) return s;
+        CU(cudaMemcpyAsync(p->hf, f, sizeof(double) * ng, cudaMemcpyHostToDevice, p->stream));
+        df = p->hf;
+        du = p->hf;  // in place
+    }
+    double2* xh = nullptr;
+    if (X_half) {
+        if (flags & SK_DEVICE) {
+            xh = reinterpret_cast<double2*>(X_half);
+        } else {
+            const size_t nx = static_cast<size_t>(p->nrhs) * p->g.cols * p->M;
+            if ((s = ensure(reinterpret_cast<void**>(&p->hX), sizeof(double2) * std::max(nx, static_cast<size_t>(p->nrhs) * p->M * p->N))) != SK_OK)
+                return s;
+            xh = p->hX;
+        }
+    }
+    CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4 * p->nrhs, p->stream));
+    sk::Slabs sl{};
+    sl.P = 1;
+    sl.rank = 0;
+    sl.row_b[0] = 0;
+    sl.row_b[1] = p->g.rows;
+    sl.col_b[0] = 0;
+    sl.col_b[1] = p->g.cols;
+    p->last_launches = 0;
+    if ((s = run_grid(p, sl, p->g.rows, p->g.cols, 0, df, p->spec, du, xh, 7)) != SK_OK) return s;
+    if (!(flags & SK_DEVICE)) {
+        CU(cudaMemcpyAsync(u, du, sizeof(double) * ng, cudaMemcpyDeviceToHost, p->stream));
+        if (X_half) {
+            const size_t nx = static_cast<size_t>(p->nrhs) * p->g.cols * p->M;
+            CU(cudaMemcpyAsync(X_half, xh, sizeof(double2) * nx, cudaMemcpyDeviceToHost, p->stream));
+        }
+    }
+    if ((flags & SK_ASYNC) && (flags & SK_DEVICE)) return SK_OK;
+    s = check_precondition(p, p->nrhs);
+    collect_times(p, 7);
+    return s;
+}
+
+sk_status sk_last_mean(sk_plan_t p, double out[3]) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    double h[4];
+    CU(cudaMemcpyAsync(h, p->stats, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    out[0] = h[0];
+    out[1] = h[1];
+    out[2] = h[2];
+    return SK_OK;
+}
+
+sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_dev) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    if (!coeffs_dev || !phys_dev || L < 0) return fail(SK_ERR_ARGUMENT, "bad shgen arguments");
+    if (L >= p->N / 2) return fail(SK_ERR_ARGUMENT, "degree L must be below N/2");
+    sk::ShgenParams sp{p->g, L, coeffs_dev, p->spec, p->g.rows};
+    CU(sk::launch_shgen(sp, p->stream));
+    sk::LambdaParams lp{};
+    lp.g = p->g;
+    lp.fd = p->fl.d;
+    lp.rows_local = p->g.rows;
+    lp.nrhs = 1;
+    lp.in_rhs_stride = 0;
+    lp.out_rhs_stride = 0;
+    lp.spec = p->spec;
+    lp.u = phys_dev;
+    CU(sk::launch_lambda_inv(lp, p->thr_lambda, p->smem_lambda, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+static sk_status make_slabs(sk_plan_t p, int P, const int* rb, const int* cb, int rank, sk::Slabs& sl) {
+    if (P < 1 || P > sk::kMaxRanks || rank < 0 || rank >= P || !rb || !cb)
+        return fail(SK_ERR_ARGUMENT, "bad slab description");
+    if (rb[0] != 0 || rb[P] != p->g.rows || cb[0] != 0 || cb[P] != p->g.cols)
+        return fail(SK_ERR_ARGUMENT, "slabs must cover rows [0, M/2] and modes [0, N/2]");
+    sl.P = P;
+    sl.rank = rank;
+    for (int i = 0; i <= P; ++i) {
+        sl.row_b[i] = rb[i];
+        sl.col_b[i] = cb[i];
+        if (i > 0 && (rb[i] < rb[i - 1] || cb[i] < cb[i - 1])) return fail(SK_ERR_ARGUMENT, "slabs must be ordered");
+    }
+    return SK_OK;
+}
+
+sk_status sk_stage_lambda_fwd(sk_plan_t p, int P, const int* rb, const int* cb, int rank, const double* f_rows_dev,
+                              double* send_dev) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    sk::Slabs sl{};
+    if ((s = make_slabs(p, P, rb, cb, rank, sl)) != SK_OK) return s;
+    const int rows = rb[rank + 1] - rb[rank];
+    if (rows == 0) return SK_OK;
+    p->last_launches = 0;
+    return run_grid(p, sl, rows, cb[rank + 1] - cb[rank], cb[rank], f_rows_dev,
+                    reinterpret_cast<double2*>(send_dev), nullptr, nullptr, 1);
+}
+
+sk_status sk_stage_theta(sk_plan_t p, int P, const int* rb, const int* cb, int rank, double* recv_dev) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    sk::Slabs sl{};
+    if ((s = make_slabs(p, P, rb, cb, rank, sl)) != SK_OK) return s;
+    const int ncols = cb[rank + 1] - cb[rank];
+    CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4, p->stream));
+    if (ncols == 0) return SK_OK;
+    p->last_launches = 0;
+    return run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2);
+}
+
+sk_status sk_stage_lambda_inv(sk_plan_t p, int P, const int* rb, const int* cb, int rank, const double* back_dev,
+                              double* u_rows_dev) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    sk::Slabs sl{};
+    if ((s = make_slabs(p, P, rb, cb, rank, sl)) != SK_OK) return s;
+    const int rows = rb[rank + 1] - rb[rank];
+    if (rows == 0) return SK_OK;
+    p->last_launches = 0;
+    return run_grid(p, sl, rows, cb[rank + 1] - cb[rank], cb[rank], nullptr,
+                    const_cast<double2*>(reinterpret_cast<const double2*>(back_dev)), u_rows_dev, nullptr, 4);
+}
+
+}  // extern "C"

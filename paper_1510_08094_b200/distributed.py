@@ -1,0 +1,153 @@
+"""Slab-decomposed grid solve over several GPUs (one process per GPU).
+
+The lambda stages work on physical theta rows, the theta stage on lambda
+modes; the two transposes between them are all-to-all exchanges over NCCL
+(torch.distributed plumbing, NVLink/NVSwitch on a B200 box).  The reference
+is single-process (its only parallelism is std::thread over lambda columns,
+poisson.cpp:147-159); SURVEY §8e.
+
+Block layout of the exchanges: rank r's send buffer after the
+forward lambda stage is [k][p - row_b[r]] for all modes k, so the block for
+destination d is the contiguous range k in [col_b[d], col_b[d+1]); rank d's
+receive buffer is the concatenation over sources s of [k - col_b[d]][p -
+row_b[s]] blocks, which the theta stage reads piecewise and overwrites in
+place; the return exchange sends the same blocks back.
+
+The per-rank stage work is pluggable (``backend``) so that the host-side
+orchestration can be exercised on CPU with gloo (tests/test_distributed.py);
+the product backend is the CUDA library (``CudaStages``).
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import numpy as np
+
+
+def slab_bounds(total: int, parts: int) -> List[int]:
+    """Contiguous near-equal split of range(total) into `parts` slabs."""
+    return [(total * i) // parts for i in range(parts + 1)]
+
+
+class CudaStages:
+    """The three stage entry points of libsk_poisson.so for one rank."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def lambda_fwd(self, P, rb, cb, rank, f_rows, send):
+        self.plan.stage_lambda_fwd(P, rb, cb, rank, f_rows, send)
+
+    def theta(self, P, rb, cb, rank, recv):
+        self.plan.stage_theta(P, rb, cb, rank, recv)
+
+    def lambda_inv(self, P, rb, cb, rank, back, u_rows):
+        self.plan.stage_lambda_inv(P, rb, cb, rank, back, u_rows)
+
+
+class SlabSolver:
+    """One rank of the P-way slab-decomposed grid solve.
+
+    ``solve(f_rows)`` takes this rank's physical rows (row_b[r]..row_b[r+1])
+    of f, shape (rows_r, N) float64, and returns the same rows of u.
+    """
+
+    def __init__(self, M: int, N: int, rank: int, world: int, device=None, backend=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.M, self.N, self.rank, self.P = M, N, rank, world
+        self.rows, self.cols = M // 2 + 1, N // 2 + 1
+        self.rb = slab_bounds(self.rows, world)
+        self.cb = slab_bounds(self.cols, world)
+        self.group = group
+        self.device = device if device is not None else torch.device("cpu")
+        if backend is None:
+            from .poisson import Plan
+            self._plan = Plan(M, N, 1, device.index if hasattr(device, "index") and device.index is not None else 0)
+            backend = CudaStages(self._plan)
+        self.backend = backend
+        r = rank
+        self.rows_r = self.rb[r + 1] - self.rb[r]
+        self.cols_r = self.cb[r + 1] - self.cb[r]
+        # exchange sizes in doubles (complex = 2 doubles)
+        self.send_split = [2 * (self.cb[d + 1] - self.cb[d]) * self.rows_r for d in range(world)]
+        self.recv_split = [2 * self.cols_r * (self.rb[s + 1] - self.rb[s]) for s in range(world)]
+        kw = dict(dtype=torch.float64, device=self.device)
+        self.send = torch.empty(sum(self.send_split), **kw)
+        self.recv = torch.empty(sum(self.recv_split), **kw)
+        self.back = torch.empty(sum(self.send_split), **kw)
+
+    def solve(self, f_rows, u_rows=None):
+        torch, dist = self.torch, self.dist
+        if u_rows is None:
+            u_rows = torch.empty_like(f_rows)
+        P, rb, cb, r = self.P, self.rb, self.cb, self.rank
+        self.backend.lambda_fwd(P, rb, cb, r, f_rows, self.send)
+        dist.all_to_all_single(self.recv, self.send, self.recv_split, self.send_split, group=self.group)
+        self.backend.theta(P, rb, cb, r, self.recv)
+        dist.all_to_all_single(self.back, self.recv, self.send_split, self.recv_split, group=self.group)
+        self.backend.lambda_inv(P, rb, cb, r, self.back, u_rows)
+        return u_rows
+
+    def check_precondition(self):
+        """All-reduce of the mean / max|F| statistics of the last solve and
+        the reference's nonzero-mean test (poisson.cpp:111-116)."""
+        torch, dist = self.torch, self.dist
+        mean, fmax = self._plan.last_mean()
+        t = torch.tensor([mean.real, mean.imag], dtype=torch.float64, device=self.device)
+        m = torch.tensor([fmax], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, group=self.group)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+        mu = complex(t[0].item(), t[1].item())
+        fscale = m.item()
+        if fscale != 0.0 and abs(mu) > 1e-6 * 4.0 * np.pi * fscale:
+            from ._lib import precondition_error
+            raise precondition_error("poisson solve: right-hand side has a nonzero surface mean")
+
+
+def emulate_slabs(f: np.ndarray, M: int, N: int, P: int) -> np.ndarray:
+    """Run the P-rank slab path on ONE GPU, the all-to-all replaced by device
+    copies between the per-rank buffers (no rank waits on another)."""
+    import torch
+
+    from .poisson import Plan
+    rows, cols = M // 2 + 1, N // 2 + 1
+    rb, cb = slab_bounds(rows, P), slab_bounds(cols, P)
+    dev = torch.device("cuda")
+    fd = torch.from_numpy(np.ascontiguousarray(f)).to(dev)
+    with Plan(M, N) as plan:
+        st = CudaStages(plan)
+        sends = []
+        for r in range(P):
+            rr = rb[r + 1] - rb[r]
+            s = torch.empty(2 * cols * rr, dtype=torch.float64, device=dev)
+            st.lambda_fwd(P, rb, cb, r, fd[rb[r]: rb[r + 1]].contiguous(), s)
+            sends.append(s)
+        recvs = []
+        for d in range(P):
+            parts = [sends[s][2 * cb[d] * (rb[s + 1] - rb[s]): 2 * cb[d + 1] * (rb[s + 1] - rb[s])] for s in range(P)]
+            recv = torch.cat(parts).contiguous()
+            st.theta(P, rb, cb, d, recv)
+            recvs.append(recv)
+        u = torch.empty((rows, N), dtype=torch.float64, device=dev)
+        for s in range(P):
+            rs = rb[s + 1] - rb[s]
+            parts = [recvs[d][2 * (cb[d + 1] - cb[d]) * rb[s]: 2 * (cb[d + 1] - cb[d]) * rb[s + 1]] for d in range(P)]
+            back = torch.cat(parts).contiguous()
+            ur = torch.empty((rs, N), dtype=torch.float64, device=dev)
+            st.lambda_inv(P, rb, cb, s, back, ur)
+            u[rb[s]: rb[s + 1]] = ur
+        torch.cuda.synchronize()
+        return u.cpu().numpy()
+
+
+def gather_rows(u_rows, rows_bounds: Sequence[int], group=None):
+    """Collect all ranks' row slabs on every rank (for tests / small cases)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    parts = [torch.empty((rows_bounds[i + 1] - rows_bounds[i], u_rows.shape[1]), dtype=u_rows.dtype,
+                         device=u_rows.device) for i in range(world)]
+    dist.all_gather(parts, u_rows.contiguous(), group=group)
+    return torch.cat(parts)

@@ -1,0 +1,298 @@
+"""Host-side mirror of the reference Poisson interface (namespace spherekit).
+
+Reference                                         here
+------------------------------------------------  ------------------------------------
+PoissonProblem{m, n, f}      poisson.hpp:23-26    PoissonProblem(m, n, f)
+PoissonSolution{x}           poisson.hpp:28-30    PoissonSolution(x)
+solve(pb)                    poisson.hpp:47       solve(pb)            -> sk_solve_coeffs
+ResidualReport               poisson.hpp:49-53    ResidualReport
+residual(pb, sol)            poisson.hpp:54       residual(pb, sol)    -> sk_residual
+bench_poisson(sizes)         poisson.hpp:62       bench_poisson(sizes)
+integration_weights(m)       poisson.hpp:21       integration_weights(m)
+sample_dfs -> analyze_2d -> Msin^2 -> solve ->    solve_grid(f_phys)   -> sk_solve_grid
+  sample_grid (the grid-level composition)
+
+Matrices are numpy complex128 arrays in the reference layout (row i = theta
+mode i - m/2, column kc = lambda mode kc - n/2).  Errors raise the
+reference's exception types (size_error, precondition_error,
+structure_error).  Everything computes on the GPU through libsk_poisson.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import time
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import DeviceError, UnsupportedError, precondition_error, size_error, structure_error
+
+__all__ = [
+    "Plan", "PoissonProblem", "PoissonSolution", "ResidualReport", "BenchRow", "solve", "residual", "solve_grid",
+    "bench_poisson", "integration_weights", "size_error", "precondition_error", "structure_error", "DeviceError",
+    "UnsupportedError",
+]
+
+
+def _ptr(a) -> Optional[int]:
+    """Raw address of a numpy array or a torch tensor (None passes NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch.Tensor
+
+
+def _is_device(a) -> bool:
+    return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+class Plan:
+    """An M x N problem (M = doubled theta count, N = lambda count) with
+    ``nrhs`` right-hand sides on one CUDA device: owns device buffers, FFT
+    tables and a stream (sk_plan_create)."""
+
+    def __init__(self, M: int, N: int, nrhs: int = 1, device: int = 0):
+        self.lib = _lib.load()
+        self.M, self.N, self.nrhs, self.device = int(M), int(N), int(nrhs), int(device)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.sk_plan_create(self.M, self.N, self.nrhs, self.device, ctypes.byref(h)))
+        self._h = h
+
+    # -- lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.sk_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: int) -> None:
+        _lib.check(self.lib.sk_plan_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    def sync(self) -> None:
+        _lib.check(self.lib.sk_sync(self._h))
+
+    def info(self) -> dict:
+        a = (ctypes.c_longlong * 16)()
+        _lib.check(self.lib.sk_plan_info(self._h, a))
+        keys = ["M", "N", "nrhs", "device", "grid_ok", "rows", "theta_split", "theta_threads", "lambda_threads",
+                "last_launches", "theta_smem", "lambda_smem"]
+        return {k: int(a[i]) for i, k in enumerate(keys)}
+
+    @property
+    def grid_supported(self) -> bool:
+        return bool(self.info()["grid_ok"])
+
+    def enable_stage_timing(self, on: bool = True) -> None:
+        _lib.check(self.lib.sk_enable_stage_timing(self._h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        t = (ctypes.c_double * 4)()
+        _lib.check(self.lib.sk_stage_times(self._h, t))
+        return {"lambda_fwd_ms": t[0], "theta_ms": t[1], "lambda_inv_ms": t[2], "coeff_solve_ms": t[3]}
+
+    def last_launches(self) -> int:
+        return self.info()["last_launches"]
+
+    # -- coefficient space (drop-in for spherekit::solve)
+    def solve_coeffs(self, F, X=None, sync: bool = True):
+        """F: (nrhs, M, N) or (M, N) complex128, numpy (host) or torch CUDA."""
+        dev = _is_device(F)
+        if X is None:
+            if dev:
+                import torch
+                X = torch.empty_like(F)
+            else:
+                F = np.ascontiguousarray(F, dtype=np.complex128)
+                X = np.empty_like(F)
+        self._check_shape(F, (self.M, self.N))
+        flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
+        _lib.check(self.lib.sk_solve_coeffs(self._h, _ptr(F), _ptr(X), flags))
+        return X
+
+    def residual(self, F, X):
+        dev = _is_device(F)
+        if not dev:
+            F = np.ascontiguousarray(F, dtype=np.complex128)
+            X = np.ascontiguousarray(X, dtype=np.complex128)
+        out = (ctypes.c_double * 3)()
+        _lib.check(self.lib.sk_residual(self._h, _ptr(F), _ptr(X), out, _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return ResidualReport(out[0], out[1], out[2])
+
+    # -- grid space
+    def solve_grid(self, f, u=None, coeffs: bool = False, sync: bool = True):
+        """f: (nrhs, M/2+1, N) or (M/2+1, N) float64 physical samples.
+        Returns u (same shape), and with ``coeffs`` also the k >= 0 solution
+        coefficients X_half[k][i] = X[i][k + N/2] ((N/2+1) x M complex)."""
+        dev = _is_device(f)
+        rows = self.M // 2 + 1
+        self._check_shape(f, (rows, self.N))
+        Xh = None
+        if dev:
+            import torch
+            if u is None:
+                u = torch.empty_like(f)
+            if coeffs:
+                Xh = torch.empty((self.nrhs, self.N // 2 + 1, self.M), dtype=torch.complex128, device=f.device)
+        else:
+            f = np.ascontiguousarray(f, dtype=np.float64)
+            if u is None:
+                u = np.empty_like(f)
+            if coeffs:
+                Xh = np.empty((self.nrhs, self.N // 2 + 1, self.M), np.complex128)
+        flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
+        _lib.check(self.lib.sk_solve_grid(self._h, _ptr(f), _ptr(u), _ptr(Xh), flags))
+        if coeffs:
+            if self.nrhs == 1:
+                Xh = Xh[0]
+            return u, Xh
+        return u
+
+    def last_mean(self):
+        out = (ctypes.c_double * 3)()
+        _lib.check(self.lib.sk_last_mean(self._h, out))
+        return complex(out[0], out[1]), out[2]
+
+    def shgen(self, L: int, coeffs_dev, phys_dev) -> None:
+        _lib.check(self.lib.sk_shgen(self._h, int(L), _ptr(coeffs_dev), _ptr(phys_dev)))
+
+    # -- slab stages (multi-GPU)
+    def _bounds(self, P, row_b, col_b):
+        rb = (ctypes.c_int * (P + 1))(*row_b)
+        cb = (ctypes.c_int * (P + 1))(*col_b)
+        return rb, cb
+
+    def stage_lambda_fwd(self, P, row_b, col_b, rank, f_rows, send):
+        rb, cb = self._bounds(P, row_b, col_b)
+        _lib.check(self.lib.sk_stage_lambda_fwd(self._h, P, rb, cb, rank, _ptr(f_rows), _ptr(send)))
+
+    def stage_theta(self, P, row_b, col_b, rank, recv):
+        rb, cb = self._bounds(P, row_b, col_b)
+        _lib.check(self.lib.sk_stage_theta(self._h, P, rb, cb, rank, _ptr(recv)))
+
+    def stage_lambda_inv(self, P, row_b, col_b, rank, back, u_rows):
+        rb, cb = self._bounds(P, row_b, col_b)
+        _lib.check(self.lib.sk_stage_lambda_inv(self._h, P, rb, cb, rank, _ptr(back), _ptr(u_rows)))
+
+    def _check_shape(self, a, tail):
+        shp = tuple(a.shape)
+        if shp[-2:] != tuple(tail):
+            raise size_error(f"expected trailing shape {tail}, got {shp}")
+        lead = int(np.prod(shp[:-2])) if len(shp) > 2 else 1
+        if lead != self.nrhs:
+            raise size_error(f"expected {self.nrhs} right-hand side(s), got {lead}")
+
+
+# ------------------------------------------------------------ reference API
+@dataclasses.dataclass
+class PoissonProblem:
+    m: int
+    n: int
+    f: np.ndarray  # m x n complex128: 2D Fourier coefficients of sin(theta)^2 f~
+
+
+@dataclasses.dataclass
+class PoissonSolution:
+    x: np.ndarray  # m x n complex128: 2D Fourier coefficients of u~
+
+
+@dataclasses.dataclass
+class ResidualReport:
+    interior_max: float = 0.0
+    replaced_row_abs: float = 0.0
+    constraint_abs: float = 0.0
+
+
+@dataclasses.dataclass
+class BenchRow:
+    size: int
+    reps: int
+    seconds: float
+
+
+_plans: dict = {}
+
+
+def _plan(m: int, n: int, nrhs: int = 1) -> Plan:
+    key = (m, n, nrhs)
+    p = _plans.get(key)
+    if p is None:
+        p = Plan(m, n, nrhs)
+        _plans[key] = p
+    return p
+
+
+def _check_sizes(m, n):
+    if m <= 0 or n <= 0 or m % 2 or n % 2:
+        raise size_error("poisson solve: sizes must be positive and even")
+
+
+def solve(pb: PoissonProblem) -> PoissonSolution:
+    """spherekit::solve (poisson.cpp:121-161) on the GPU: bit-identical X for
+    every k != 0 column; k = 0 to rounding."""
+    _check_sizes(pb.m, pb.n)
+    F = np.ascontiguousarray(pb.f, dtype=np.complex128)
+    if F.shape != (pb.m, pb.n):
+        raise size_error("poisson solve: f must be m x n")
+    return PoissonSolution(_plan(pb.m, pb.n).solve_coeffs(F))
+
+
+def residual(pb: PoissonProblem, sol: PoissonSolution) -> ResidualReport:
+    """spherekit::residual (poisson.cpp:163-186)."""
+    _check_sizes(pb.m, pb.n)
+    return _plan(pb.m, pb.n).residual(pb.f, sol.x)
+
+
+def solve_grid(f_phys: np.ndarray, m: Optional[int] = None, coeffs: bool = False):
+    """Physical samples f ((m/2+1) x n, theta_p = 2 pi p/m, lambda_q = -pi +
+    2 pi q/n) -> physical solution u of Lap u = f, integral(u) = 0."""
+    rows, n = f_phys.shape[-2:]
+    m = 2 * (rows - 1) if m is None else m
+    _check_sizes(m, n)
+    return _plan(m, n).solve_grid(f_phys, coeffs=coeffs)
+
+
+def integration_weights(m: int) -> np.ndarray:
+    """poisson.cpp:42-50: w_k = 2/(1-k^2) for even k, 0 for odd k."""
+    k = np.arange(m) - m // 2
+    w = np.zeros(m, np.complex128)
+    even = (k % 2) == 0
+    w[even] = 2.0 / (1.0 - k[even].astype(np.float64) ** 2)
+    return w
+
+
+def bench_poisson(sizes, reps: Optional[int] = None):
+    """poisson.cpp:188-230: best-of-reps time of one coefficient-space solve
+    per size on the synthetic band-limited workload (same RNG stream)."""
+    from .inputs import bench_problem
+    rows = []
+    for i, s in enumerate(sizes):
+        if s < 16 or s % 2:
+            raise size_error("bench_poisson: sizes must be even and >= 16")
+        F = bench_problem(list(sizes[: i + 1]))
+        plan = _plan(s, s)
+        r = reps if reps is not None else max(3, int(4e7 / (float(s) * s)))
+        best = float("inf")
+        for _ in range(r):
+            t0 = time.perf_counter()
+            plan.solve_coeffs(F)
+            best = min(best, time.perf_counter() - t0)
+        rows.append(BenchRow(s, r, best))
+    return rows

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the oracle, plus size-independent properties at full size."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests need a B200 (there is no CPU fallback)")
+    import paper_1510_08094_b200 as p
+    return p
+
+
+def _coeff_cases():
+    out = []
+    for f in sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))):
+        d = np.load(f)
+        if "F" in d and "X" in d:
+            out.append(os.path.basename(f)[:-4])
+    return out
+
+
+def _assert_reference_bits(X, Xref, n):
+    """Bit-identical for every k != 0 column; k = 0 to rounding."""
+    cols = np.arange(n) != n // 2
+    np.testing.assert_array_equal(X[:, cols], Xref[:, cols])
+    scale = max(np.abs(Xref).max(), 1e-300)
+    assert np.abs(X[:, n // 2] - Xref[:, n // 2]).max() <= 1e-15 * scale + 1e-300
+
+
+@pytest.mark.parametrize("name", _coeff_cases())
+def test_coeff_solve_matches_reference_golden(pkg, name):
+    d = golden(name)
+    F = d["F"]
+    m, n = F.shape
+    sol = pkg.solve(pkg.PoissonProblem(m, n, F))
+    _assert_reference_bits(sol.x, d["X"], n)
+
+
+@pytest.mark.parametrize("s", [512, 1024, 2048])
+def test_coeff_solve_bench_workload_vs_oracle(pkg, oracle, s):
+    F = oracle.bench_problem([s])
+    with pkg.Plan(s, s) as plan:
+        X = plan.solve_coeffs(F)
+    _assert_reference_bits(X, oracle.solve(F, threads=8), s)
+
+
+@pytest.mark.parametrize("m,n,seed", [(64, 32, 1), (32, 64, 2), (150, 40, 3), (18, 22, 4)])
+def test_coeff_solve_rectangular_vs_oracle(pkg, oracle, m, n, seed):
+    F = oracle.random_mean_zero_problem(m, n, seed)
+    X = pkg.solve(pkg.PoissonProblem(m, n, F)).x
+    _assert_reference_bits(X, oracle.solve(F), n)
+
+
+def test_coeff_solve_errors(pkg):
+    d = golden("kat_precondition_16")
+    with pytest.raises(pkg.precondition_error):
+        pkg.solve(pkg.PoissonProblem(16, 16, d["F"]))
+    with pytest.raises(pkg.size_error):
+        pkg.solve(pkg.PoissonProblem(15, 16, np.zeros((15, 16), complex)))
+    X = pkg.solve(pkg.PoissonProblem(16, 16, np.zeros((16, 16), complex))).x
+    assert not X.any()
+
+
+def test_kat_cos_theta_and_residual(pkg):
+    d = golden("kat_cos_theta_64")
+    pb = pkg.PoissonProblem(64, 64, d["F"])
+    sol = pkg.solve(pb)
+    expect = np.zeros((64, 64), complex)
+    expect[31, 32] = expect[33, 32] = -0.25
+    assert np.abs(sol.x - expect).max() < 1e-13
+    r = pkg.residual(pb, sol)
+    assert r.interior_max < 1e-12 and r.constraint_abs < 1e-12
+    ref = d["residual"]
+    assert abs(r.interior_max - ref[0]) <= 1e-15 and abs(r.constraint_abs - ref[2]) <= 1e-15
+
+
+def test_residual_vs_oracle(pkg, oracle):
+    F = oracle.random_mean_zero_problem(32, 32, 5)
+    X = oracle.solve(F)
+    with pkg.Plan(32, 32) as plan:
+        r = plan.residual(F, X)
+        ro = oracle.residual(F, X)
+        assert abs(r.interior_max - ro[0]) <= 1e-15 and abs(r.replaced_row_abs - ro[1]) <= 1e-15
+        assert abs(r.constraint_abs - ro[2]) <= 1e-15
+        X2 = X.copy()
+        X2[7, 9] += 1e-3  # test_poisson.cpp:176-184
+        assert plan.residual(F, X2).interior_max > 1e-5
+
+
+def test_coeff_solve_batched_rhs(pkg, oracle):
+    Fs = np.stack([oracle.random_mean_zero_problem(64, 64, 100 + r) for r in range(5)])
+    with pkg.Plan(64, 64, nrhs=5) as plan:
+        X = plan.solve_coeffs(Fs)
+    for r in range(5):
+        _assert_reference_bits(X[r], oracle.solve(Fs[r]), 64)
+
+
+# ------------------------------------------------------------- grid path
+def _grid_cases():
+    return [os.path.basename(f)[:-4] for f in sorted(glob.glob(os.path.join(GOLDEN, "grid_sh_*.npz")))]
+
+
+@pytest.mark.parametrize("name", _grid_cases())
+def test_grid_solve_matches_reference_golden(pkg, name):
+    from oracle.oracle import phys_from_doubled
+    d = golden(name)
+    m, n = d["X"].shape
+    with pkg.Plan(m, n) as plan:
+        u, Xh = plan.solve_grid(d["phys"], coeffs=True)
+    uref = phys_from_doubled(d["U"], m).real
+    assert np.abs(u - uref).max() <= 1e-10 * np.abs(uref).max()
+    Xref = d["X"][:, n // 2:].T  # k = 0..N/2-1 columns
+    assert np.abs(Xh[: n // 2] - Xref).max() <= 1e-10 * np.abs(d["X"]).max()
+    # the analytic solution
+    assert np.abs(u - d["u_exact"]).max() <= 1e-12 * np.abs(d["u_exact"]).max()
+
+
+@pytest.mark.parametrize("m,n,L", [(512, 256, 32), (112, 98, 20), (160, 90, 30), (40, 12, 4), (8, 4, 1)])
+def test_grid_solve_vs_oracle(pkg, oracle, m, n, L):
+    from paper_1510_08094_b200 import inputs
+    c = inputs.sh_coeffs(m + n, L, 2.0)
+    f = oracle.shgen(m, n, L, c)
+    _, _, u_ref, _ = oracle.grid_pipeline(f, m, threads=4)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+def test_grid_solve_rough_data_vs_oracle(pkg, oracle):
+    """Non-band-limited (random) data with zero mean: parity holds to rounding
+    only where the k<0 half is the mirror of k>=0 (real data)."""
+    rng = np.random.default_rng(3)
+    m, n = 64, 48
+    f = rng.standard_normal((m // 2 + 1, n))
+    # remove the surface mean (the constant 1 has w^T e_0 = 2)
+    g = oracle.dfs_double(f, m)
+    A = oracle.analyze_2d(g)
+    w = oracle.integration_weights(m)
+    mu = (w * A[:, n // 2]).sum() / 2.0  # mean of f~ relative to the constant 1 (w^T e_0 = 2)
+    f = f - mu.real
+    _, _, u_ref, _ = oracle.grid_pipeline(f, m)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+def test_grid_precondition_error(pkg):
+    m, n = 32, 16
+    f = np.ones((m // 2 + 1, n))
+    with pkg.Plan(m, n) as plan:
+        with pytest.raises(pkg.precondition_error):
+            plan.solve_grid(f)
+
+
+def test_shgen_vs_oracle(pkg, oracle):
+    import torch
+    from paper_1510_08094_b200 import inputs
+    m, n, L = 96, 80, 30
+    c = inputs.sh_coeffs(5, L, 2.0)
+    ref = oracle.shgen(m, n, L, c)
+    with pkg.Plan(m, n) as plan:
+        cd = torch.from_numpy(c).cuda()
+        out = torch.empty((m // 2 + 1, n), dtype=torch.float64, device="cuda")
+        plan.shgen(L, cd, out)
+        torch.cuda.synchronize()
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_grid_batched_rhs_bitwise(pkg, oracle):
+    from paper_1510_08094_b200 import inputs
+    m, n, L = 128, 64, 20
+    fs = np.stack([oracle.shgen(m, n, L, inputs.sh_coeffs(40 + r, L, 1.5)) for r in range(3)])
+    with pkg.Plan(m, n, nrhs=3) as plan:
+        ub = plan.solve_grid(fs)
+    with pkg.Plan(m, n) as plan:
+        for r in range(3):
+            assert np.array_equal(plan.solve_grid(fs[r]), ub[r])
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_slab_stages_bitwise_equal_single_gpu(pkg, oracle, P):
+    """The multi-rank slab path (stage entry points + the all-to-all block
+    layout) emulated on one GPU with device copies: bit-identical to the
+    single-GPU solve."""
+    import torch
+    from paper_1510_08094_b200 import distributed as dist_mod, inputs
+    m, n, L = 160, 96, 24
+    f = oracle.shgen(m, n, L, inputs.sh_coeffs(9, L, 2.0))
+    with pkg.Plan(m, n) as plan:
+        u1 = plan.solve_grid(f)
+    u = dist_mod.emulate_slabs(f, m, n, P)
+    assert np.array_equal(u, u1)
+
+
+def test_grid_full_size_analytic_C2(pkg):
+    """Size-independent property at config C2 (4096 x 2048, L = 512): the
+    grid solve reproduces the analytic solution -sum c_lm Y/(l(l+1))."""
+    import torch
+    from paper_1510_08094_b200 import inputs
+    cfg = inputs.CONFIGS["C2"]
+    with pkg.Plan(cfg.M, cfg.N) as plan:
+        rows = cfg.M // 2 + 1
+        f = torch.empty((rows, cfg.N), dtype=torch.float64, device="cuda")
+        ue = torch.empty_like(f)
+        plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(2, cfg.L, cfg.p)).cuda(), f)
+        plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(2, cfg.L, cfg.p, solution=True)).cuda(), ue)
+        u = plan.solve_grid(f)
+        torch.cuda.synchronize()
+        err = (u - ue).abs().max().item() / ue.abs().max().item()
+    assert err <= 1e-10, err

@@ -1,0 +1,107 @@
+"""CPU: pin the oracle (C++ restatement) against the reference's golden
+vectors and, where it was built, against the reference library itself."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+
+def _golden_solves():
+    out = []
+    for f in sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))):
+        d = np.load(f)
+        if "F" in d and "X" in d:
+            out.append(os.path.basename(f)[:-4])
+    return out
+
+
+@pytest.mark.parametrize("name", _golden_solves())
+def test_oracle_solve_bit_identical_to_reference_golden(oracle, name):
+    d = golden(name)
+    X = oracle.solve(d["F"], threads=2)
+    assert np.array_equal(X, d["X"])
+
+
+def test_kat_cos_theta(oracle):
+    # test_poisson.cpp:53-67: X = -1/4 at (i=31,33; kc=32), else 0, to 1e-13
+    d = golden("kat_cos_theta_64")
+    X = oracle.solve(d["F"])
+    expect = np.zeros((64, 64), complex)
+    expect[31, 32] = expect[33, 32] = -0.25
+    assert np.abs(X - expect).max() < 1e-13
+    r = oracle.residual(d["F"], X)
+    assert r[0] < 1e-12 and r[2] < 1e-12
+
+
+def test_precondition_error(oracle):
+    from oracle.oracle import OracleError
+    d = golden("kat_precondition_16")
+    assert int(d["expected_code"]) == 2
+    with pytest.raises(OracleError) as e:
+        oracle.solve(d["F"])
+    assert e.value.code == 2
+
+
+def test_zero_rhs_gives_zero(oracle):
+    X = oracle.solve(np.zeros((16, 16), complex))
+    assert not X.any()
+
+
+def test_size_errors(oracle):
+    from oracle.oracle import OracleError
+    with pytest.raises(OracleError) as e:
+        oracle.solve(np.zeros((15, 16), complex))
+    assert e.value.code == 1
+
+
+def test_bordered_zero_mode(oracle):
+    d = golden("bordered_zero_mode_32")
+    x = oracle.band_solve_dense_row(d["lap"], 2, 2, 16, d["w"], 0j, d["b"])
+    assert np.array_equal(x, d["x"])
+
+
+@pytest.mark.parametrize("name", [os.path.basename(f)[:-4] for f in sorted(glob.glob(os.path.join(GOLDEN, "grid_sh_*.npz")))])
+def test_oracle_grid_pipeline_matches_reference(oracle, name):
+    d = golden(name)
+    m = d["X"].shape[0]
+    X, U, up, mean = oracle.grid_pipeline(d["phys"], m)
+    assert np.array_equal(X, d["X"]) and np.array_equal(U, d["U"])
+    # and the reference composition reproduces the analytic solution
+    assert np.abs(up - d["u_exact"]).max() <= 1e-13 * np.abs(d["u_exact"]).max()
+
+
+def test_fourier_conventions(oracle):
+    d = golden("fourier_pure_modes_16")
+    xs = -np.pi + 2 * np.pi * np.arange(16) / 16
+    assert np.abs(oracle.analyze_1d(np.ones(16, complex)) - d["const"]).max() < 1e-15
+    c = oracle.analyze_1d(np.exp(3j * xs))
+    assert np.abs(c - d["e3"]).max() < 1e-15
+    assert abs(c[8 + 3] - 1) < 1e-15
+
+
+def test_lap_and_weights_match_reference(oracle, reference):
+    for m in (8, 16, 150, 512, 4096):
+        assert np.array_equal(oracle.build_lap(m), reference.build_lap(m).real)
+        assert not reference.build_lap(m).imag.any()
+        assert np.array_equal(oracle.integration_weights(m), reference.integration_weights(m).real)
+
+
+@pytest.mark.parametrize("s", [64, 512])
+def test_oracle_vs_reference_bench_problem(oracle, reference, s):
+    F = reference.bench_problem([s])
+    assert np.array_equal(F, oracle.bench_problem([s]))
+    assert np.array_equal(oracle.solve(F, 4), reference.solve(F, 4))
+
+
+def test_oracle_vs_reference_dfs_and_fft(oracle, reference):
+    rng = np.random.default_rng(5)
+    for m, n in [(8, 6), (150, 150), (64, 602)]:
+        phys = rng.standard_normal((m // 2 + 1, n))
+        assert np.array_equal(oracle.dfs_double(phys, m), reference.sample_dfs_phys(phys, m))
+        g = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+        assert np.array_equal(oracle.analyze_2d(g), reference.analyze_2d(g))
+        X = reference.analyze_2d(g)
+        assert np.array_equal(oracle.sample_grid(X, m, n), reference.sample_grid(X, m, n))

@@ -286,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2* s_hi = a + L;
     double2* s_lo = s_hi + P.fd.nhi;
     double* inv = reinterpret_cast<double*>(s_lo + P.fd.nlo);
-    V4* wsc = reinterpret_cast<V4*>(inv + (L / 2 + 2));
+    V4* wsc = reinterpret_cast<V4*>(inv + theta_chain_slots(L));
     double2* misc = reinterpret_cast<double2*>(wsc + 32);
     double* red = reinterpret_cast<double*>(misc + 16);
 

@@ -59,9 +59,13 @@ struct ResidualParams {
     double* out;  // [0] interior max, [1] replaced-row abs, [2..3] constraint sum (re, im)
 };
 
+// Pivot-reciprocal slots of the theta kernel (even, so later regions stay
+// 16-byte aligned).
+__host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 2) + 1) & ~1; }
+
 // Dynamic shared memory of theta_kernel (bytes).
 __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
-    const size_t chain_max = static_cast<size_t>(L / 2 + 2);
+    const size_t chain_max = static_cast<size_t>(theta_chain_slots(L));
     return static_cast<size_t>(L) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
            16 * 16 + 64 * 8;
 }

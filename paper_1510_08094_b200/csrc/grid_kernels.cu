@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(512) lambda_fwd_kernel(LambdaParams P) {
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    __syncthreads();
     const double2* src =
         reinterpret_cast<const double2*>(P.f + rhs * P.in_rhs_stride + static_cast<long long>(row) * P.g.N);
     for (int j = tid; j < L; j += nthr) a[j] = __ldg(src + j);
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(512) lambda_inv_kernel(LambdaParams P) {
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    __syncthreads();  // the pre-processing below reads the staged twiddles
     const double2* in = P.spec + rhs * P.in_rhs_stride;
     const int* rev = P.fd.rev;
     for (int k = tid; k <= L / 2; k += nthr) {
@@ -162,9 +164,60 @@ __device__ __forceinline__ double msin2_diag(int t, int L) { return (t == -L || 
 // the pivot recurrence, affine compositions of the two sweeps), so the result
 // equals a sequential Thomas sweep up to rounding.
 __device__ void solve_chain(double2* a, const int* rev, double* inv, V4* wsc, const Chain& ch, int L, double k2,
-                            double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
+                            double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first,
+                            bool sequential) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int n = ch.n;
+    if (sequential) {
+        // Low lambda modes (k^2 small against j^2/2) are only weakly diagonally
+        // dominant; the scan formulation below loses digits there, so these
+        // columns run the plain ascending Thomas recurrence in one thread.
+        if (tid == 0 && n > 0) {
+            const bool upc = ch.dt > 0;
+            auto tq = [&](int i) { return ch.t0 + ch.dt * i; };
+            auto pq = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
+            double2 xm = inner, x0 = a[pq(0)];
+            double ip = 0.0, cprev = 0.0;
+            double2 rp = make_double2(0.0, 0.0);
+            for (int i = 0; i < n; ++i) {
+                const int t = tq(i);
+                const double2 xp = (i + 1 < n) ? a[pq(i + 1)] : make_double2(0.0, 0.0);
+                const double d2 = msin2_diag(t, L);
+                const double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+                fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+                const double A = upc ? lap_lower(t, L) : lap_upper(t, L);
+                const double d = lap_diag(t, L) - k2 - A * cprev * ip;
+                const double al = -A * ip;
+                rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
+                a[pq(i)] = rp;
+                ip = 1.0 / d;
+                inv[i] = ip;
+                cprev = upc ? lap_upper(t, L) : lap_lower(t, L);
+                xm = x0;
+                x0 = xp;
+            }
+            double2 x = make_double2(0.0, 0.0);
+            double2 ws = make_double2(0.0, 0.0);
+            for (int i = n - 1; i >= 0; --i) {
+                const int t = tq(i);
+                const double C = upc ? lap_upper(t, L) : lap_lower(t, L);
+                const double iv = inv[i];
+                const double2 r = a[pq(i)];
+                x = make_double2((r.x - C * x.x) * iv, (r.y - C * x.y) * iv);
+                a[pq(i)] = x;
+                if (want_wsum) {
+                    const double w = 2.0 / (1.0 - (double)t * t);
+                    ws.x = fma(w, x.x, ws.x);
+                    ws.y = fma(w, x.y, ws.y);
+                }
+            }
+            *x_first = x;
+            wsum.x += ws.x;
+            wsum.y += ws.y;
+        }
+        __syncthreads();
+        return;
+    }
     const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
     const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
     const bool up = ch.dt > 0;
@@ -377,8 +430,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
     __syncthreads();
-    solve_chain(a, rev, inv, wsc, cp, L, k2, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    solve_chain(a, rev, inv, wsc, cm, L, k2, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    const bool seq = kg < P.kseq;
+    solve_chain(a, rev, inv, wsc, cp, L, k2, inner_p, fmax_acc, wsum, want_wsum, &misc[3], seq);
+    solve_chain(a, rev, inv, wsc, cm, L, k2, inner_m, fmax_acc, wsum, want_wsum, &misc[4], seq);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
         double2 x0;

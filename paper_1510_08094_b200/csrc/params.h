@@ -33,6 +33,7 @@ struct ThetaParams {
     long long rhs_stride;  // complex per rhs in buf
     double* stats;    // per rhs: [0..1] mean (re, im), [2] max|F|, [3] unused
     double2* xhalf;   // optional: solution coefficients X[k][i], (N/2+1) x M per rhs
+    int kseq;         // lambda modes k < kseq use the sequential Thomas recurrence
 };
 
 struct ShgenParams {

@@ -157,12 +157,20 @@ __device__ __forceinline__ void dft(double2* x) {
 }
 
 // ------------------------------------------------------------------- stages
+__device__ __forceinline__ int fdiv(int n, unsigned mag, int sh1, int sh2) {
+    const unsigned t = __umulhi(static_cast<unsigned>(n), mag);
+    return static_cast<int>((t + ((static_cast<unsigned>(n) - t) >> sh1)) >> sh2);
+}
+
 // Forward DIF stage: x_q = a[base + q span]; y = DFT_R(x); y_q *= w^(q j).
 template <int R>
-__device__ __forceinline__ void dif_stage(double2* a, int L, int span, int tw, const Tw& T, int tid, int nthr) {
-    const int nb = L / R;
+__device__ __forceinline__ void dif_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
+    const int span = d.span[s], tw = d.tw[s];
+    const unsigned mag = d.mag[s];
+    const int sh1 = d.sh1[s], sh2 = d.sh2[s];
+    const int nb = d.L / R;
     for (int b = tid; b < nb; b += nthr) {
-        const int g = b / span;
+        const int g = fdiv(b, mag, sh1, sh2);
         const int j = b - g * span;
         const int base = g * span * R + j;
         double2 x[R];
@@ -170,30 +178,43 @@ __device__ __forceinline__ void dif_stage(double2* a, int L, int span, int tw, c
         for (int q = 0; q < R; ++q) x[q] = a[base + q * span];
         dft<R, -1>(x);
         a[base] = x[0];
-        const int step = j * tw;
+        if (j == 0) {
 #pragma unroll
-        for (int q = 1; q < R; ++q) {
-            const double2 w = T(q * step);
-            a[base + q * span] = j == 0 ? x[q] : cmul(x[q], w);
+            for (int q = 1; q < R; ++q) a[base + q * span] = x[q];
+        } else {
+            const double2 w1 = T(j * tw);
+            double2 w = w1;
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                a[base + q * span] = cmul(x[q], w);
+                if (q + 1 < R) w = cmul(w, w1);
+            }
         }
     }
 }
 
 // Inverse DIT stage: x_q = a[base + q span] * conj(w)^(q j); y = DFT^+_R(x).
 template <int R>
-__device__ __forceinline__ void dit_stage(double2* a, int L, int span, int tw, const Tw& T, int tid, int nthr) {
-    const int nb = L / R;
+__device__ __forceinline__ void dit_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
+    const int span = d.span[s], tw = d.tw[s];
+    const unsigned mag = d.mag[s];
+    const int sh1 = d.sh1[s], sh2 = d.sh2[s];
+    const int nb = d.L / R;
     for (int b = tid; b < nb; b += nthr) {
-        const int g = b / span;
+        const int g = fdiv(b, mag, sh1, sh2);
         const int j = b - g * span;
         const int base = g * span * R + j;
         double2 x[R];
-        x[0] = a[base];
-        const int step = j * tw;
 #pragma unroll
-        for (int q = 1; q < R; ++q) {
-            const double2 v = a[base + q * span];
-            x[q] = j == 0 ? v : cmulc(v, T(q * step));
+        for (int q = 0; q < R; ++q) x[q] = a[base + q * span];
+        if (j != 0) {
+            const double2 w1 = T(j * tw);
+            double2 w = w1;
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                x[q] = cmulc(x[q], w);
+                if (q + 1 < R) w = cmul(w, w1);
+            }
         }
         dft<R, +1>(x);
 #pragma unroll
@@ -206,12 +227,12 @@ __device__ __forceinline__ void dit_stage(double2* a, int L, int span, int tw, c
 __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     for (int s = 0; s < d.nst; ++s) {
         switch (d.R[s]) {
-            case 2: dif_stage<2>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 3: dif_stage<3>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 4: dif_stage<4>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 5: dif_stage<5>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 7: dif_stage<7>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            default: dif_stage<8>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 2: dif_stage<2>(a, d, s, T, tid, nthr); break;
+            case 3: dif_stage<3>(a, d, s, T, tid, nthr); break;
+            case 4: dif_stage<4>(a, d, s, T, tid, nthr); break;
+            case 5: dif_stage<5>(a, d, s, T, tid, nthr); break;
+            case 7: dif_stage<7>(a, d, s, T, tid, nthr); break;
+            default: dif_stage<8>(a, d, s, T, tid, nthr); break;
         }
         __syncthreads();
     }
@@ -220,12 +241,12 @@ __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const 
 __device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     for (int s = d.nst - 1; s >= 0; --s) {
         switch (d.R[s]) {
-            case 2: dit_stage<2>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 3: dit_stage<3>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 4: dit_stage<4>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 5: dit_stage<5>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            case 7: dit_stage<7>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
-            default: dit_stage<8>(a, d.L, d.span[s], d.tw[s], T, tid, nthr); break;
+            case 2: dit_stage<2>(a, d, s, T, tid, nthr); break;
+            case 3: dit_stage<3>(a, d, s, T, tid, nthr); break;
+            case 4: dit_stage<4>(a, d, s, T, tid, nthr); break;
+            case 5: dit_stage<5>(a, d, s, T, tid, nthr); break;
+            case 7: dit_stage<7>(a, d, s, T, tid, nthr); break;
+            default: dit_stage<8>(a, d, s, T, tid, nthr); break;
         }
         __syncthreads();
     }

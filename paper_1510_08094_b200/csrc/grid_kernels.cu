@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(512) lambda_inv_kernel(LambdaParams P) {
 }
 
 // -------------------------------------------------------------- theta stage
-
 // theta-mode index of natural FFT index tau in parity class par (t = 2 tau + par
 // folded into [-M/2, M/2)).
 __device__ __forceinline__ int t_of(int tau, int par, int L) {
@@ -131,6 +130,10 @@ __device__ __forceinline__ int t_of(int tau, int par, int L) {
     return t < L ? t : t - 2 * L;
 }
 
+// The four chains of one lambda mode.  Parity class par (t = 2 tau + par),
+// side +: t = t0, t0+2, ... (tau ascending from tau0), side -: t = -2+par,
+// -4+par, ... (tau descending from L-1).  Element i of a chain is coupled to
+// i-1 (towards j = 0) and i+1 (towards the truncation boundary).
 struct Chain {
     int n;       // length
     int tau0;    // natural FFT index of element 0
@@ -138,6 +141,16 @@ struct Chain {
     int t0;      // theta mode of element 0
     int dt;      // +2 or -2
 };
+
+__device__ __forceinline__ void make_chains(int par, int L, Chain& cp, Chain& cm) {
+    if (par == 0) {
+        cp = Chain{(L - 1 >= 2) ? (L - 1 - 2) / 2 + 1 : 0, 1, +1, 2, +2};
+        cm = Chain{(L >= 2) ? (L - 2) / 2 + 1 : 0, L - 1, -1, -2, -2};
+    } else {
+        cp = Chain{(L - 1 >= 1) ? (L - 1 - 1) / 2 + 1 : 0, 0, +1, 1, +2};
+        cm = Chain{(L >= 1) ? (L - 1) / 2 + 1 : 0, L - 1, -1, -1, -2};
+    }
+}
 
 // Coefficients of row t of (lap - k^2) (poisson.cpp:15-40 closed form; the
 // +-1 offsets are exact zeros): lower = lap[t][t-2], upper = lap[t][t+2].
@@ -156,76 +169,65 @@ __device__ __forceinline__ double lap_diag(int t, int L) {
 // Msin^2 diagonal (poisson.cpp:61; 1/4 on the first and last rows)
 __device__ __forceinline__ double msin2_diag(int t, int L) { return (t == -L || t == L - 1) ? 0.25 : 0.5; }
 
-// Solves one chain of the per-mode system in place.  The chain's rows are
-// a_i x_{i-1} + b_i x_i + c_i x_{i+1} = F_i with F = Msin^2 X computed on the
-// fly from the transform output.  Each thread owns a contiguous segment; the
-// Thomas recurrences (pivots d'_i, forward r'_i, backward x_i) are evaluated
-// as segment-local passes joined by three block scans (Moebius composition of
-// the pivot recurrence, affine compositions of the two sweeps), so the result
-// equals a sequential Thomas sweep up to rounding.
-__device__ void solve_chain(double2* a, const int* rev, double* inv, V4* wsc, const Chain& ch, int L, double k2,
-                            double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first,
-                            bool sequential) {
+// chain-local coefficients: A couples to element i-1, C to element i+1
+__device__ __forceinline__ double chainA(const Chain& ch, int i, int L) {
+    const int t = ch.t0 + ch.dt * i;
+    return ch.dt > 0 ? lap_lower(t, L) : lap_upper(t, L);
+}
+__device__ __forceinline__ double chainC(const Chain& ch, int i, int L) {
+    const int t = ch.t0 + ch.dt * i;
+    return ch.dt > 0 ? lap_upper(t, L) : lap_lower(t, L);
+}
+
+// Pivot table: for every lambda mode k >= 0 and parity class, the reciprocal
+// Thomas pivots 1/d'_i of both chains, indexed by the natural FFT index tau
+// of the element: ipt[(k * 2 + par) * L + tau].  The pivots depend only on
+// (M, k), so they are computed once per plan by the sequential recurrence
+// d'_0 = b_0, d'_i = b_i - a_i c_{i-1} / d'_{i-1} — the same recurrence the
+// reference's band_solve runs (banded.cpp:121-147, no row ever swaps for
+// these systems) — which keeps the parallel sweeps below as accurate as the
+// sequential algorithm.
+__global__ void __launch_bounds__(128) pivot_table_kernel(int L, int k0, int ncols, double* ipt) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= ncols * 4) return;
+    const int kl = id >> 2, par = (id >> 1) & 1, side = id & 1;
+    const int kg = k0 + kl;
+    const double k2 = static_cast<double>(kg) * static_cast<double>(kg);
+    Chain cp, cm;
+    make_chains(par, L, cp, cm);
+    const Chain& ch = side == 0 ? cp : cm;
+    double* out = ipt + (static_cast<size_t>(kl) * 2 + par) * L;
+    double ip = 0.0, cprev = 0.0;
+    for (int i = 0; i < ch.n; ++i) {
+        const int t = ch.t0 + ch.dt * i;
+        const double A = chainA(ch, i, L);
+        const double d = lap_diag(t, L) - k2 - A * cprev * ip;
+        ip = 1.0 / d;
+        out[ch.tau0 + ch.dtau * i] = ip;
+        cprev = chainC(ch, i, L);
+    }
+}
+
+// Solves one chain in place: rows a_i x_{i-1} + b_i x_i + c_i x_{i+1} = F_i
+// with F = Msin^2 X computed on the fly from the transform output.  With the
+// pivots given, the Thomas sweeps are two affine recurrences
+//   r'_i = F_i + alpha_i r'_{i-1},   alpha_i = -a_i / d'_{i-1}
+//   x_i  = r'_i / d'_i + beta_i x_{i+1},  beta_i = -c_i / d'_i
+// Each thread owns a contiguous segment: a local pass composes its segment's
+// affine map, a block scan gives every segment its incoming value, and a
+// second pass applies it.  `ip` holds the chain's pivots (shared memory,
+// chain-element order).
+__device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* wsc, const Chain& ch, int L,
+                            double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int n = ch.n;
-    if (sequential) {
-        // Low lambda modes (k^2 small against j^2/2) are only weakly diagonally
-        // dominant; the scan formulation below loses digits there, so these
-        // columns run the plain ascending Thomas recurrence in one thread.
-        if (tid == 0 && n > 0) {
-            const bool upc = ch.dt > 0;
-            auto tq = [&](int i) { return ch.t0 + ch.dt * i; };
-            auto pq = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
-            double2 xm = inner, x0 = a[pq(0)];
-            double ip = 0.0, cprev = 0.0;
-            double2 rp = make_double2(0.0, 0.0);
-            for (int i = 0; i < n; ++i) {
-                const int t = tq(i);
-                const double2 xp = (i + 1 < n) ? a[pq(i + 1)] : make_double2(0.0, 0.0);
-                const double d2 = msin2_diag(t, L);
-                const double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
-                fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
-                const double A = upc ? lap_lower(t, L) : lap_upper(t, L);
-                const double d = lap_diag(t, L) - k2 - A * cprev * ip;
-                const double al = -A * ip;
-                rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
-                a[pq(i)] = rp;
-                ip = 1.0 / d;
-                inv[i] = ip;
-                cprev = upc ? lap_upper(t, L) : lap_lower(t, L);
-                xm = x0;
-                x0 = xp;
-            }
-            double2 x = make_double2(0.0, 0.0);
-            double2 ws = make_double2(0.0, 0.0);
-            for (int i = n - 1; i >= 0; --i) {
-                const int t = tq(i);
-                const double C = upc ? lap_upper(t, L) : lap_lower(t, L);
-                const double iv = inv[i];
-                const double2 r = a[pq(i)];
-                x = make_double2((r.x - C * x.x) * iv, (r.y - C * x.y) * iv);
-                a[pq(i)] = x;
-                if (want_wsum) {
-                    const double w = 2.0 / (1.0 - (double)t * t);
-                    ws.x = fma(w, x.x, ws.x);
-                    ws.y = fma(w, x.y, ws.y);
-                }
-            }
-            *x_first = x;
-            wsum.x += ws.x;
-            wsum.y += ws.y;
-        }
-        __syncthreads();
-        return;
-    }
     const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
     const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
-    const bool up = ch.dt > 0;
-    auto tt = [&](int i) { return ch.t0 + ch.dt * i; };
     auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
-    auto A = [&](int i) { return up ? lap_lower(tt(i), L) : lap_upper(tt(i), L); };
-    auto C = [&](int i) { return (i < 0) ? 0.0 : (up ? lap_upper(tt(i), L) : lap_lower(tt(i), L)); };
-    auto B = [&](int i) { return lap_diag(tt(i), L) - k2; };
+    auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
+        const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
+        return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+    };
     // boundary neighbours (original transform values) before anyone writes
     double2 xlo = make_double2(0.0, 0.0), xhi = make_double2(0.0, 0.0);
     if (s < e) {
@@ -234,95 +236,131 @@ __device__ void solve_chain(double2* a, const int* rev, double* inv, V4* wsc, co
     }
     __syncthreads();
 
-    // ---- pass A: Moebius product of the pivot recurrence over the segment
-    V4 mob = MobOp::identity();
-    for (int i = s; i < e; ++i) {
-        const V4 Mi{B(i), -A(i) * C(i - 1), 1.0, 0.0};
-        mob = MobOp::combine(mob, Mi);
-    }
-    const V4 min = block_exclusive_scan<MobOp, false>(mob, wsc);
-    // state [p; q] = min * [1; 0]; 1/d'_{s-1} = q / p
-    double inv_prev = (min.a != 0.0) ? min.c / min.a : 0.0;
-
-    // ---- pass B: pivots (stored as reciprocals) and the local forward sweep
-    auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
-        const int t = tt(i);
-        const double d2 = msin2_diag(t, L);
-        return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
-    };
+    // ---- local forward summary: r'_{e-1} = P r'_{s-1} + rt
     V4 aff = AffOp::identity();
     {
         double2 xm = xlo;
         double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
-        double ip = inv_prev;
+        double ipp = (s > 0) ? ip[s - 1] : 0.0;
         for (int i = s; i < e; ++i) {
             const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
             const double2 F = Fof(xm, x0, xp, i);
-            const double d = B(i) - A(i) * C(i - 1) * ip;
-            const double iv = 1.0 / d;
-            inv[i] = iv;
-            const double al = -A(i) * ip;
-            aff = AffOp::combine(aff, V4{al, F.x, F.y, 0.0});
-            ip = iv;
+            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+            const double al = -chainA(ch, i, L) * ipp;
+            aff = V4{al * aff.a, fma(al, aff.b, F.x), fma(al, aff.c, F.y), 0.0};
+            ipp = ip[i];
             xm = x0;
             x0 = xp;
         }
     }
     const V4 rin = block_exclusive_scan<AffOp, false>(aff, wsc);  // r'_{s-1} = rin.(b, c)
 
-    // ---- pass C: forward sweep with the true incoming value, r' in place
-    double2 bsum_x = make_double2(0.0, 0.0);
+    // ---- forward sweep with the true incoming value, r' in place
     {
         double2 rp = make_double2(rin.b, rin.c);
-        double ip = (s > 0) ? inv[s - 1] : 0.0;
+        double ipp = (s > 0) ? ip[s - 1] : 0.0;
         double2 xm = xlo;
         double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
         for (int i = s; i < e; ++i) {
+            const int pi = pos(i);
             const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
             const double2 F = Fof(xm, x0, xp, i);
-            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
-            const double al = -A(i) * ip;
+            const double al = -chainA(ch, i, L) * ipp;
             rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
-            a[pos(i)] = rp;
-            ip = inv[i];
+            a[pi] = rp;
+            ipp = ip[i];
             xm = x0;
             x0 = xp;
         }
     }
     __syncthreads();
 
-    // ---- pass D: local backward summary x_s = P x_e + xt
+    // ---- local backward summary x_s = P x_e + xt
     V4 baff = AffOp::identity();
     for (int i = e - 1; i >= s; --i) {
-        const double iv = inv[i];
+        const double iv = ip[i];
         const double2 r = a[pos(i)];
-        baff = AffOp::combine(baff, V4{-C(i) * iv, r.x * iv, r.y * iv, 0.0});
+        const double be = -chainC(ch, i, L) * iv;
+        baff = V4{be * baff.a, fma(be, baff.b, r.x * iv), fma(be, baff.c, r.y * iv), 0.0};
     }
     const V4 xin = block_exclusive_scan<AffOp, true>(baff, wsc);  // x_e
 
-    // ---- pass E: back substitution, x in place
+    // ---- back substitution, x in place
+    double2 ws = make_double2(0.0, 0.0);
     {
         double2 x = make_double2(xin.b, xin.c);
         for (int i = e - 1; i >= s; --i) {
-            const double iv = inv[i];
-            const double2 r = a[pos(i)];
-            const double c = -C(i) * iv;
+            const int pi = pos(i);
+            const double iv = ip[i];
+            const double2 r = a[pi];
+            const double c = -chainC(ch, i, L) * iv;
             x = make_double2(fma(c, x.x, r.x * iv), fma(c, x.y, r.y * iv));
-            a[pos(i)] = x;
+            a[pi] = x;
             if (want_wsum) {
-                const double t = tt(i);
+                const double t = ch.t0 + ch.dt * i;
                 const double w = 2.0 / (1.0 - t * t);
-                bsum_x.x = fma(w, x.x, bsum_x.x);
-                bsum_x.y = fma(w, x.y, bsum_x.y);
+                ws.x = fma(w, x.x, ws.x);
+                ws.y = fma(w, x.y, ws.y);
             }
             if (i == 0) *x_first = x;
         }
     }
-    wsum.x += bsum_x.x;
-    wsum.y += bsum_x.y;
+    wsum.x += ws.x;
+    wsum.y += ws.y;
     __syncthreads();
 }
 
+// The lowest lambda modes are only weakly diagonally dominant (k = 0 not at
+// all); for them the segmented sweeps lose digits, so one thread runs the
+// plain sequential recurrences (pivots from the table).
+__device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, const Chain& ch, int L, double2 inner,
+                                double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
+    if (threadIdx.x == 0 && ch.n > 0) {
+        const int n = ch.n;
+        auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
+        double2 xm = inner, x0 = a[pos(0)];
+        double2 rp = make_double2(0.0, 0.0);
+        double ipp = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double2 xp = (i + 1 < n) ? a[pos(i + 1)] : make_double2(0.0, 0.0);
+            const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
+            const double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+            const double al = -chainA(ch, i, L) * ipp;
+            rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
+            a[pos(i)] = rp;
+            ipp = ip[i];
+            xm = x0;
+            x0 = xp;
+        }
+        double2 x = make_double2(0.0, 0.0);
+        double2 ws = make_double2(0.0, 0.0);
+        for (int i = n - 1; i >= 0; --i) {
+            const int pi = pos(i);
+            const double iv = ip[i];
+            const double2 r = a[pi];
+            const double c = -chainC(ch, i, L) * iv;
+            x = make_double2(fma(c, x.x, r.x * iv), fma(c, x.y, r.y * iv));
+            a[pi] = x;
+            if (want_wsum) {
+                const double t = ch.t0 + ch.dt * i;
+                const double w = 2.0 / (1.0 - t * t);
+                ws.x = fma(w, x.x, ws.x);
+                ws.y = fma(w, x.y, ws.y);
+            }
+        }
+        *x_first = x;
+        wsum.x += ws.x;
+        wsum.y += ws.y;
+    }
+    __syncthreads();
+}
+
+// Load a chain's pivots from the plan table into shared memory (chain order).
+__device__ __forceinline__ void load_pivots(double* ip, const double* tab, const Chain& ch) {
+    for (int i = threadIdx.x; i < ch.n; i += blockDim.x) ip[i] = __ldg(tab + ch.tau0 + ch.dtau * i);
+    __syncthreads();
+}
 
 // One 2-CTA cluster per lambda mode k: CTA `par` (0/1) owns the theta modes
 // of parity par.  Folding the DFS-symmetric column onto the two parity
@@ -338,8 +376,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2* a = reinterpret_cast<double2*>(smem_raw);
     double2* s_hi = a + L;
     double2* s_lo = s_hi + P.fd.nhi;
-    double* inv = reinterpret_cast<double*>(s_lo + P.fd.nlo);
-    V4* wsc = reinterpret_cast<V4*>(inv + theta_chain_slots(L));
+    double* ip = reinterpret_cast<double*>(s_lo + P.fd.nlo);
+    V4* wsc = reinterpret_cast<V4*>(ip + theta_chain_slots(L));
     double2* misc = reinterpret_cast<double2*>(wsc + 32);
     double* red = reinterpret_cast<double*>(misc + 16);
 
@@ -353,6 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const double sgn = (kg & 1) ? -1.0 : 1.0;
     const int* rev = P.fd.rev;
     double2* colbase = P.buf + rhs * P.rhs_stride;
+    const double* ptab = P.pivots + (static_cast<size_t>(kl) * 2 + par) * L;
 
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     __syncthreads();
@@ -398,13 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
 
     // ---- chains
     Chain cp, cm;
-    if (par == 0) {
-        cp = Chain{(L - 1 >= 2) ? (L - 1 - 2) / 2 + 1 : 0, 1, +1, 2, +2};
-        cm = Chain{(L >= 2) ? (L - 2) / 2 + 1 : 0, L - 1, -1, -2, -2};
-    } else {
-        cp = Chain{(L - 1 >= 1) ? (L - 1 - 1) / 2 + 1 : 0, 0, +1, 1, +2};
-        cm = Chain{(L >= 1) ? (L - 1) / 2 + 1 : 0, L - 1, -1, -1, -2};
-    }
+    make_chains(par, L, cp, cm);
     // inner neighbours and the j = 0 row data, read before any chain writes
     if (tid == 0) {
         if (par == 0) {
@@ -429,10 +462,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double fmax_acc = (par == 0) ? sqrt(F0.x * F0.x + F0.y * F0.y) : 0.0;
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
-    __syncthreads();
     const bool seq = kg < P.kseq;
-    solve_chain(a, rev, inv, wsc, cp, L, k2, inner_p, fmax_acc, wsum, want_wsum, &misc[3], seq);
-    solve_chain(a, rev, inv, wsc, cm, L, k2, inner_m, fmax_acc, wsum, want_wsum, &misc[4], seq);
+    load_pivots(ip, ptab, cp);
+    if (seq) solve_chain_seq(a, rev, ip, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    else solve_chain(a, rev, ip, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    load_pivots(ip, ptab, cm);
+    if (seq) solve_chain_seq(a, rev, ip, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    else solve_chain(a, rev, ip, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
         double2 x0;
@@ -573,6 +609,12 @@ cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream
         attr = true;
     }
     theta_kernel<<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, cudaStream_t st) {
+    const int n = ncols * 4;
+    pivot_table_kernel<<<(n + 127) / 128, 128, 0, st>>>(L, k0, ncols, ipt);
     return cudaGetLastError();
 }
 

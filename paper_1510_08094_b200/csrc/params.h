@@ -34,6 +34,7 @@ struct ThetaParams {
     double* stats;    // per rhs: [0..1] mean (re, im), [2] max|F|, [3] unused
     double2* xhalf;   // optional: solution coefficients X[k][i], (N/2+1) x M per rhs
     int kseq;         // lambda modes k < kseq use the sequential Thomas recurrence
+    const double* pivots;  // pivot table for modes k0..k0+ncols-1 (pivot_table_kernel)
 };
 
 struct ShgenParams {
@@ -75,6 +76,7 @@ cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cuda
 cudaError_t launch_lambda_inv(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
+cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 

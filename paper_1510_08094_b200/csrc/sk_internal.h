@@ -22,6 +22,10 @@ struct FftDesc {
     int R[kMaxStages] = {};
     int span[kMaxStages] = {};
     int tw[kMaxStages] = {};
+    // b / span[s] as ((umulhi(b, mag) + ((b - umulhi) >> sh1)) >> sh2) (Granlund-Montgomery)
+    unsigned mag[kMaxStages] = {};
+    int sh1[kMaxStages] = {};
+    int sh2[kMaxStages] = {};
     // twiddle table for the 2L-th roots exp(-2 pi i m / 2L), m in [0, 2L):
     // T(m) = hi[m >> shift] * lo[m & (B-1)], B = 1 << shift
     int shift = 0;

@@ -87,6 +87,13 @@ sk_status build_fft(int L, DevFft& out) {
         d.R[s] = R[s];
         d.span[s] = sz / R[s];
         d.tw[s] = 2 * L / sz;
+        // Granlund-Montgomery constants for unsigned division by span[s]
+        const unsigned dv = static_cast<unsigned>(d.span[s]);
+        int l = 0;
+        while ((1ull << l) < dv) ++l;
+        d.mag[s] = static_cast<unsigned>(((1ull << 32) * ((1ull << l) - dv)) / dv + 1);
+        d.sh1[s] = l < 1 ? l : 1;
+        d.sh2[s] = l > 1 ? l - 1 : 0;
         sz /= R[s];
     }
     const long long n2 = 2LL * L;
@@ -232,6 +239,7 @@ struct sk_plan_s {
     double* hu = nullptr;
     double* rbuf = nullptr;    // residual output (4)
     double2* coef_stage = nullptr;  // shgen coefficients
+    double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -360,6 +368,17 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
             sk_plan_destroy(p);
             return s;
         }
+        // data-independent Thomas pivots of every (lambda mode, parity) chain
+        const size_t np = static_cast<size_t>(p->g.cols) * 2 * p->g.Lt;
+        if ((s = ensure(reinterpret_cast<void**>(&p->pivots), sizeof(double) * np)) != SK_OK) {
+            sk_plan_destroy(p);
+            return s;
+        }
+        if (sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->stream) != cudaSuccess ||
+            cudaStreamSynchronize(p->stream) != cudaSuccess) {
+            sk_plan_destroy(p);
+            return fail(SK_ERR_CUDA, "pivot table construction failed");
+        }
     }
     *out = p;
     return SK_OK;
@@ -373,7 +392,7 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
                     static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
                     static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
-                    static_cast<void*>(p->coef_stage)})
+                    static_cast<void*>(p->coef_stage), static_cast<void*>(p->pivots)})
         if (q) cudaFree(q);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
@@ -529,7 +548,8 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.rhs_stride = static_cast<long long>(p->g.rows) * ncols_local;
         tp.stats = p->stats;
         tp.xhalf = xhalf;
-        tp.kseq = 32;
+        tp.kseq = 4;
+        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
         if (p->timing) CU(cudaEventRecord(p->ev[3], p->stream));

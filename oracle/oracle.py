@@ -181,6 +181,25 @@ class Oracle(_Lib):
                    _ptr(up), _I(threads), _ptr(mean))
         return X, U, up, complex(mean[0], mean[1])
 
+    def grid_pipeline_real(self, phys, m, threads=1):
+        """The composition for real data with the k < 0 half taken as the
+        Hermitian mirror of k > 0 (X(t,-k) = conj X(-t,k); the unpaired
+        t = -M/2 row maps to itself) before synthesis — the real-output
+        variant the GPU grid path implements.  Identical to grid_pipeline for
+        band-limited data; for rough data the reference's own output is
+        complex (its truncated operators are not mirror-symmetric)."""
+        n = phys.shape[1]
+        X, _, _, _ = self.grid_pipeline(phys, m, threads)
+        L = m // 2
+        t = np.arange(m) - L
+        tt = np.where(t == -L, -L, -t) + L
+        Xm = X.copy()
+        for kc in range(1, n // 2):
+            k = kc - n // 2
+            Xm[:, kc] = np.conj(X[tt, n // 2 - k])
+        U = self.sample_grid(Xm, m, n)
+        return phys_from_doubled(U, m).real
+
     def shgen(self, m, n, L, coeffs, threads=8):
         phys = np.zeros((m // 2 + 1, n))
         self._call("shgen", _I(m), _I(n), _I(L), _ptr(np.ascontiguousarray(coeffs, np.float64)), _ptr(phys),

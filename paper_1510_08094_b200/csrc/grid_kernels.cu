@@ -312,41 +312,103 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
 
 // The lowest lambda modes are only weakly diagonally dominant (k = 0 not at
 // all); for them the segmented sweeps lose digits, so one thread runs the
-// plain sequential recurrences (pivots from the table).
+// plain sequential recurrences (pivots from the table).  The chain is walked
+// in chunks of U elements whose shared-memory operands are fetched one chunk
+// ahead (the chunks touch disjoint slots), so only the FMA recurrence itself
+// is on the critical path.
 __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, const Chain& ch, int L, double2 inner,
                                 double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
+    constexpr int U = 8;
     if (threadIdx.x == 0 && ch.n > 0) {
         const int n = ch.n;
         auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
-        double2 xm = inner, x0 = a[pos(0)];
-        double2 rp = make_double2(0.0, 0.0);
-        double ipp = 0.0;
-        for (int i = 0; i < n; ++i) {
-            const double2 xp = (i + 1 < n) ? a[pos(i + 1)] : make_double2(0.0, 0.0);
-            const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
-            const double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
-            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
-            const double al = -chainA(ch, i, L) * ipp;
-            rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
-            a[pos(i)] = rp;
-            ipp = ip[i];
-            xm = x0;
-            x0 = xp;
+        // ---- forward: r'_i = F_i + alpha_i r'_{i-1}
+        int pc[U];
+        double2 xc[U];
+        double2 xnext0;  // X of the first element of the following chunk
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            pc[u] = u < n ? pos(u) : 0;
+            xc[u] = u < n ? a[pc[u]] : make_double2(0.0, 0.0);
         }
+        xnext0 = U < n ? a[pos(U)] : make_double2(0.0, 0.0);
+        double2 xm = inner, rp = make_double2(0.0, 0.0);
+        double ipp = 0.0;
+        for (int c0 = 0; c0 < n; c0 += U) {
+            // prefetch the next chunk (slots disjoint from this chunk's)
+            int pn[U];
+            double2 xn[U];
+            double2 xnn;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = c0 + U + u;
+                pn[u] = i < n ? pos(i) : 0;
+                xn[u] = i < n ? a[pn[u]] : make_double2(0.0, 0.0);
+            }
+            xnn = (c0 + 2 * U < n) ? a[pos(c0 + 2 * U)] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = c0 + u;
+                if (i < n) {
+                    const double2 x0 = xc[u];
+                    const double2 xp = (u + 1 < U) ? ((i + 1 < n) ? xc[u + 1] : make_double2(0.0, 0.0)) : xnext0;
+                    const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
+                    const double2 F =
+                        make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+                    fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+                    const double al = -chainA(ch, i, L) * ipp;
+                    rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
+                    a[pc[u]] = rp;
+                    ipp = ip[i];
+                    xm = x0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                pc[u] = pn[u];
+                xc[u] = xn[u];
+            }
+            xnext0 = xnn;
+        }
+        // ---- backward: x_i = r'_i / d'_i - c_i / d'_i x_{i+1}
         double2 x = make_double2(0.0, 0.0);
         double2 ws = make_double2(0.0, 0.0);
-        for (int i = n - 1; i >= 0; --i) {
-            const int pi = pos(i);
-            const double iv = ip[i];
-            const double2 r = a[pi];
-            const double c = -chainC(ch, i, L) * iv;
-            x = make_double2(fma(c, x.x, r.x * iv), fma(c, x.y, r.y * iv));
-            a[pi] = x;
-            if (want_wsum) {
-                const double t = ch.t0 + ch.dt * i;
-                const double w = 2.0 / (1.0 - t * t);
-                ws.x = fma(w, x.x, ws.x);
-                ws.y = fma(w, x.y, ws.y);
+        const int last = n - 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = last - u;
+            pc[u] = i >= 0 ? pos(i) : 0;
+            xc[u] = i >= 0 ? a[pc[u]] : make_double2(0.0, 0.0);
+        }
+        for (int c0 = last; c0 >= 0; c0 -= U) {
+            int pn[U];
+            double2 xn[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = c0 - U - u;
+                pn[u] = i >= 0 ? pos(i) : 0;
+                xn[u] = i >= 0 ? a[pn[u]] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = c0 - u;
+                if (i >= 0) {
+                    const double iv = ip[i];
+                    const double c = -chainC(ch, i, L) * iv;
+                    x = make_double2(fma(c, x.x, xc[u].x * iv), fma(c, x.y, xc[u].y * iv));
+                    a[pc[u]] = x;
+                    if (want_wsum) {
+                        const double t = ch.t0 + ch.dt * i;
+                        const double w = 2.0 / (1.0 - t * t);
+                        ws.x = fma(w, x.x, ws.x);
+                        ws.y = fma(w, x.y, ws.y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                pc[u] = pn[u];
+                xc[u] = xn[u];
             }
         }
         *x_first = x;

@@ -548,7 +548,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.rhs_stride = static_cast<long long>(p->g.rows) * ncols_local;
         tp.stats = p->stats;
         tp.xhalf = xhalf;
-        tp.kseq = 4;
+        tp.kseq = 2;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));

@@ -33,3 +33,20 @@ def reference():
 def golden(name):
     import numpy as np
     return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+def pytest_collection_modifyitems(config, items):
+    """Without an explicit -m, GPU tests are skipped where no device exists."""
+    if config.getoption("-m"):
+        return
+    try:
+        import torch
+        have = torch.cuda.is_available()
+    except Exception:
+        have = False
+    if have:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device (run with -m gpu on a B200)")
+    for it in items:
+        if "gpu" in it.keywords:
+            it.add_marker(skip)

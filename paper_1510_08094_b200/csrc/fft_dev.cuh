@@ -146,6 +146,61 @@ __device__ __forceinline__ void dft7(double2* x) {
     x[4] = csub(a3, b3);
 }
 
+// exp(-2 pi i m / R) for the composite radices (correctly rounded constants)
+static __constant__ double2 kW10[10] = {{1, 0}, {0.80901699437494745, -0.58778525229247314}, {0.30901699437494745, -0.95105651629515353}, {-0.30901699437494745, -0.95105651629515353}, {-0.80901699437494745, -0.58778525229247314}, {-1, 0}, {-0.80901699437494745, 0.58778525229247314}, {-0.30901699437494745, 0.95105651629515353}, {0.30901699437494745, 0.95105651629515353}, {0.80901699437494745, 0.58778525229247314}};
+static __constant__ double2 kW16[16] = {{1, 0}, {0.92387953251128674, -0.38268343236508978}, {0.70710678118654757, -0.70710678118654757}, {0.38268343236508978, -0.92387953251128674}, {0, -1}, {-0.38268343236508978, -0.92387953251128674}, {-0.70710678118654757, -0.70710678118654757}, {-0.92387953251128674, -0.38268343236508978}, {-1, 0}, {-0.92387953251128674, 0.38268343236508978}, {-0.70710678118654757, 0.70710678118654757}, {-0.38268343236508978, 0.92387953251128674}, {0, 1}, {0.38268343236508978, 0.92387953251128674}, {0.70710678118654757, 0.70710678118654757}, {0.92387953251128674, 0.38268343236508978}};
+static __constant__ double2 kW20[20] = {{1, 0}, {0.95105651629515353, -0.30901699437494745}, {0.80901699437494745, -0.58778525229247314}, {0.58778525229247314, -0.80901699437494745}, {0.30901699437494745, -0.95105651629515353}, {0, -1}, {-0.30901699437494745, -0.95105651629515353}, {-0.58778525229247314, -0.80901699437494745}, {-0.80901699437494745, -0.58778525229247314}, {-0.95105651629515353, -0.30901699437494745}, {-1, 0}, {-0.95105651629515353, 0.30901699437494745}, {-0.80901699437494745, 0.58778525229247314}, {-0.58778525229247314, 0.80901699437494745}, {-0.30901699437494745, 0.95105651629515353}, {0, 1}, {0.30901699437494745, 0.95105651629515353}, {0.58778525229247314, 0.80901699437494745}, {0.80901699437494745, 0.58778525229247314}, {0.95105651629515353, 0.30901699437494745}};
+static __constant__ double2 kW25[25] = {{1, 0}, {0.96858316112863108, -0.24868988716485479}, {0.87630668004386358, -0.48175367410171527}, {0.72896862742141155, -0.68454710592868873}, {0.53582679497899666, -0.84432792550201508}, {0.30901699437494745, -0.95105651629515353}, {0.062790519529313374, -0.99802672842827156}, {-0.18738131458572463, -0.98228725072868872}, {-0.42577929156507266, -0.90482705246601958}, {-0.63742398974868975, -0.77051324277578925}, {-0.80901699437494745, -0.58778525229247314}, {-0.92977648588825146, -0.36812455268467797}, {-0.99211470131447788, -0.12533323356430426}, {-0.99211470131447788, 0.12533323356430426}, {-0.92977648588825146, 0.36812455268467797}, {-0.80901699437494745, 0.58778525229247314}, {-0.63742398974868975, 0.77051324277578925}, {-0.42577929156507266, 0.90482705246601958}, {-0.18738131458572463, 0.98228725072868872}, {0.062790519529313374, 0.99802672842827156}, {0.30901699437494745, 0.95105651629515353}, {0.53582679497899666, 0.84432792550201508}, {0.72896862742141155, 0.68454710592868873}, {0.87630668004386358, 0.48175367410171527}, {0.96858316112863108, 0.24868988716485479}};
+static __constant__ double2 kW32[32] = {{1, 0}, {0.98078528040323043, -0.19509032201612828}, {0.92387953251128674, -0.38268343236508978}, {0.83146961230254524, -0.55557023301960218}, {0.70710678118654757, -0.70710678118654757}, {0.55557023301960218, -0.83146961230254524}, {0.38268343236508978, -0.92387953251128674}, {0.19509032201612828, -0.98078528040323043}, {0, -1}, {-0.19509032201612828, -0.98078528040323043}, {-0.38268343236508978, -0.92387953251128674}, {-0.55557023301960218, -0.83146961230254524}, {-0.70710678118654757, -0.70710678118654757}, {-0.83146961230254524, -0.55557023301960218}, {-0.92387953251128674, -0.38268343236508978}, {-0.98078528040323043, -0.19509032201612828}, {-1, 0}, {-0.98078528040323043, 0.19509032201612828}, {-0.92387953251128674, 0.38268343236508978}, {-0.83146961230254524, 0.55557023301960218}, {-0.70710678118654757, 0.70710678118654757}, {-0.55557023301960218, 0.83146961230254524}, {-0.38268343236508978, 0.92387953251128674}, {-0.19509032201612828, 0.98078528040323043}, {0, 1}, {0.19509032201612828, 0.98078528040323043}, {0.38268343236508978, 0.92387953251128674}, {0.55557023301960218, 0.83146961230254524}, {0.70710678118654757, 0.70710678118654757}, {0.83146961230254524, 0.55557023301960218}, {0.92387953251128674, 0.38268343236508978}, {0.98078528040323043, 0.19509032201612828}};
+
+template <int R>
+__device__ __forceinline__ double2 wconst(int m) {
+    if constexpr (R == 10) return kW10[m];
+    else if constexpr (R == 16) return kW16[m];
+    else if constexpr (R == 20) return kW20[m];
+    else if constexpr (R == 25) return kW25[m];
+    else return kW32[m];
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(double2* x);
+
+// DFT of length R = R1 R2 in registers (Cooley-Tukey, n = R2 n1 + n2,
+// k = k1 + R1 k2): R2 inner DFTs of length R1, constant twiddles
+// exp(SIGN 2 pi i n2 k1 / R), R1 outer DFTs of length R2; natural order out.
+template <int R1, int R2, int SIGN>
+__device__ __forceinline__ void dftc(double2* x) {
+    constexpr int R = R1 * R2;
+    double2 z[R];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+        double2 y[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) y[n1] = x[R2 * n1 + n2];
+        dft<R1, SIGN>(y);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            const int m = (n2 * k1) % R;
+            if (m == 0) {
+                z[k1 * R2 + n2] = y[k1];
+            } else {
+                double2 w = wconst<R>(m);
+                if (SIGN > 0) w.y = -w.y;
+                z[k1 * R2 + n2] = cmul(y[k1], w);
+            }
+        }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+        double2 y[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) y[n2] = z[k1 * R2 + n2];
+        dft<R2, SIGN>(y);
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) x[k1 + R1 * k2] = y[k2];
+    }
+}
+
 template <int R, int SIGN>
 __device__ __forceinline__ void dft(double2* x) {
     if constexpr (R == 2) dft2<SIGN>(x);
@@ -153,7 +208,12 @@ __device__ __forceinline__ void dft(double2* x) {
     else if constexpr (R == 4) dft4<SIGN>(x);
     else if constexpr (R == 5) dft5<SIGN>(x);
     else if constexpr (R == 7) dft7<SIGN>(x);
-    else dft8<SIGN>(x);
+    else if constexpr (R == 8) dft8<SIGN>(x);
+    else if constexpr (R == 10) dftc<2, 5, SIGN>(x);
+    else if constexpr (R == 16) dftc<4, 4, SIGN>(x);
+    else if constexpr (R == 20) dftc<4, 5, SIGN>(x);
+    else if constexpr (R == 25) dftc<5, 5, SIGN>(x);
+    else dftc<4, 8, SIGN>(x);
 }
 
 // ------------------------------------------------------------------- stages
@@ -162,63 +222,84 @@ __device__ __forceinline__ int fdiv(int n, unsigned mag, int sh1, int sh2) {
     return static_cast<int>((t + ((static_cast<unsigned>(n) - t) >> sh1)) >> sh2);
 }
 
-// Forward DIF stage: x_q = a[base + q span]; y = DFT_R(x); y_q *= w^(q j).
+// One butterfly's registers.
 template <int R>
-__device__ __forceinline__ void dif_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
+struct Bfly {
+    double2 x[R];
+    int base, j;
+};
+
+template <int R>
+__device__ __forceinline__ void bf_load(Bfly<R>& B, const double2* a, int b, int span, unsigned mag, int sh1, int sh2) {
+    const int g = fdiv(b, mag, sh1, sh2);
+    B.j = b - g * span;
+    B.base = g * span * R + B.j;
+#pragma unroll
+    for (int q = 0; q < R; ++q) B.x[q] = a[B.base + q * span];
+}
+
+// Forward DIF butterfly: y = DFT_R(x); y_q *= w^(q j); store in place.
+template <int R>
+__device__ __forceinline__ void bf_dif(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
+    dft<R, -1>(B.x);
+    if (B.j != 0) {
+        const double2 w1 = T(B.j * tw);
+        double2 w = w1;
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+            B.x[q] = cmul(B.x[q], w);
+            if (q + 1 < R) w = cmul(w, w1);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
+}
+
+// Inverse DIT butterfly: x_q *= conj(w)^(q j); y = DFT^+_R(x); store in place.
+template <int R>
+__device__ __forceinline__ void bf_dit(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
+    if (B.j != 0) {
+        const double2 w1 = T(B.j * tw);
+        double2 w = w1;
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+            B.x[q] = cmulc(B.x[q], w);
+            if (q + 1 < R) w = cmul(w, w1);
+        }
+    }
+    dft<R, +1>(B.x);
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
+}
+
+// One stage over all butterflies; small radices keep two butterflies'
+// shared-memory loads in flight.
+template <int R, bool FWD>
+__device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
     const int span = d.span[s], tw = d.tw[s];
     const unsigned mag = d.mag[s];
     const int sh1 = d.sh1[s], sh2 = d.sh2[s];
     const int nb = d.L / R;
-    for (int b = tid; b < nb; b += nthr) {
-        const int g = fdiv(b, mag, sh1, sh2);
-        const int j = b - g * span;
-        const int base = g * span * R + j;
-        double2 x[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) x[q] = a[base + q * span];
-        dft<R, -1>(x);
-        a[base] = x[0];
-        if (j == 0) {
-#pragma unroll
-            for (int q = 1; q < R; ++q) a[base + q * span] = x[q];
-        } else {
-            const double2 w1 = T(j * tw);
-            double2 w = w1;
-#pragma unroll
-            for (int q = 1; q < R; ++q) {
-                a[base + q * span] = cmul(x[q], w);
-                if (q + 1 < R) w = cmul(w, w1);
+    int b = tid;
+    if constexpr (R <= 8) {
+        for (; b + nthr < nb; b += 2 * nthr) {
+            Bfly<R> p, q;
+            bf_load(p, a, b, span, mag, sh1, sh2);
+            bf_load(q, a, b + nthr, span, mag, sh1, sh2);
+            if constexpr (FWD) {
+                bf_dif(p, a, span, tw, T);
+                bf_dif(q, a, span, tw, T);
+            } else {
+                bf_dit(p, a, span, tw, T);
+                bf_dit(q, a, span, tw, T);
             }
         }
     }
-}
-
-// Inverse DIT stage: x_q = a[base + q span] * conj(w)^(q j); y = DFT^+_R(x).
-template <int R>
-__device__ __forceinline__ void dit_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
-    const int span = d.span[s], tw = d.tw[s];
-    const unsigned mag = d.mag[s];
-    const int sh1 = d.sh1[s], sh2 = d.sh2[s];
-    const int nb = d.L / R;
-    for (int b = tid; b < nb; b += nthr) {
-        const int g = fdiv(b, mag, sh1, sh2);
-        const int j = b - g * span;
-        const int base = g * span * R + j;
-        double2 x[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) x[q] = a[base + q * span];
-        if (j != 0) {
-            const double2 w1 = T(j * tw);
-            double2 w = w1;
-#pragma unroll
-            for (int q = 1; q < R; ++q) {
-                x[q] = cmulc(x[q], w);
-                if (q + 1 < R) w = cmul(w, w1);
-            }
-        }
-        dft<R, +1>(x);
-#pragma unroll
-        for (int q = 0; q < R; ++q) a[base + q * span] = x[q];
+    for (; b < nb; b += nthr) {
+        Bfly<R> p;
+        bf_load(p, a, b, span, mag, sh1, sh2);
+        if constexpr (FWD) bf_dif(p, a, span, tw, T);
+        else bf_dit(p, a, span, tw, T);
     }
 }
 
@@ -227,12 +308,16 @@ __device__ __forceinline__ void dit_stage(double2* a, const FftDesc& d, int s, c
 __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     for (int s = 0; s < d.nst; ++s) {
         switch (d.R[s]) {
-            case 2: dif_stage<2>(a, d, s, T, tid, nthr); break;
-            case 3: dif_stage<3>(a, d, s, T, tid, nthr); break;
-            case 4: dif_stage<4>(a, d, s, T, tid, nthr); break;
-            case 5: dif_stage<5>(a, d, s, T, tid, nthr); break;
-            case 7: dif_stage<7>(a, d, s, T, tid, nthr); break;
-            default: dif_stage<8>(a, d, s, T, tid, nthr); break;
+            case 2: fft_stage<2, true>(a, d, s, T, tid, nthr); break;
+            case 3: fft_stage<3, true>(a, d, s, T, tid, nthr); break;
+            case 4: fft_stage<4, true>(a, d, s, T, tid, nthr); break;
+            case 5: fft_stage<5, true>(a, d, s, T, tid, nthr); break;
+            case 7: fft_stage<7, true>(a, d, s, T, tid, nthr); break;
+            case 8: fft_stage<8, true>(a, d, s, T, tid, nthr); break;
+            case 10: fft_stage<10, true>(a, d, s, T, tid, nthr); break;
+            case 16: fft_stage<16, true>(a, d, s, T, tid, nthr); break;
+            case 20: fft_stage<20, true>(a, d, s, T, tid, nthr); break;
+            default: fft_stage<25, true>(a, d, s, T, tid, nthr); break;
         }
         __syncthreads();
     }
@@ -241,12 +326,16 @@ __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const 
 __device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     for (int s = d.nst - 1; s >= 0; --s) {
         switch (d.R[s]) {
-            case 2: dit_stage<2>(a, d, s, T, tid, nthr); break;
-            case 3: dit_stage<3>(a, d, s, T, tid, nthr); break;
-            case 4: dit_stage<4>(a, d, s, T, tid, nthr); break;
-            case 5: dit_stage<5>(a, d, s, T, tid, nthr); break;
-            case 7: dit_stage<7>(a, d, s, T, tid, nthr); break;
-            default: dit_stage<8>(a, d, s, T, tid, nthr); break;
+            case 2: fft_stage<2, false>(a, d, s, T, tid, nthr); break;
+            case 3: fft_stage<3, false>(a, d, s, T, tid, nthr); break;
+            case 4: fft_stage<4, false>(a, d, s, T, tid, nthr); break;
+            case 5: fft_stage<5, false>(a, d, s, T, tid, nthr); break;
+            case 7: fft_stage<7, false>(a, d, s, T, tid, nthr); break;
+            case 8: fft_stage<8, false>(a, d, s, T, tid, nthr); break;
+            case 10: fft_stage<10, false>(a, d, s, T, tid, nthr); break;
+            case 16: fft_stage<16, false>(a, d, s, T, tid, nthr); break;
+            case 20: fft_stage<20, false>(a, d, s, T, tid, nthr); break;
+            default: fft_stage<25, false>(a, d, s, T, tid, nthr); break;
         }
         __syncthreads();
     }

@@ -169,14 +169,25 @@ __device__ __forceinline__ double lap_diag(int t, int L) {
 // Msin^2 diagonal (poisson.cpp:61; 1/4 on the first and last rows)
 __device__ __forceinline__ double msin2_diag(int t, int L) { return (t == -L || t == L - 1) ? 0.25 : 0.5; }
 
-// chain-local coefficients: A couples to element i-1, C to element i+1
+// chain-local coefficients: A couples to element i-1, C to element i+1.
+// With sigma = sign(dt): A = (t - 2 sigma)(t - sigma)/4 (it vanishes at the
+// first element, t0 in {+-1, +-2}), C = (t + 2 sigma)(t + sigma)/4 except at
+// the last element, where the neighbour falls off the truncated operator.
 __device__ __forceinline__ double chainA(const Chain& ch, int i, int L) {
-    const int t = ch.t0 + ch.dt * i;
-    return ch.dt > 0 ? lap_lower(t, L) : lap_upper(t, L);
+    const double t = ch.t0 + ch.dt * i, sg = ch.dt > 0 ? 1.0 : -1.0;
+    (void)L;
+    return 0.25 * (t - 2.0 * sg) * (t - sg);
 }
 __device__ __forceinline__ double chainC(const Chain& ch, int i, int L) {
+    const double t = ch.t0 + ch.dt * i, sg = ch.dt > 0 ? 1.0 : -1.0;
+    (void)L;
+    return (i + 1 < ch.n) ? 0.25 * (t + 2.0 * sg) * (t + sg) : 0.0;
+}
+// Msin^2 diagonal along a chain: 1/4 only at the truncation rows t = -L and
+// t = L-1, which can only be a chain's last element.
+__device__ __forceinline__ double chainD2(const Chain& ch, int i, int L) {
     const int t = ch.t0 + ch.dt * i;
-    return ch.dt > 0 ? lap_upper(t, L) : lap_lower(t, L);
+    return (i + 1 == ch.n && (t == -L || t == L - 1)) ? 0.25 : 0.5;
 }
 
 // Pivot table: for every lambda mode k >= 0 and parity class, the reciprocal
@@ -225,7 +236,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
     auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
     auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
-        const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
+        const double d2 = chainD2(ch, i, L);
         return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
     };
     // boundary neighbours (original transform values) before anyone writes
@@ -352,7 +363,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
                 if (i < n) {
                     const double2 x0 = xc[u];
                     const double2 xp = (u + 1 < U) ? ((i + 1 < n) ? xc[u + 1] : make_double2(0.0, 0.0)) : xnext0;
-                    const double d2 = msin2_diag(ch.t0 + ch.dt * i, L);
+                    const double d2 = chainD2(ch, i, L);
                     const double2 F =
                         make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
                     fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));

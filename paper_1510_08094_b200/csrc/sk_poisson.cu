@@ -29,33 +29,34 @@ sk_status fail(sk_status s, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(SK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Radix plan: as few in-place stages as the register budget allows.
+// Powers of two go to 16s (then 8/4/2); fives pair into 25s, a leftover five
+// joins a 2 or 4 (10, 20); threes and sevens stay single.
 bool factor_radices(int L, std::vector<int>& R) {
     R.clear();
     if (L < 1) return false;
-    int m = L;
-    int p2 = 0;
-    while (m % 2 == 0) {
-        m /= 2;
-        ++p2;
+    int m = L, p2 = 0, p5 = 0;
+    while (m % 2 == 0) { m /= 2; ++p2; }
+    while (m % 5 == 0) { m /= 5; ++p5; }
+    std::vector<int> r2;
+    while (p2 >= 4) { r2.push_back(16); p2 -= 4; }
+    if (p2 == 3) r2.push_back(8);
+    if (p2 == 2) r2.push_back(4);
+    if (p2 == 1) {
+        if (!r2.empty()) { r2.back() = 8; r2.push_back(4); }  // 32 = 8 * 4
+        else r2.push_back(2);
     }
-    while (p2 >= 3) {
-        if (p2 == 4) {
-            R.push_back(4);
-            R.push_back(4);
-            p2 = 0;
-            break;
-        }
-        R.push_back(8);
-        p2 -= 3;
+    std::vector<int> r5;
+    while (p5 >= 2) { r5.push_back(25); p5 -= 2; }
+    if (p5 == 1) {
+        bool merged = false;
+        for (int& x : r2)
+            if (x == 2 || x == 4) { x *= 5; merged = true; break; }
+        if (!merged) r5.push_back(5);
     }
-    if (p2 == 2) R.push_back(4);
-    if (p2 == 1) R.push_back(2);
-    for (int q : {5, 3, 7}) {
-        while (m % q == 0) {
-            R.push_back(q);
-            m /= q;
-        }
-    }
+    for (int x : r2) R.push_back(x);
+    for (int x : r5) R.push_back(x);
+    for (int q : {3, 7}) while (m % q == 0) { R.push_back(q); m /= q; }
     return m == 1 && static_cast<int>(R.size()) <= sk::kMaxStages;
 }
 

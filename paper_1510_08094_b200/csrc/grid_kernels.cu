@@ -256,7 +256,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
         for (int i = s; i < e; ++i) {
             const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
             const double2 F = Fof(xm, x0, xp, i);
-            fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+            fmax_acc = fmax(fmax_acc, F.x * F.x + F.y * F.y);  // squared; sqrt at the end
             const double al = -chainA(ch, i, L) * ipp;
             aff = V4{al * aff.a, fma(al, aff.b, F.x), fma(al, aff.c, F.y), 0.0};
             ipp = ip[i];
@@ -350,6 +350,9 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
             int pn[U];
             double2 xn[U];
             double2 xnn;
+            double ipc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ipc[u] = (c0 + u < n) ? ip[c0 + u] : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = c0 + U + u;
@@ -357,6 +360,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
                 xn[u] = i < n ? a[pn[u]] : make_double2(0.0, 0.0);
             }
             xnn = (c0 + 2 * U < n) ? a[pos(c0 + 2 * U)] : make_double2(0.0, 0.0);
+            double2 rc[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = c0 + u;
@@ -366,14 +370,17 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
                     const double d2 = chainD2(ch, i, L);
                     const double2 F =
                         make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
-                    fmax_acc = fmax(fmax_acc, sqrt(F.x * F.x + F.y * F.y));
+                    fmax_acc = fmax(fmax_acc, F.x * F.x + F.y * F.y);  // squared; sqrt at the end
                     const double al = -chainA(ch, i, L) * ipp;
                     rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
-                    a[pc[u]] = rp;
-                    ipp = ip[i];
+                    rc[u] = rp;
+                    ipp = ipc[u];
                     xm = x0;
                 }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c0 + u < n) a[pc[u]] = rc[u];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 pc[u] = pn[u];
@@ -400,14 +407,18 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
                 pn[u] = i >= 0 ? pos(i) : 0;
                 xn[u] = i >= 0 ? a[pn[u]] : make_double2(0.0, 0.0);
             }
+            double ipc[U];
+            double2 xo[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ipc[u] = (c0 - u >= 0) ? ip[c0 - u] : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = c0 - u;
                 if (i >= 0) {
-                    const double iv = ip[i];
+                    const double iv = ipc[u];
                     const double c = -chainC(ch, i, L) * iv;
                     x = make_double2(fma(c, x.x, xc[u].x * iv), fma(c, x.y, xc[u].y * iv));
-                    a[pc[u]] = x;
+                    xo[u] = x;
                     if (want_wsum) {
                         const double t = ch.t0 + ch.dt * i;
                         const double w = 2.0 / (1.0 - t * t);
@@ -416,6 +427,9 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
                     }
                 }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c0 - u >= 0) a[pc[u]] = xo[u];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 pc[u] = pn[u];
@@ -532,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     }
     __syncthreads();
     const double2 inner_p = misc[0], inner_m = misc[1], F0 = misc[2];
-    double fmax_acc = (par == 0) ? sqrt(F0.x * F0.x + F0.y * F0.y) : 0.0;
+    double fmax_acc = (par == 0) ? F0.x * F0.x + F0.y * F0.y : 0.0;  // max |F|^2
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
     const bool seq = kg < P.kseq;
@@ -555,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         }
         a[__ldg(rev + 0)] = x0;
     }
-    const double fm = block_max(fmax_acc, red);
+    const double fm = sqrt(block_max(fmax_acc, red));
     if (tid == 0) atomic_max_nonneg(st + 2, fm);
     __syncthreads();
 

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -241,6 +242,7 @@ struct sk_plan_s {
     double* rbuf = nullptr;    // residual output (4)
     double2* coef_stage = nullptr;  // shgen coefficients
     double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
+    int kseq = 2;              // lambda modes solved by the sequential recurrence
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -313,6 +315,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         return fail(SK_ERR_CUDA, "stream creation failed");
     }
     p->own_stream = true;
+    if (const char* e = std::getenv("SK_KSEQ")) p->kseq = std::atoi(e);
     p->g.M = M;
     p->g.N = N;
     p->g.Lt = M / 2;
@@ -549,7 +552,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.rhs_stride = static_cast<long long>(p->g.rows) * ncols_local;
         tp.stats = p->stats;
         tp.xhalf = xhalf;
-        tp.kseq = 2;
+        tp.kseq = p->kseq;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));

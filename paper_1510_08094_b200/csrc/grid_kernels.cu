@@ -21,6 +21,7 @@
 
 #include "block_ops.cuh"
 #include "fft_dev.cuh"
+#include "tma.cuh"
 #include "params.h"
 #include "sk_internal.h"
 
@@ -43,29 +44,36 @@ __device__ __forceinline__ size_t theta_addr(const Slabs& sl, int ncols, int kl,
 // One CTA per physical row: load the real row as N/2 complex pairs, forward
 // DIF FFT, split into the N/2+1 modes of the real transform, apply
 // analyze_1d's (-1)^k / N (fourier.cpp:44-51), store transposed.
-__global__ void __launch_bounds__(512) lambda_fwd_kernel(LambdaParams P) {
+__global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int L = P.fd.L;
     double2* a = reinterpret_cast<double2*>(smem_raw);
     double2* s_hi = a + L;
     double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
-    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
-    __syncthreads();
     const double2* src =
         reinterpret_cast<const double2*>(P.f + rhs * P.in_rhs_stride + static_cast<long long>(row) * P.g.N);
-    for (int j = tid; j < L; j += nthr) a[j] = __ldg(src + j);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
+        bulk_g2s_chunked(a, src, static_cast<uint32_t>(L) * 16, bar);  // the real row as N/2 complex pairs
+    }
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();
+    mbar_wait(bar, 0);
     fft_forward(a, P.fd, T, tid, nthr);
     const double invN = 1.0 / P.g.N;
     double2* out = P.spec + rhs * P.out_rhs_stride;
-    const int* rev = P.fd.rev;
     for (int k = tid; k <= L / 2; k += nthr) {
         const int km = L - k;  // partner mode
-        const double2 z = a[__ldg(rev + k)];
-        const double2 zp = a[__ldg(rev + (km == L ? 0 : km))];
+        const double2 z = a[s_rev[k]];
+        const double2 zp = a[s_rev[km == L ? 0 : km]];
         // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
         const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
@@ -81,19 +89,20 @@ __global__ void __launch_bounds__(512) lambda_fwd_kernel(LambdaParams P) {
 // Inverse: gather the N/2+1 modes of a physical row, apply sample_grid's
 // (-1)^k (fourier.cpp:61-62), pack into N/2 complex, inverse DIT FFT, store
 // the real row (unnormalised backward transform, as FFTW_BACKWARD).
-__global__ void __launch_bounds__(512) lambda_inv_kernel(LambdaParams P) {
+__global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int L = P.fd.L;
     double2* a = reinterpret_cast<double2*>(smem_raw);
     double2* s_hi = a + L;
     double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();  // the pre-processing below reads the staged twiddles
     const double2* in = P.spec + rhs * P.in_rhs_stride;
-    const int* rev = P.fd.rev;
     for (int k = tid; k <= L / 2; k += nthr) {
         const int km = L - k;
         double2 v = in[static_cast<size_t>(k) * P.rows_local + row];
@@ -108,12 +117,12 @@ __global__ void __launch_bounds__(512) lambda_inv_kernel(LambdaParams P) {
         {
             const double2 E = make_double2(v.x + w.x, v.y - w.y);
             const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
-            a[__ldg(rev + k)] = make_double2(E.x - O.y, E.y + O.x);
+            a[s_rev[k]] = make_double2(E.x - O.y, E.y + O.x);
         }
         if (k != 0 && km != k) {
             const double2 E = make_double2(w.x + v.x, w.y - v.y);
             const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-            a[__ldg(rev + km)] = make_double2(E.x - O.y, E.y + O.x);
+            a[s_rev[km]] = make_double2(E.x - O.y, E.y + O.x);
         }
     }
     __syncthreads();
@@ -226,8 +235,8 @@ __global__ void __launch_bounds__(128) pivot_table_kernel(int L, int k0, int nco
 //   x_i  = r'_i / d'_i + beta_i x_{i+1},  beta_i = -c_i / d'_i
 // Each thread owns a contiguous segment: a local pass composes its segment's
 // affine map, a block scan gives every segment its incoming value, and a
-// second pass applies it.  `ip` holds the chain's pivots (shared memory,
-// chain-element order).
+// second pass applies it.  ip[tau] is the pivot of the element at natural
+// FFT index tau (shared-memory window of the plan table).
 __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* wsc, const Chain& ch, int L,
                             double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -252,14 +261,14 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     {
         double2 xm = xlo;
         double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
-        double ipp = (s > 0) ? ip[s - 1] : 0.0;
+        double ipp = (s > 0) ? ip[ch.tau0 + ch.dtau * (s - 1)] : 0.0;
         for (int i = s; i < e; ++i) {
             const double2 xp = (i + 1 < e) ? a[pos(i + 1)] : xhi;
             const double2 F = Fof(xm, x0, xp, i);
             fmax_acc = fmax(fmax_acc, F.x * F.x + F.y * F.y);  // squared; sqrt at the end
             const double al = -chainA(ch, i, L) * ipp;
             aff = V4{al * aff.a, fma(al, aff.b, F.x), fma(al, aff.c, F.y), 0.0};
-            ipp = ip[i];
+            ipp = ip[ch.tau0 + ch.dtau * i];
             xm = x0;
             x0 = xp;
         }
@@ -269,7 +278,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     // ---- forward sweep with the true incoming value, r' in place
     {
         double2 rp = make_double2(rin.b, rin.c);
-        double ipp = (s > 0) ? ip[s - 1] : 0.0;
+        double ipp = (s > 0) ? ip[ch.tau0 + ch.dtau * (s - 1)] : 0.0;
         double2 xm = xlo;
         double2 x0 = (s < e) ? a[pos(s)] : make_double2(0.0, 0.0);
         for (int i = s; i < e; ++i) {
@@ -279,7 +288,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
             const double al = -chainA(ch, i, L) * ipp;
             rp = make_double2(fma(al, rp.x, F.x), fma(al, rp.y, F.y));
             a[pi] = rp;
-            ipp = ip[i];
+            ipp = ip[ch.tau0 + ch.dtau * i];
             xm = x0;
             x0 = xp;
         }
@@ -289,7 +298,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     // ---- local backward summary x_s = P x_e + xt
     V4 baff = AffOp::identity();
     for (int i = e - 1; i >= s; --i) {
-        const double iv = ip[i];
+        const double iv = ip[ch.tau0 + ch.dtau * i];
         const double2 r = a[pos(i)];
         const double be = -chainC(ch, i, L) * iv;
         baff = V4{be * baff.a, fma(be, baff.b, r.x * iv), fma(be, baff.c, r.y * iv), 0.0};
@@ -302,7 +311,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
         double2 x = make_double2(xin.b, xin.c);
         for (int i = e - 1; i >= s; --i) {
             const int pi = pos(i);
-            const double iv = ip[i];
+            const double iv = ip[ch.tau0 + ch.dtau * i];
             const double2 r = a[pi];
             const double c = -chainC(ch, i, L) * iv;
             x = make_double2(fma(c, x.x, r.x * iv), fma(c, x.y, r.y * iv));
@@ -352,7 +361,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
             double2 xnn;
             double ipc[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) ipc[u] = (c0 + u < n) ? ip[c0 + u] : 0.0;
+            for (int u = 0; u < U; ++u) ipc[u] = (c0 + u < n) ? ip[ch.tau0 + ch.dtau * (c0 + u)] : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = c0 + U + u;
@@ -410,7 +419,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
             double ipc[U];
             double2 xo[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) ipc[u] = (c0 - u >= 0) ? ip[c0 - u] : 0.0;
+            for (int u = 0; u < U; ++u) ipc[u] = (c0 - u >= 0) ? ip[ch.tau0 + ch.dtau * (c0 - u)] : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int i = c0 - u;
@@ -443,10 +452,15 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
     __syncthreads();
 }
 
-// Load a chain's pivots from the plan table into shared memory (chain order).
-__device__ __forceinline__ void load_pivots(double* ip, const double* tab, const Chain& ch) {
-    for (int i = threadIdx.x; i < ch.n; i += blockDim.x) ip[i] = __ldg(tab + ch.tau0 + ch.dtau * i);
-    __syncthreads();
+// Issue the bulk copy of a chain's pivot window (16-byte aligned superset of
+// table entries [row + tau_lo, row + tau_hi)) into `dst`; returns the pointer
+// p with p[tau] = pivot of the element at natural index tau, and the bytes.
+__device__ __forceinline__ const double* pivot_window(double* dst, const double* row, size_t row_abs, int tau_lo,
+                                                      int tau_hi, uint32_t& bytes) {
+    const size_t a0 = (row_abs + tau_lo) & ~static_cast<size_t>(1);
+    const size_t a1 = (row_abs + tau_hi + 1) & ~static_cast<size_t>(1);
+    bytes = static_cast<uint32_t>((a1 - a0) * 8);
+    return dst + (static_cast<long long>(row_abs) - static_cast<long long>(a0));
 }
 
 // One 2-CTA cluster per lambda mode k: CTA `par` (0/1) owns the theta modes
@@ -461,12 +475,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     cg::cluster_group cluster = cg::this_cluster();
     const int L = P.fd.L;  // M/2
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + L;
+    double2* s_hi = a + L + 1;  // a holds the raw column (L+1 values) before the fold
     double2* s_lo = s_hi + P.fd.nhi;
     double* ip = reinterpret_cast<double*>(s_lo + P.fd.nlo);
     V4* wsc = reinterpret_cast<V4*>(ip + theta_chain_slots(L));
     double2* misc = reinterpret_cast<double2*>(wsc + 32);
     double* red = reinterpret_cast<double*>(misc + 16);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 64);
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int par = static_cast<int>(cluster.block_rank());
@@ -478,17 +493,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const double sgn = (kg & 1) ? -1.0 : 1.0;
     const int* rev = P.fd.rev;
     double2* colbase = P.buf + rhs * P.rhs_stride;
-    const double* ptab = P.pivots + (static_cast<size_t>(kl) * 2 + par) * L;
 
+    Chain cp, cm;
+    make_chains(par, L, cp, cm);
+    const size_t prow = (static_cast<size_t>(kl) * 2 + par) * L;  // pivot row (table index)
+
+    // ---- bulk copies: the raw column (L+1 values) and the t > 0 chain's pivots
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t bytes = 0, pb = 0;
+        const double* pv = pivot_window(ip, P.pivots, prow, cp.tau0, cp.tau0 + cp.n, pb);
+        (void)pv;
+        for (int s = 0; s < P.sl.P; ++s) {
+            const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
+            if (r1 > r0) bytes += (r1 - r0) * 16;
+        }
+        mbar_expect_tx(&bars[0], bytes + pb);
+        for (int s = 0; s < P.sl.P; ++s) {
+            const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
+            if (r1 > r0)
+                bulk_g2s_chunked(a + r0, colbase + theta_addr(P.sl, P.ncols, kl, r0), (r1 - r0) * 16, &bars[0]);
+        }
+        const size_t a0 = (prow + cp.tau0) & ~static_cast<size_t>(1);
+        if (pb) bulk_g2s_chunked(ip, P.pivots + a0, pb, &bars[0]);
+    }
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    uint32_t pb_unused = 0;
+    const double* ipp = pivot_window(ip, P.pivots, prow, cp.tau0, cp.tau0 + cp.n, pb_unused);
+    mbar_wait(&bars[0], 0);
     __syncthreads();
 
-    // ---- load + DFS fold (first radix-2 step), scaled by 1/M
+    // ---- DFS fold (first radix-2 step) in place, scaled by 1/M
     const double invM = 1.0 / P.g.M;
     for (int r = tid; r <= L / 2; r += nthr) {
         const int rm = L - r;
-        const double2 ar = colbase[theta_addr(P.sl, P.ncols, kl, r)];
-        const double2 am = colbase[theta_addr(P.sl, P.ncols, kl, rm)];
+        const double2 ar = a[r];
+        const double2 am = a[rm];
         if (par == 0) {
             // e_r = a_r + s a_{L-r}
             a[r] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
@@ -523,8 +568,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     }
 
     // ---- chains
-    Chain cp, cm;
-    make_chains(par, L, cp, cm);
     // inner neighbours and the j = 0 row data, read before any chain writes
     if (tid == 0) {
         if (par == 0) {
@@ -550,12 +593,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
     const bool seq = kg < P.kseq;
-    load_pivots(ip, ptab, cp);
-    if (seq) solve_chain_seq(a, rev, ip, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    else solve_chain(a, rev, ip, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    load_pivots(ip, ptab, cm);
-    if (seq) solve_chain_seq(a, rev, ip, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
-    else solve_chain(a, rev, ip, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    if (seq) solve_chain_seq(a, rev, ipp, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    else solve_chain(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    // the t < 0 chain's pivots replace the t > 0 chain's in the window
+    const double* ipm = ip;
+    if (cm.n > 0) {
+        uint32_t pb = 0;
+        ipm = pivot_window(ip, P.pivots, prow, L - cm.n, L, pb);
+        if (tid == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[1], pb);
+            bulk_g2s_chunked(ip, P.pivots + ((prow + L - cm.n) & ~static_cast<size_t>(1)), pb, &bars[1]);
+        }
+        mbar_wait(&bars[1], 0);
+    }
+    if (seq) solve_chain_seq(a, rev, ipm, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    else solve_chain(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
         double2 x0;

@@ -63,13 +63,13 @@ struct ResidualParams {
 
 // Pivot-reciprocal slots of the theta kernel (even, so later regions stay
 // 16-byte aligned).
-__host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 2) + 1) & ~1; }
+__host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 4) + 1) & ~1; }
 
 // Dynamic shared memory of theta_kernel (bytes).
 __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
     const size_t chain_max = static_cast<size_t>(theta_chain_slots(L));
-    return static_cast<size_t>(L) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
-           16 * 16 + 64 * 8;
+    return static_cast<size_t>(L + 1) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
+           16 * 16 + 64 * 8 + 2 * 8;
 }
 
 cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);

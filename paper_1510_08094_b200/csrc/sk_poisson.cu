@@ -242,7 +242,7 @@ struct sk_plan_s {
     double* rbuf = nullptr;    // residual output (4)
     double2* coef_stage = nullptr;  // shgen coefficients
     double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
-    int kseq = 2;              // lambda modes solved by the sequential recurrence
+    int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -356,7 +356,8 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     if (p->grid_ok) {
         const int Lt = M / 2, Ll = N / 2;
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
-        p->smem_lambda = static_cast<size_t>(Ll) * 16 + static_cast<size_t>(p->fl.d.nhi + p->fl.d.nlo) * 16;
+        p->smem_lambda = static_cast<size_t>(Ll) * 16 + static_cast<size_t>(p->fl.d.nhi + p->fl.d.nlo) * 16 +
+                         static_cast<size_t>((Ll + 3) & ~3) * 4 + 16;
         const size_t cap = 227 * 1024;
         if (p->smem_theta > cap || p->smem_lambda > cap) {
             p->grid_ok = false;
@@ -364,7 +365,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
                           " exceeds the on-chip (shared memory) limit of this build";
         }
         p->thr_theta = round_threads(Lt / 8, 64, 512);
-        p->thr_lambda = round_threads(Ll / 8, 64, 512);
+        p->thr_lambda = round_threads(Ll / 8, 64, 256);
     }
     if (p->grid_ok) {
         const size_t n = static_cast<size_t>(nrhs) * p->g.rows * p->g.cols;
@@ -553,7 +554,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.stats = p->stats;
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
-        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;
+        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;  // rows for this rank's modes
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
         if (p->timing) CU(cudaEventRecord(p->ev[3], p->stream));

@@ -1,0 +1,62 @@
+// Bulk asynchronous global->shared copies (the TMA engine's non-tensor
+// cp.async.bulk path) completed on an mbarrier transaction count.  One thread
+// issues the copies; every thread waits on the barrier phase.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sk {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+// make barrier initialisation / prior generic shared-memory accesses visible
+// to the async proxy before bulk copies are issued
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// bytes % 16 == 0, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue a (possibly large) copy in chunks; returns the byte count.
+__device__ __forceinline__ uint32_t bulk_g2s_chunked(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    constexpr uint32_t kChunk = 32768;
+    uint32_t done = 0;
+    while (done < bytes) {
+        const uint32_t n = (bytes - done) < kChunk ? (bytes - done) : kChunk;
+        bulk_g2s(static_cast<char*>(dst) + done, static_cast<const char*>(src) + done, n, bar);
+        done += n;
+    }
+    return bytes;
+}
+
+}  // namespace sk

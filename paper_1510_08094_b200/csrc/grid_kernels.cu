@@ -103,26 +103,41 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P) {
     for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();  // the pre-processing below reads the staged twiddles
     const double2* in = P.spec + rhs * P.in_rhs_stride;
-    for (int k = tid; k <= L / 2; k += nthr) {
-        const int km = L - k;
-        double2 v = in[static_cast<size_t>(k) * P.rows_local + row];
-        double2 w = in[static_cast<size_t>(km) * P.rows_local + row];
-        if (k & 1) v = make_double2(-v.x, -v.y);
-        if (km & 1) w = make_double2(-w.x, -w.y);
-        if (k == 0) {  // DC and Nyquist of a real signal are real
-            v.y = 0.0;
-            w.y = 0.0;
+    // the strided gather is latency-bound: keep G pairs of loads in flight
+    constexpr int G = 4;
+    for (int k0 = tid; k0 <= L / 2; k0 += G * nthr) {
+        double2 vv[G], ww[G];
+#pragma unroll
+        for (int g2 = 0; g2 < G; ++g2) {
+            const int k = k0 + g2 * nthr;
+            if (k <= L / 2) {
+                vv[g2] = __ldg(in + static_cast<size_t>(k) * P.rows_local + row);
+                ww[g2] = __ldg(in + static_cast<size_t>(L - k) * P.rows_local + row);
+            }
         }
-        // Z_k = E_k + i O_k, E_k = V_k + conj V_{L-k}, O_k = (V_k - conj V_{L-k}) conj(T(k))
-        {
-            const double2 E = make_double2(v.x + w.x, v.y - w.y);
-            const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
-            a[s_rev[k]] = make_double2(E.x - O.y, E.y + O.x);
-        }
-        if (k != 0 && km != k) {
-            const double2 E = make_double2(w.x + v.x, w.y - v.y);
-            const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-            a[s_rev[km]] = make_double2(E.x - O.y, E.y + O.x);
+#pragma unroll
+        for (int g2 = 0; g2 < G; ++g2) {
+            const int k = k0 + g2 * nthr;
+            if (k > L / 2) continue;
+            const int km = L - k;
+            double2 v = vv[g2], w = ww[g2];
+            if (k & 1) v = make_double2(-v.x, -v.y);
+            if (km & 1) w = make_double2(-w.x, -w.y);
+            if (k == 0) {  // DC and Nyquist of a real signal are real
+                v.y = 0.0;
+                w.y = 0.0;
+            }
+            // Z_k = E_k + i O_k, E_k = V_k + conj V_{L-k}, O_k = (V_k - conj V_{L-k}) conj(T(k))
+            {
+                const double2 E = make_double2(v.x + w.x, v.y - w.y);
+                const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
+                a[s_rev[k]] = make_double2(E.x - O.y, E.y + O.x);
+            }
+            if (k != 0 && km != k) {
+                const double2 E = make_double2(w.x + v.x, w.y - v.y);
+                const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
+                a[s_rev[km]] = make_double2(E.x - O.y, E.y + O.x);
+            }
         }
     }
     __syncthreads();

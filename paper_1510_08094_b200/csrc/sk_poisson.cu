@@ -30,35 +30,39 @@ sk_status fail(sk_status s, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(SK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-// Radix plan: as few in-place stages as the register budget allows.
-// Powers of two go to 16s (then 8/4/2); fives pair into 25s, a leftover five
-// joins a 2 or 4 (10, 20); threes and sevens stay single.
-bool factor_radices(int L, std::vector<int>& R) {
+// Radix plan for an in-place transform of length L run by `nthr` threads:
+// the factorisation into register radices {2,3,4,5,7,8,10,16,20,25} that
+// minimises a simple time model, sum over stages of
+// ceil(L/R / nthr) * (R + 6) + 30 (rounds of butterflies per thread times a
+// butterfly's cost, plus a per-stage barrier), so stages stay balanced.
+void search_radices(int m, int nthr, int L, int maxr, std::vector<int>& cur, double cost, double& best,
+                    std::vector<int>& out) {
+    if (cost >= best) return;
+    if (m == 1) {
+        best = cost;
+        out = cur;
+        return;
+    }
+    if (static_cast<int>(cur.size()) >= sk::kMaxStages) return;
+    static const int kRad[] = {25, 20, 16, 10, 8, 7, 5, 4, 3, 2};
+    for (int r : kRad) {
+        if (r > maxr || m % r != 0) continue;
+        const long long nb = L / r;
+        const double c = static_cast<double>((nb + nthr - 1) / nthr) * (r + 6) + 30;
+        cur.push_back(r);
+        search_radices(m / r, nthr, L, r, cur, cost + c, best, out);
+        cur.pop_back();
+    }
+}
+
+bool factor_radices(int L, int nthr, std::vector<int>& R) {
     R.clear();
     if (L < 1) return false;
-    int m = L, p2 = 0, p5 = 0;
-    while (m % 2 == 0) { m /= 2; ++p2; }
-    while (m % 5 == 0) { m /= 5; ++p5; }
-    std::vector<int> r2;
-    while (p2 >= 4) { r2.push_back(16); p2 -= 4; }
-    if (p2 == 3) r2.push_back(8);
-    if (p2 == 2) r2.push_back(4);
-    if (p2 == 1) {
-        if (!r2.empty()) { r2.back() = 8; r2.push_back(4); }  // 32 = 8 * 4
-        else r2.push_back(2);
-    }
-    std::vector<int> r5;
-    while (p5 >= 2) { r5.push_back(25); p5 -= 2; }
-    if (p5 == 1) {
-        bool merged = false;
-        for (int& x : r2)
-            if (x == 2 || x == 4) { x *= 5; merged = true; break; }
-        if (!merged) r5.push_back(5);
-    }
-    for (int x : r2) R.push_back(x);
-    for (int x : r5) R.push_back(x);
-    for (int q : {3, 7}) while (m % q == 0) { R.push_back(q); m /= q; }
-    return m == 1 && static_cast<int>(R.size()) <= sk::kMaxStages;
+    if (L == 1) return true;
+    std::vector<int> cur;
+    double best = 1e300;
+    search_radices(L, nthr, L, 25, cur, 0.0, best, R);
+    return !R.empty();
 }
 
 struct DevFft {
@@ -78,9 +82,9 @@ void root(long long m, long long n, double& c, double& s) {
     s = static_cast<double>(-sinl(a));
 }
 
-sk_status build_fft(int L, DevFft& out) {
+sk_status build_fft(int L, int nthr, DevFft& out) {
     std::vector<int> R;
-    if (!factor_radices(L, R)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
+    if (!factor_radices(L, nthr, R)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
     sk::FftDesc& d = out.d;
     d.L = L;
     d.nst = static_cast<int>(R.size());
@@ -345,11 +349,13 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         p->grid_ok = false;
         p->grid_why = "grid path needs M >= 8 and N >= 4";
     }
-    if (p->grid_ok && (s = build_fft(M / 2, p->ft)) != SK_OK) {
+    p->thr_theta = round_threads((M / 2) / 8, 64, 512);
+    p->thr_lambda = round_threads((N / 2) / 8, 64, 256);
+    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
-    if (p->grid_ok && (s = build_fft(N / 2, p->fl)) != SK_OK) {
+    if (p->grid_ok && (s = build_fft(N / 2, p->thr_lambda, p->fl)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
@@ -364,8 +370,6 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
             p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +
                           " exceeds the on-chip (shared memory) limit of this build";
         }
-        p->thr_theta = round_threads(Lt / 8, 64, 512);
-        p->thr_lambda = round_threads(Ll / 8, 64, 256);
     }
     if (p->grid_ok) {
         const size_t n = static_cast<size_t>(nrhs) * p->g.rows * p->g.cols;

@@ -143,11 +143,14 @@ def emulate_slabs(f: np.ndarray, M: int, N: int, P: int) -> np.ndarray:
 
 
 def gather_rows(u_rows, rows_bounds: Sequence[int], group=None):
-    """Collect all ranks' row slabs on every rank (for tests / small cases)."""
+    """Collect all ranks' row slabs on every rank (for tests / small cases);
+    slabs are padded to a common height for the collective."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    parts = [torch.empty((rows_bounds[i + 1] - rows_bounds[i], u_rows.shape[1]), dtype=u_rows.dtype,
-                         device=u_rows.device) for i in range(world)]
-    dist.all_gather(parts, u_rows.contiguous(), group=group)
-    return torch.cat(parts)
+    hmax = max(rows_bounds[i + 1] - rows_bounds[i] for i in range(world))
+    pad = torch.zeros((hmax, u_rows.shape[1]), dtype=u_rows.dtype, device=u_rows.device)
+    pad[: u_rows.shape[0]] = u_rows
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([parts[i][: rows_bounds[i + 1] - rows_bounds[i]] for i in range(world)])

@@ -1,0 +1,106 @@
+"""CPU, gloo, world_size 2 (and 3): the slab-decomposed orchestration
+(SlabSolver: row/mode slabs, all-to-all split sizes and block layouts)
+produces exactly the single-process result.  The per-rank stage work is a
+numpy stand-in with the same buffer layouts as the CUDA stages (the CUDA
+stages themselves are checked on the GPU, tests/test_gpu_parity.py
+test_slab_stages_bitwise_equal_single_gpu)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+class NumpyStages:
+    """Layout-faithful stand-in: lambda_fwd = analyze_1d of each row (k >= 0),
+    theta = a column-global map per lambda mode, lambda_inv = synthesis."""
+
+    def __init__(self, M, N):
+        self.M, self.N = M, N
+        self.rows, self.cols = M // 2 + 1, N // 2 + 1
+        self.sign = (-1.0) ** np.arange(self.cols)
+
+    def lambda_fwd(self, P, rb, cb, rank, f_rows, send):
+        import torch
+        X = np.fft.rfft(f_rows.numpy(), axis=1) / self.N * self.sign  # (rows_r, cols)
+        send.copy_(torch.from_numpy(np.ascontiguousarray(X.T).view(np.float64).ravel()))
+
+    def theta_map(self, cols, kappas):
+        return cols * (1.0 + kappas[:, None]) + 0.25 * np.cumsum(cols, axis=1)[:, ::-1]
+
+    def theta(self, P, rb, cb, rank, recv):
+        import torch
+        c0, c1 = cb[rank], cb[rank + 1]
+        nc = c1 - c0
+        buf = recv.numpy().view(np.complex128)
+        cols = np.zeros((nc, self.rows), complex)
+        for s in range(P):
+            rs = rb[s + 1] - rb[s]
+            cols[:, rb[s]: rb[s + 1]] = buf[nc * rb[s]: nc * rb[s + 1]].reshape(nc, rs)
+        out = self.theta_map(cols, np.arange(c0, c1, dtype=float))
+        for s in range(P):
+            buf[nc * rb[s]: nc * rb[s + 1]] = out[:, rb[s]: rb[s + 1]].ravel()
+        recv.copy_(torch.from_numpy(buf.view(np.float64)))
+
+    def lambda_inv(self, P, rb, cb, rank, back, u_rows):
+        import torch
+        rr = rb[rank + 1] - rb[rank]
+        V = back.numpy().view(np.complex128).reshape(self.cols, rr).T * self.sign
+        u_rows.copy_(torch.from_numpy(np.fft.irfft(V, n=self.N, axis=1) * self.N))
+
+    def full(self, f):
+        X = np.fft.rfft(f, axis=1) / self.N * self.sign
+        V = self.theta_map(X.T.copy(), np.arange(self.cols, dtype=float)).T
+        return np.fft.irfft(V * self.sign, n=self.N, axis=1) * self.N
+
+
+def _worker(rank, world, port, M, N, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1510_08094_b200.distributed import SlabSolver, gather_rows
+    rng = np.random.default_rng(7)
+    f = rng.standard_normal((M // 2 + 1, N))
+    st = NumpyStages(M, N)
+    solver = SlabSolver(M, N, rank, world, device=torch.device("cpu"), backend=st)
+    rows = torch.from_numpy(f[solver.rb[rank]: solver.rb[rank + 1]].copy())
+    u = solver.solve(rows)
+    allu = gather_rows(u, solver.rb)
+    if rank == 0:
+        q.put((allu.numpy(), st.full(f)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,M,N", [(2, 40, 24), (3, 38, 30)])
+def test_slab_orchestration_gloo(world, M, N):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, ref = q.get(timeout=90)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+
+
+def test_slab_bounds_cover():
+    from paper_1510_08094_b200.distributed import slab_bounds
+    for total in (1, 7, 10001, 5001):
+        for P in (1, 2, 3, 8):
+            b = slab_bounds(total, P)
+            assert b[0] == 0 and b[-1] == total and all(b[i] <= b[i + 1] for i in range(P))

@@ -1,0 +1,29 @@
+"""CPU: the C++ drop-in shim (include/spherekit/poisson_b200.hpp) compiles
+against the reference's own headers and links with libsk_poisson.so; without
+a device it fails loudly instead of falling back to the CPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INC = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not present")
+def test_cpp_shim_against_reference_headers(tmp_path):
+    from paper_1510_08094_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_1510_08094_b200 import build
+        build.build()
+    exe = tmp_path / "shim_check"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{REF_INC}", f"-I{ROOT}/include",
+                    os.path.join(ROOT, "tests", "cpp", "shim_check.cpp"), f"-L{libdir}", "-l:libsk_poisson.so",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    import torch
+    if torch.cuda.is_available():
+        assert r.returncode == 0, r.stdout + r.stderr
+    else:
+        assert r.returncode == 3 and "device error" in r.stdout, r.stdout + r.stderr

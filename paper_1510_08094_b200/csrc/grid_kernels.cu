@@ -29,6 +29,19 @@ namespace cg = cooperative_groups;
 
 namespace sk {
 
+#ifdef SK_PHASES
+__device__ unsigned long long g_phase[4096][12];
+#define SK_PROBE(i)                                                         \
+    do {                                                                    \
+        __syncthreads();                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_phase[blockIdx.x][i] = clock64(); \
+    } while (0)
+#else
+#define SK_PROBE(i) \
+    do {            \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ layout
 // Element (kl, p) of a lambda-mode column on the theta rank: pieces from each
 // source rank s are [kl][p - row_b[s]] blocks of ncols x rows_s, concatenated.
@@ -158,6 +171,8 @@ __device__ __forceinline__ int t_of(int tau, int par, int L) {
 // side +: t = t0, t0+2, ... (tau ascending from tau0), side -: t = -2+par,
 // -4+par, ... (tau descending from L-1).  Element i of a chain is coupled to
 // i-1 (towards j = 0) and i+1 (towards the truncation boundary).
+constexpr int kSegMax = 12;  // register-resident chain segment length per thread
+
 struct Chain {
     int n;       // length
     int tau0;    // natural FFT index of element 0
@@ -345,6 +360,116 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     __syncthreads();
 }
 
+// Register-resident variant of solve_chain for segments of at most SMAX
+// elements per thread: every chain element is read from shared memory once
+// (its position through the digit-reversal table once), F, r' and the pivots
+// stay in registers across the four sweeps, and x is written once.
+template <int SMAX>
+__device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4* wsc, const Chain& ch, int L,
+                                double2 inner, double& fmax_acc, double2& wsum, bool want_wsum, double2* x_first) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int n = ch.n;
+    const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
+    const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
+    const int m = e - s;
+    int pos[SMAX];
+    double2 v[SMAX];   // X, then F, then r'
+    double ipv[SMAX];
+#pragma unroll
+    for (int u = 0; u < SMAX; ++u)
+        if (u < m) pos[u] = __ldg(rev + ch.tau0 + ch.dtau * (s + u));
+    const double ip_before = (s > 0 && m > 0) ? ip[ch.tau0 + ch.dtau * (s - 1)] : 0.0;
+    double2 xlo = make_double2(0.0, 0.0), xhi = make_double2(0.0, 0.0);
+    if (m > 0) {
+        xlo = (s == 0) ? inner : a[__ldg(rev + ch.tau0 + ch.dtau * (s - 1))];
+        xhi = (e < n) ? a[__ldg(rev + ch.tau0 + ch.dtau * e)] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < SMAX; ++u) {
+        if (u < m) {
+            v[u] = a[pos[u]];
+            ipv[u] = ip[ch.tau0 + ch.dtau * (s + u)];
+        }
+    }
+    // F = Msin^2 X in registers (ascending, keeping the previous original X)
+    {
+        double2 xm = xlo;
+#pragma unroll
+        for (int u = 0; u < SMAX; ++u) {
+            if (u < m) {
+                const double2 x0 = v[u];
+                const double2 xp = (u + 1 < m) ? v[u + 1] : xhi;
+                const double d2 = chainD2(ch, s + u, L);
+                v[u] = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+                fmax_acc = fmax(fmax_acc, v[u].x * v[u].x + v[u].y * v[u].y);  // squared
+                xm = x0;
+            }
+        }
+    }
+    // local forward summary
+    V4 aff = AffOp::identity();
+    {
+        double ipp = ip_before;
+#pragma unroll
+        for (int u = 0; u < SMAX; ++u) {
+            if (u < m) {
+                const double al = -chainA(ch, s + u, L) * ipp;
+                aff = V4{al * aff.a, fma(al, aff.b, v[u].x), fma(al, aff.c, v[u].y), 0.0};
+                ipp = ipv[u];
+            }
+        }
+    }
+    const V4 rin = block_exclusive_scan<AffOp, false>(aff, wsc);
+    // forward sweep: r' in registers
+    {
+        double2 rp = make_double2(rin.b, rin.c);
+        double ipp = ip_before;
+#pragma unroll
+        for (int u = 0; u < SMAX; ++u) {
+            if (u < m) {
+                const double al = -chainA(ch, s + u, L) * ipp;
+                rp = make_double2(fma(al, rp.x, v[u].x), fma(al, rp.y, v[u].y));
+                v[u] = rp;
+                ipp = ipv[u];
+            }
+        }
+    }
+    // local backward summary
+    V4 baff = AffOp::identity();
+#pragma unroll
+    for (int u = SMAX - 1; u >= 0; --u) {
+        if (u < m) {
+            const double iv = ipv[u];
+            const double be = -chainC(ch, s + u, L) * iv;
+            baff = V4{be * baff.a, fma(be, baff.b, v[u].x * iv), fma(be, baff.c, v[u].y * iv), 0.0};
+        }
+    }
+    const V4 xin = block_exclusive_scan<AffOp, true>(baff, wsc);  // also orders every read above before the writes below
+    double2 ws = make_double2(0.0, 0.0);
+    {
+        double2 x = make_double2(xin.b, xin.c);
+#pragma unroll
+        for (int u = SMAX - 1; u >= 0; --u) {
+            if (u < m) {
+                const double iv = ipv[u];
+                const double c = -chainC(ch, s + u, L) * iv;
+                x = make_double2(fma(c, x.x, v[u].x * iv), fma(c, x.y, v[u].y * iv));
+                a[pos[u]] = x;
+                if (want_wsum) {
+                    const double t = ch.t0 + ch.dt * (s + u);
+                    const double w = 2.0 / (1.0 - t * t);
+                    ws.x = fma(w, x.x, ws.x);
+                    ws.y = fma(w, x.y, ws.y);
+                }
+                if (s + u == 0) *x_first = x;
+            }
+        }
+    }
+    wsum.x += ws.x;
+    wsum.y += ws.y;
+    __syncthreads();
+}
+
 // The lowest lambda modes are only weakly diagonally dominant (k = 0 not at
 // all); for them the segmented sweeps lose digits, so one thread runs the
 // plain sequential recurrences (pivots from the table).  The chain is walked
@@ -514,6 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const size_t prow = (static_cast<size_t>(kl) * 2 + par) * L;  // pivot row (table index)
 
     // ---- bulk copies: the raw column (L+1 values) and the t > 0 chain's pivots
+    SK_PROBE(0);
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -543,6 +669,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     mbar_wait(&bars[0], 0);
     __syncthreads();
 
+    SK_PROBE(1);
     // ---- DFS fold (first radix-2 step) in place, scaled by 1/M
     const double invM = 1.0 / P.g.M;
     for (int r = tid; r <= L / 2; r += nthr) {
@@ -561,7 +688,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         }
     }
     __syncthreads();
+    SK_PROBE(2);
     fft_forward(a, P.fd, T, tid, nthr);
+    SK_PROBE(3);
 
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
     double* st = P.stats + 4 * rhs;
@@ -609,7 +738,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const bool want_wsum = (kg == 0 && par == 0);
     const bool seq = kg < P.kseq;
     if (seq) solve_chain_seq(a, rev, ipp, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    else if (cp.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
     else solve_chain(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    SK_PROBE(4);
     // the t < 0 chain's pivots replace the t > 0 chain's in the window
     const double* ipm = ip;
     if (cm.n > 0) {
@@ -622,8 +753,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         }
         mbar_wait(&bars[1], 0);
     }
+    SK_PROBE(5);
     if (seq) solve_chain_seq(a, rev, ipm, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    else if (cm.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
     else solve_chain(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    SK_PROBE(6);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
         double2 x0;
@@ -652,7 +786,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     }
     __syncthreads();
 
+    SK_PROBE(7);
     fft_inverse(a, P.fd, T, tid, nthr);
+    SK_PROBE(8);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
     cluster.sync();
@@ -666,7 +802,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
         colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }
+    SK_PROBE(9);
     cluster.sync();
+    SK_PROBE(10);
 }
 
 // ------------------------------------------------------------------ shgen

@@ -1,0 +1,33 @@
+"""Per-phase cycle breakdown of theta_kernel (debug build with -DSK_PHASES:
+tools/libsk_poisson_phases.so).  Usage: python tools/phases.py C3"""
+import ctypes, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1510_08094_b200 import _lib
+_lib.LIB_PATH = os.path.join(ROOT, "tools", "libsk_poisson_phases.so")
+import torch
+from paper_1510_08094_b200 import inputs
+from paper_1510_08094_b200.poisson import Plan
+
+cfg = inputs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"]
+plan = Plan(cfg.M, cfg.N)
+rows = cfg.M // 2 + 1
+f = torch.empty((rows, cfg.N), dtype=torch.float64, device="cuda")
+plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(1, cfg.L, cfg.p)).cuda(), f)
+u = torch.empty_like(f)
+for _ in range(3):
+    plan.solve_grid(f, u)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (4096 * 12))()
+assert _lib.load().sk_debug_phases(buf) == 0
+a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 12).astype(np.int64)
+n = min(4096, 2 * (cfg.N // 2 + 1))
+a = a[:n]
+names = ["issue loads", "TMA wait", "fold", "fft fwd", "mean+inner+chain+ solve", "pivot- TMA wait",
+         "chain- solve", "x0/fmax/export", "fft inv", "cluster sync+combine", ""]
+d = np.diff(a[:, :11], axis=1)
+tot = (a[:, 10] - a[:, 0])
+print(f"{cfg.name}: CTAs sampled {n}, mean cycles per CTA {tot.mean():.0f}")
+for i in range(10):
+    print(f"  {names[i]:28s} {d[:, i].mean():9.0f} cyc  {100 * d[:, i].mean() / tot.mean():5.1f}%")

@@ -30,7 +30,7 @@ namespace cg = cooperative_groups;
 namespace sk {
 
 #ifdef SK_PHASES
-__device__ unsigned long long g_phase[4096][12];
+__device__ unsigned long long g_phase[4096][24];
 #define SK_PROBE(i)                                                         \
     do {                                                                    \
         __syncthreads();                                                    \
@@ -391,6 +391,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
             ipv[u] = ip[ch.tau0 + ch.dtau * (s + u)];
         }
     }
+    if (ch.dt > 0) SK_PROBE(12);
     // F = Msin^2 X in registers (ascending, keeping the previous original X)
     {
         double2 xm = xlo;
@@ -406,6 +407,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
             }
         }
     }
+    if (ch.dt > 0) SK_PROBE(13);
     // local forward summary
     V4 aff = AffOp::identity();
     {
@@ -419,7 +421,9 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
             }
         }
     }
+    if (ch.dt > 0) SK_PROBE(14);
     const V4 rin = block_exclusive_scan<AffOp, false>(aff, wsc);
+    if (ch.dt > 0) SK_PROBE(15);
     // forward sweep: r' in registers
     {
         double2 rp = make_double2(rin.b, rin.c);
@@ -434,6 +438,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
             }
         }
     }
+    if (ch.dt > 0) SK_PROBE(16);
     // local backward summary
     V4 baff = AffOp::identity();
 #pragma unroll
@@ -444,7 +449,9 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
             baff = V4{be * baff.a, fma(be, baff.b, v[u].x * iv), fma(be, baff.c, v[u].y * iv), 0.0};
         }
     }
+    if (ch.dt > 0) SK_PROBE(17);
     const V4 xin = block_exclusive_scan<AffOp, true>(baff, wsc);  // also orders every read above before the writes below
+    if (ch.dt > 0) SK_PROBE(18);
     double2 ws = make_double2(0.0, 0.0);
     {
         double2 x = make_double2(xin.b, xin.c);
@@ -468,6 +475,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
     wsum.x += ws.x;
     wsum.y += ws.y;
     __syncthreads();
+    if (ch.dt > 0) SK_PROBE(19);
 }
 
 // The lowest lambda modes are only weakly diagonally dominant (k = 0 not at

@@ -290,9 +290,9 @@ sk_status check_precondition(sk_plan_t p, int nrhs) {
 }  // namespace
 
 #ifdef SK_PHASES
-namespace sk { extern __device__ unsigned long long g_phase[4096][12]; }
+namespace sk { extern __device__ unsigned long long g_phase[4096][24]; }
 extern "C" int sk_debug_phases(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, sk::g_phase, sizeof(unsigned long long) * 4096 * 12) == cudaSuccess ? 0 : 1;
+    return cudaMemcpyFromSymbol(out, sk::g_phase, sizeof(unsigned long long) * 4096 * 24) == cudaSuccess ? 0 : 1;
 }
 #endif
 

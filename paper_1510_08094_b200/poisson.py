@@ -85,6 +85,16 @@ class Plan:
 
     def set_stream(self, stream_ptr: int) -> None:
         _lib.check(self.lib.sk_plan_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+        self._stream = stream_ptr
+
+    def _follow_torch(self, t) -> None:
+        """Device tensors: run on torch's current stream of that device, so the
+        library's reads/writes are ordered with the surrounding torch work."""
+        if _is_device(t):
+            import torch
+            sp = torch.cuda.current_stream(t.device).cuda_stream
+            if getattr(self, "_stream", None) != sp:
+                self.set_stream(sp)
 
     def sync(self) -> None:
         _lib.check(self.lib.sk_sync(self._h))
@@ -123,6 +133,7 @@ class Plan:
                 F = np.ascontiguousarray(F, dtype=np.complex128)
                 X = np.empty_like(F)
         self._check_shape(F, (self.M, self.N))
+        self._follow_torch(F)
         flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
         _lib.check(self.lib.sk_solve_coeffs(self._h, _ptr(F), _ptr(X), flags))
         return X
@@ -133,6 +144,7 @@ class Plan:
             F = np.ascontiguousarray(F, dtype=np.complex128)
             X = np.ascontiguousarray(X, dtype=np.complex128)
         out = (ctypes.c_double * 3)()
+        self._follow_torch(F)
         _lib.check(self.lib.sk_residual(self._h, _ptr(F), _ptr(X), out, _lib.SK_DEVICE if dev else _lib.SK_HOST))
         return ResidualReport(out[0], out[1], out[2])
 
@@ -157,6 +169,7 @@ class Plan:
                 u = np.empty_like(f)
             if coeffs:
                 Xh = np.empty((self.nrhs, self.N // 2 + 1, self.M), np.complex128)
+        self._follow_torch(f)
         flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
         _lib.check(self.lib.sk_solve_grid(self._h, _ptr(f), _ptr(u), _ptr(Xh), flags))
         if coeffs:
@@ -171,6 +184,7 @@ class Plan:
         return complex(out[0], out[1]), out[2]
 
     def shgen(self, L: int, coeffs_dev, phys_dev) -> None:
+        self._follow_torch(phys_dev)
         _lib.check(self.lib.sk_shgen(self._h, int(L), _ptr(coeffs_dev), _ptr(phys_dev)))
 
     # -- slab stages (multi-GPU)
@@ -181,14 +195,17 @@ class Plan:
 
     def stage_lambda_fwd(self, P, row_b, col_b, rank, f_rows, send):
         rb, cb = self._bounds(P, row_b, col_b)
+        self._follow_torch(f_rows)
         _lib.check(self.lib.sk_stage_lambda_fwd(self._h, P, rb, cb, rank, _ptr(f_rows), _ptr(send)))
 
     def stage_theta(self, P, row_b, col_b, rank, recv):
         rb, cb = self._bounds(P, row_b, col_b)
+        self._follow_torch(recv)
         _lib.check(self.lib.sk_stage_theta(self._h, P, rb, cb, rank, _ptr(recv)))
 
     def stage_lambda_inv(self, P, row_b, col_b, rank, back, u_rows):
         rb, cb = self._bounds(P, row_b, col_b)
+        self._follow_torch(back)
         _lib.check(self.lib.sk_stage_lambda_inv(self._h, P, rb, cb, rank, _ptr(back), _ptr(u_rows)))
 
     def _check_shape(self, a, tail):

@@ -238,43 +238,42 @@ __device__ __forceinline__ void bf_load(Bfly<R>& B, const double2* a, int b, int
     for (int q = 0; q < R; ++q) B.x[q] = a[B.base + q * span];
 }
 
-// Forward DIF butterfly: y = DFT_R(x); y_q *= w^(q j); store in place.
-template <int R>
-__device__ __forceinline__ void bf_dif(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
-    dft<R, -1>(B.x);
-    if (B.j != 0) {
-        const double2 w1 = T(B.j * tw);
-        double2 w = w1;
+// Twiddle powers w^q, q = 1..R-1, w = T(j tw) for SIGN = -1 (exp(-2 pi i ...))
+// and its conjugate for SIGN = +1, built by repeated multiplication.
+template <int R, int SIGN>
+__device__ __forceinline__ void bf_twiddle(double2* x, int j, int tw, const Tw& T) {
+    if (j == 0) return;
+    double2 w1 = T(j * tw);
+    if (SIGN > 0) w1.y = -w1.y;
+    double2 w = w1;
 #pragma unroll
-        for (int q = 1; q < R; ++q) {
-            B.x[q] = cmul(B.x[q], w);
-            if (q + 1 < R) w = cmul(w, w1);
-        }
+    for (int q = 1; q < R; ++q) {
+        x[q] = cmul(x[q], w);
+        if (q + 1 < R) w = cmul(w, w1);
     }
+}
+
+// DIF butterfly: y = DFT_R(x); y_q *= w^(q j); store in place.
+template <int R, int SIGN>
+__device__ __forceinline__ void bf_dif(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
+    dft<R, SIGN>(B.x);
+    bf_twiddle<R, SIGN>(B.x, B.j, tw, T);
 #pragma unroll
     for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
 }
 
-// Inverse DIT butterfly: x_q *= conj(w)^(q j); y = DFT^+_R(x); store in place.
-template <int R>
+// DIT butterfly: x_q *= w^(q j); y = DFT_R(x); store in place.
+template <int R, int SIGN>
 __device__ __forceinline__ void bf_dit(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
-    if (B.j != 0) {
-        const double2 w1 = T(B.j * tw);
-        double2 w = w1;
-#pragma unroll
-        for (int q = 1; q < R; ++q) {
-            B.x[q] = cmulc(B.x[q], w);
-            if (q + 1 < R) w = cmul(w, w1);
-        }
-    }
-    dft<R, +1>(B.x);
+    bf_twiddle<R, SIGN>(B.x, B.j, tw, T);
+    dft<R, SIGN>(B.x);
 #pragma unroll
     for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
 }
 
 // One stage over all butterflies; small radices keep two butterflies'
 // shared-memory loads in flight.
-template <int R, bool FWD>
+template <int R, bool DIF, int SIGN>
 __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
     const int span = d.span[s], tw = d.tw[s];
     const unsigned mag = d.mag[s];
@@ -286,59 +285,72 @@ __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, c
             Bfly<R> p, q;
             bf_load(p, a, b, span, mag, sh1, sh2);
             bf_load(q, a, b + nthr, span, mag, sh1, sh2);
-            if constexpr (FWD) {
-                bf_dif(p, a, span, tw, T);
-                bf_dif(q, a, span, tw, T);
+            if constexpr (DIF) {
+                bf_dif<R, SIGN>(p, a, span, tw, T);
+                bf_dif<R, SIGN>(q, a, span, tw, T);
             } else {
-                bf_dit(p, a, span, tw, T);
-                bf_dit(q, a, span, tw, T);
+                bf_dit<R, SIGN>(p, a, span, tw, T);
+                bf_dit<R, SIGN>(q, a, span, tw, T);
             }
         }
     }
     for (; b < nb; b += nthr) {
         Bfly<R> p;
         bf_load(p, a, b, span, mag, sh1, sh2);
-        if constexpr (FWD) bf_dif(p, a, span, tw, T);
-        else bf_dit(p, a, span, tw, T);
+        if constexpr (DIF) bf_dif<R, SIGN>(p, a, span, tw, T);
+        else bf_dit<R, SIGN>(p, a, span, tw, T);
     }
 }
 
-// Whole transforms; callers must __syncthreads() before (data ready) — the
-// routines end with a barrier.
+template <bool DIF, int SIGN>
+__device__ __forceinline__ void fft_stage_dispatch(double2* a, const FftDesc& d, int s, const Tw& T, int tid,
+                                                   int nthr) {
+    switch (d.R[s]) {
+        case 2: fft_stage<2, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 3: fft_stage<3, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 4: fft_stage<4, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 5: fft_stage<5, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 7: fft_stage<7, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 8: fft_stage<8, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 10: fft_stage<10, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 16: fft_stage<16, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 20: fft_stage<20, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        default: fft_stage<25, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+    }
+}
+
+// Whole transforms (callers __syncthreads() before; each ends with a barrier).
+// DIF stages run s = 0..nst-1 and take natural order to digit-reversed order;
+// DIT stages run s = nst-1..0 and take digit-reversed order to natural order.
+//   fft_forward      DIF, exp(-):  natural -> reversed   (lambda forward)
+//   fft_inverse      DIT, exp(+):  reversed -> natural   (lambda inverse)
+//   fft_forward_dit  DIT, exp(-):  reversed -> natural   (theta forward)
+//   fft_inverse_dif  DIF, exp(+):  natural -> reversed   (theta inverse)
+template <bool DIF, int SIGN>
+__device__ __forceinline__ void fft_run(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
+    if constexpr (DIF) {
+        for (int s = 0; s < d.nst; ++s) {
+            fft_stage_dispatch<true, SIGN>(a, d, s, T, tid, nthr);
+            __syncthreads();
+        }
+    } else {
+        for (int s = d.nst - 1; s >= 0; --s) {
+            fft_stage_dispatch<false, SIGN>(a, d, s, T, tid, nthr);
+            __syncthreads();
+        }
+    }
+}
 __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    for (int s = 0; s < d.nst; ++s) {
-        switch (d.R[s]) {
-            case 2: fft_stage<2, true>(a, d, s, T, tid, nthr); break;
-            case 3: fft_stage<3, true>(a, d, s, T, tid, nthr); break;
-            case 4: fft_stage<4, true>(a, d, s, T, tid, nthr); break;
-            case 5: fft_stage<5, true>(a, d, s, T, tid, nthr); break;
-            case 7: fft_stage<7, true>(a, d, s, T, tid, nthr); break;
-            case 8: fft_stage<8, true>(a, d, s, T, tid, nthr); break;
-            case 10: fft_stage<10, true>(a, d, s, T, tid, nthr); break;
-            case 16: fft_stage<16, true>(a, d, s, T, tid, nthr); break;
-            case 20: fft_stage<20, true>(a, d, s, T, tid, nthr); break;
-            default: fft_stage<25, true>(a, d, s, T, tid, nthr); break;
-        }
-        __syncthreads();
-    }
+    fft_run<true, -1>(a, d, T, tid, nthr);
 }
-
 __device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    for (int s = d.nst - 1; s >= 0; --s) {
-        switch (d.R[s]) {
-            case 2: fft_stage<2, false>(a, d, s, T, tid, nthr); break;
-            case 3: fft_stage<3, false>(a, d, s, T, tid, nthr); break;
-            case 4: fft_stage<4, false>(a, d, s, T, tid, nthr); break;
-            case 5: fft_stage<5, false>(a, d, s, T, tid, nthr); break;
-            case 7: fft_stage<7, false>(a, d, s, T, tid, nthr); break;
-            case 8: fft_stage<8, false>(a, d, s, T, tid, nthr); break;
-            case 10: fft_stage<10, false>(a, d, s, T, tid, nthr); break;
-            case 16: fft_stage<16, false>(a, d, s, T, tid, nthr); break;
-            case 20: fft_stage<20, false>(a, d, s, T, tid, nthr); break;
-            default: fft_stage<25, false>(a, d, s, T, tid, nthr); break;
-        }
-        __syncthreads();
-    }
+    fft_run<false, +1>(a, d, T, tid, nthr);
+}
+__device__ __forceinline__ void fft_forward_dit(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
+    fft_run<false, -1>(a, d, T, tid, nthr);
+}
+__device__ __forceinline__ void fft_inverse_dif(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
+    fft_run<true, +1>(a, d, T, tid, nthr);
 }
 
 // Stage the 2L-th-root twiddle tables of `d` into shared memory.

@@ -172,7 +172,6 @@ __device__ __forceinline__ int t_of(int tau, int par, int L) {
 // -4+par, ... (tau descending from L-1).  Element i of a chain is coupled to
 // i-1 (towards j = 0) and i+1 (towards the truncation boundary).
 constexpr int kSegMax = 12;  // register-resident chain segment length per thread
-constexpr int kFoldMax = 12;  // column pairs per thread in the fold/permutation
 
 struct Chain {
     int n;       // length
@@ -274,7 +273,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     const int n = ch.n;
     const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
     const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
-    auto pos = [&](int i) { return ch.tau0 + ch.dtau * i; };  // natural order
+    auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
     auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
         const double d2 = chainD2(ch, i, L);
         return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
@@ -378,12 +377,12 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
     double ipv[SMAX];
 #pragma unroll
     for (int u = 0; u < SMAX; ++u)
-        if (u < m) pos[u] = ch.tau0 + ch.dtau * (s + u);
+        if (u < m) pos[u] = __ldg(rev + ch.tau0 + ch.dtau * (s + u));
     const double ip_before = (s > 0 && m > 0) ? ip[ch.tau0 + ch.dtau * (s - 1)] : 0.0;
     double2 xlo = make_double2(0.0, 0.0), xhi = make_double2(0.0, 0.0);
     if (m > 0) {
-        xlo = (s == 0) ? inner : a[ch.tau0 + ch.dtau * (s - 1)];
-        xhi = (e < n) ? a[ch.tau0 + ch.dtau * e] : make_double2(0.0, 0.0);
+        xlo = (s == 0) ? inner : a[__ldg(rev + ch.tau0 + ch.dtau * (s - 1))];
+        xhi = (e < n) ? a[__ldg(rev + ch.tau0 + ch.dtau * e)] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < SMAX; ++u) {
@@ -490,7 +489,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
     constexpr int U = 8;
     if (threadIdx.x == 0 && ch.n > 0) {
         const int n = ch.n;
-        auto pos = [&](int i) { return ch.tau0 + ch.dtau * i; };  // natural order
+        auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
         // ---- forward: r'_i = F_i + alpha_i r'_{i-1}
         int pc[U];
         double2 xc[U];
@@ -679,47 +678,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(1);
-    // ---- DFS fold (first radix-2 step), scaled by 1/M, scattered into
-    // digit-reversed order: the forward transform is decimation in time
-    // (reversed in, natural out), so the chains below see natural order.
-    // Every value of the CTA passes through registers (kFoldMax pairs per
-    // thread) so the in-place permutation cannot overwrite an unread value.
+    // ---- DFS fold (first radix-2 step) in place, scaled by 1/M
     const double invM = 1.0 / P.g.M;
-    {
-        double2 v0[kFoldMax], v1[kFoldMax];
-        int q0[kFoldMax], q1[kFoldMax];
-#pragma unroll
-        for (int u = 0; u < kFoldMax; ++u) {
-            const int r = tid + u * nthr;
-            q0[u] = -1;
-            q1[u] = -1;
-            if (r <= L / 2) {
-                const int rm = L - r;
-                const double2 ar = a[r];
-                const double2 am = a[rm];
-                if (par == 0) {
-                    // e_r = a_r + s a_{L-r}
-                    v0[u] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
-                    v1[u] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
-                } else {
-                    // o_r = (a_r - s a_{L-r}) w_M^{-r}
-                    v0[u] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
-                    v1[u] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
-                }
-                q0[u] = __ldg(rev + r);
-                if (rm < L && rm != r) q1[u] = __ldg(rev + rm);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kFoldMax; ++u) {
-            if (q0[u] >= 0) a[q0[u]] = v0[u];
-            if (q1[u] >= 0) a[q1[u]] = v1[u];
+    for (int r = tid; r <= L / 2; r += nthr) {
+        const int rm = L - r;
+        const double2 ar = a[r];
+        const double2 am = a[rm];
+        if (par == 0) {
+            // e_r = a_r + s a_{L-r}
+            a[r] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
+            if (rm < L && rm != r) a[rm] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
+        } else {
+            // o_r = (a_r - s a_{L-r}) w_M^{-r}
+            a[r] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
+            if (rm < L && rm != r)
+                a[rm] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
         }
     }
     __syncthreads();
     SK_PROBE(2);
-    fft_forward_dit(a, P.fd, T, tid, nthr);
+    fft_forward(a, P.fd, T, tid, nthr);
     SK_PROBE(3);
 
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
@@ -729,7 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         for (int tau = tid; tau < L; tau += nthr) {
             const double t = t_of(tau, 0, L);
             const double w = 2.0 / (1.0 - t * t);
-            const double2 x = a[tau];
+            const double2 x = a[__ldg(rev + tau)];
             acc.x = fma(w, x.x, acc.x);
             acc.y = fma(w, x.y, acc.y);
         }
@@ -745,17 +723,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     // inner neighbours and the j = 0 row data, read before any chain writes
     if (tid == 0) {
         if (par == 0) {
-            const double2 x0 = a[0];
-            const double2 xp2 = cp.n > 0 ? a[1] : make_double2(0.0, 0.0);
-            const double2 xm2 = cm.n > 0 ? a[L - 1] : make_double2(0.0, 0.0);
+            const double2 x0 = a[__ldg(rev + 0)];
+            const double2 xp2 = cp.n > 0 ? a[__ldg(rev + 1)] : make_double2(0.0, 0.0);
+            const double2 xm2 = cm.n > 0 ? a[__ldg(rev + L - 1)] : make_double2(0.0, 0.0);
             misc[0] = x0;
             misc[1] = x0;
             // F_0 = -1/4 X_{-2} + d2(0) X_0 - 1/4 X_2
             const double d2 = msin2_diag(0, L);
             misc[2] = make_double2(d2 * x0.x - 0.25 * (xm2.x + xp2.x), d2 * x0.y - 0.25 * (xm2.y + xp2.y));
         } else {
-            misc[0] = cm.n > 0 ? a[L - 1] : make_double2(0.0, 0.0);  // X_{-1}: inner of t>0 chain
-            misc[1] = cp.n > 0 ? a[0] : make_double2(0.0, 0.0);      // X_{+1}: inner of t<0 chain
+            misc[0] = cm.n > 0 ? a[__ldg(rev + L - 1)] : make_double2(0.0, 0.0);  // X_{-1}: inner of t>0 chain
+            misc[1] = cp.n > 0 ? a[__ldg(rev + 0)] : make_double2(0.0, 0.0);      // X_{+1}: inner of t<0 chain
             misc[2] = make_double2(0.0, 0.0);
         }
         misc[3] = make_double2(0.0, 0.0);
@@ -799,7 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
             // constraint row 2 pi w^T X_0 = 0 replaces row j = 0 (w_0 = 2)
             x0 = make_double2(-0.5 * wsum.x, -0.5 * wsum.y);
         }
-        a[0] = x0;
+        a[__ldg(rev + 0)] = x0;
     }
     const double fm = sqrt(block_max(fmax_acc, red));
     if (tid == 0) atomic_max_nonneg(st + 2, fm);
@@ -811,13 +789,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
                       static_cast<long long>(kg) * P.g.M;
         for (int tau = tid; tau < L; tau += nthr) {
             const int t = t_of(tau, par, L);
-            xo[t + L] = a[tau];
+            xo[t + L] = a[__ldg(rev + tau)];
         }
     }
     __syncthreads();
 
     SK_PROBE(7);
-    fft_inverse_dif(a, P.fd, T, tid, nthr);  // natural in, digit-reversed out
+    fft_inverse(a, P.fd, T, tid, nthr);
     SK_PROBE(8);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
@@ -828,7 +806,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const int p_lo = par == 0 ? 0 : half;
     const int p_hi = par == 0 ? half : L + 1;
     for (int p = p_lo + tid; p < p_hi; p += nthr) {
-        const int pm = __ldg(rev + (p == L ? 0 : p));
+        const int pm = p == L ? 0 : p;
         const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
         colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }

@@ -372,8 +372,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         p->smem_lambda = static_cast<size_t>(Ll) * 16 + static_cast<size_t>(p->fl.d.nhi + p->fl.d.nlo) * 16 +
                          static_cast<size_t>((Ll + 3) & ~3) * 4 + 16;
         const size_t cap = 227 * 1024;
-        const bool fold_fits = (Lt / 2 + 1) <= 12 * p->thr_theta;  // kFoldMax pairs per thread
-        if (p->smem_theta > cap || p->smem_lambda > cap || !fold_fits) {
+        if (p->smem_theta > cap || p->smem_lambda > cap) {
             p->grid_ok = false;
             p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +
                           " exceeds the on-chip (shared memory) limit of this build";

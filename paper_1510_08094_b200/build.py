@@ -24,7 +24,7 @@ UNITS = [
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("sk_poisson.cu", []),
 ]
-HEADERS = ["sk_internal.h", "params.h", "fft_dev.cuh", "block_ops.cuh"]
+HEADERS = ["sk_internal.h", "params.h", "fft_dev.cuh", "block_ops.cuh", "tma.cuh"]
 
 
 def nvcc() -> str:

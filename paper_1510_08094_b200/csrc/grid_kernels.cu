@@ -54,14 +54,22 @@ __device__ __forceinline__ size_t theta_addr(const Slabs& sl, int ncols, int kl,
 }
 
 
-// One CTA per physical row: load the real row as N/2 complex pairs, forward
-// DIF FFT, split into the N/2+1 modes of the real transform, apply
-// analyze_1d's (-1)^k / N (fourier.cpp:44-51), store transposed.
-__global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+// Box of the spectrum tensor map: 256 lambda modes x one physical row
+// (2 doubles), i.e. the strided [k][p] column slice of one row.
+constexpr int kBoxModes = 256;
+constexpr int kLamPairs = 12;  // mode pairs per thread held in registers
+
+// One CTA per physical row: TMA bulk load of the real row (N/2 complex
+// pairs), forward DIF FFT, split into the N/2+1 modes of the real transform
+// with analyze_1d's (-1)^k / N (fourier.cpp:44-51), staged in natural order
+// in shared memory and written to the mode-major spectrum by TMA tensor
+// stores (the row -> column transpose is done by the copy engine).
+__global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
+    const int Lpad = (L / kBoxModes + 1) * kBoxModes;  // >= L+1, whole boxes
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + L;
+    double2* s_hi = a + Lpad;
     double2* s_lo = s_hi + P.fd.nhi;
     int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
     uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
@@ -82,58 +90,75 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P) {
     mbar_wait(bar, 0);
     fft_forward(a, P.fd, T, tid, nthr);
     const double invN = 1.0 / P.g.N;
-    double2* out = P.spec + rhs * P.out_rhs_stride;
-    for (int k = tid; k <= L / 2; k += nthr) {
-        const int km = L - k;  // partner mode
-        const double2 z = a[s_rev[k]];
-        const double2 zp = a[s_rev[km == L ? 0 : km]];
-        // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
-        const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
-        const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-        const double2 Xk = cadd(A, cmul(T(k), B));
-        const double2 Xm = cadd(conjd(A), cmul(T(km), conjd(B)));
-        const double sk = (k & 1) ? -invN : invN;
-        const double sm = (km & 1) ? -invN : invN;
-        out[static_cast<size_t>(k) * P.rows_local + row] = cscale(Xk, sk);
-        if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = cscale(Xm, sm);
+    // split Z (digit-reversed) into X_k, k = 0..L, through registers (the
+    // natural-order results overwrite the same buffer)
+    double2 xk[kLamPairs], xm[kLamPairs];
+#pragma unroll
+    for (int u = 0; u < kLamPairs; ++u) {
+        const int k = tid + u * nthr;
+        if (k <= L / 2) {
+            const int km = L - k;  // partner mode
+            const double2 z = a[s_rev[k]];
+            const double2 zp = a[s_rev[km == L ? 0 : km]];
+            // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
+            const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
+            const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
+            xk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
+            xm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kLamPairs; ++u) {
+        const int k = tid + u * nthr;
+        if (k <= L / 2) {
+            a[k] = xk[u];
+            a[L - k] = xm[u];
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+        for (int k0 = 0; k0 <= L; k0 += kBoxModes) tma_store_3d(&tmap, 2 * row, k0, rhs, a + k0);
+        tma_store_commit_and_wait();
     }
 }
 
-// Inverse: gather the N/2+1 modes of a physical row, apply sample_grid's
-// (-1)^k (fourier.cpp:61-62), pack into N/2 complex, inverse DIT FFT, store
-// the real row (unnormalised backward transform, as FFTW_BACKWARD).
-__global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+// Inverse: TMA tensor loads gather the row's N/2+1 modes from the mode-major
+// spectrum; sample_grid's (-1)^k (fourier.cpp:61-62) and the packing into
+// N/2 complex go through registers into digit-reversed order; inverse DIT
+// FFT; the real row is stored (unnormalised, as FFTW_BACKWARD).
+__global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
+    const int Lpad = (L / kBoxModes + 1) * kBoxModes;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + L;
+    double2* s_hi = a + Lpad;
     double2* s_lo = s_hi + P.fd.nhi;
     int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int nbox = L / kBoxModes + 1;
+        mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * kBoxModes * 16);
+        for (int k0 = 0; k0 <= L; k0 += kBoxModes) tma_load_3d(a + k0, &tmap, 2 * row, k0, rhs, bar);
+    }
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
-    __syncthreads();  // the pre-processing below reads the staged twiddles
-    const double2* in = P.spec + rhs * P.in_rhs_stride;
-    // the strided gather is latency-bound: keep G pairs of loads in flight
-    constexpr int G = 4;
-    for (int k0 = tid; k0 <= L / 2; k0 += G * nthr) {
-        double2 vv[G], ww[G];
+    __syncthreads();
+    mbar_wait(bar, 0);
+    double2 zk[kLamPairs], zm[kLamPairs];
 #pragma unroll
-        for (int g2 = 0; g2 < G; ++g2) {
-            const int k = k0 + g2 * nthr;
-            if (k <= L / 2) {
-                vv[g2] = __ldg(in + static_cast<size_t>(k) * P.rows_local + row);
-                ww[g2] = __ldg(in + static_cast<size_t>(L - k) * P.rows_local + row);
-            }
-        }
-#pragma unroll
-        for (int g2 = 0; g2 < G; ++g2) {
-            const int k = k0 + g2 * nthr;
-            if (k > L / 2) continue;
+    for (int u = 0; u < kLamPairs; ++u) {
+        const int k = tid + u * nthr;
+        if (k <= L / 2) {
             const int km = L - k;
-            double2 v = vv[g2], w = ww[g2];
+            double2 v = a[k];
+            double2 w = a[km];
             if (k & 1) v = make_double2(-v.x, -v.y);
             if (km & 1) w = make_double2(-w.x, -w.y);
             if (k == 0) {  // DC and Nyquist of a real signal are real
@@ -144,13 +169,23 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P) {
             {
                 const double2 E = make_double2(v.x + w.x, v.y - w.y);
                 const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
-                a[s_rev[k]] = make_double2(E.x - O.y, E.y + O.x);
+                zk[u] = make_double2(E.x - O.y, E.y + O.x);
             }
-            if (k != 0 && km != k) {
+            {
                 const double2 E = make_double2(w.x + v.x, w.y - v.y);
                 const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-                a[s_rev[km]] = make_double2(E.x - O.y, E.y + O.x);
+                zm[u] = make_double2(E.x - O.y, E.y + O.x);
             }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kLamPairs; ++u) {
+        const int k = tid + u * nthr;
+        if (k <= L / 2) {
+            const int km = L - k;
+            a[s_rev[k]] = zk[u];
+            if (k != 0 && km != k) a[s_rev[km]] = zm[u];
         }
     }
     __syncthreads();
@@ -882,23 +917,23 @@ __global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
 }
 
 // --------------------------------------------------------- host launchers
-cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st) {
+cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(lambda_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_fwd_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P);
+    lambda_fwd_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
 
-cudaError_t launch_lambda_inv(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st) {
+cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(lambda_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_inv_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P);
+    lambda_inv_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
 

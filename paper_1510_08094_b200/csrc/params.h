@@ -2,6 +2,7 @@
 // (sk_poisson.cu) and the kernels (grid_kernels.cu, coeff_kernels.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -72,8 +73,13 @@ __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
            16 * 16 + 64 * 8 + 2 * 8;
 }
 
-cudaError_t launch_lambda_fwd(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);
-cudaError_t launch_lambda_inv(const LambdaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
+// Lambda-stage shared memory (bytes) for transform length L and twiddle table sizes.
+inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
+    const size_t lpad = static_cast<size_t>((L / 256 + 1) * 256);
+    return lpad * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>((L + 3) & ~3) * 4 + 16;
+}
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, cudaStream_t st);

@@ -1,5 +1,7 @@
 // Host side of the C ABI (include/sk_poisson.h): plans, device buffers, FFT
 // tables, launches and the error contract.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -138,6 +140,31 @@ void free_fft(DevFft& f) {
     cudaFree(f.lo);
     cudaFree(f.rev);
     f = DevFft{};
+}
+
+// Tensor map over a mode-major spectrum [rhs][k][p] (complex, rows p
+// contiguous) as a 3-D float64 tensor {2*rows, cols, nrhs}; one box is one
+// row's slice of 256 consecutive modes.
+sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled is not available");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * rows), static_cast<cuuint64_t>(cols),
+                                static_cast<cuuint64_t>(nrhs)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rows) * 16, static_cast<cuuint64_t>(rows) * cols * 16};
+    const cuuint32_t box[3] = {2, 256, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return SK_OK;
 }
 
 int round_threads(long long want, int lo, int hi) {
@@ -369,10 +396,10 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     if (p->grid_ok) {
         const int Lt = M / 2, Ll = N / 2;
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
-        p->smem_lambda = static_cast<size_t>(Ll) * 16 + static_cast<size_t>(p->fl.d.nhi + p->fl.d.nlo) * 16 +
-                         static_cast<size_t>((Ll + 3) & ~3) * 4 + 16;
+        p->smem_lambda = sk::lambda_smem_bytes(Ll, p->fl.d.nhi, p->fl.d.nlo);
         const size_t cap = 227 * 1024;
-        if (p->smem_theta > cap || p->smem_lambda > cap) {
+        const bool pairs_fit = (Ll / 2 + 1) <= 12 * p->thr_lambda;  // kLamPairs pairs per thread
+        if (p->smem_theta > cap || p->smem_lambda > cap || !pairs_fit) {
             p->grid_ok = false;
             p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +
                           " exceeds the on-chip (shared memory) limit of this build";
@@ -547,8 +574,11 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.out_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
         lp.f = f_dev;
         lp.spec = spec;
+        CUtensorMap map;
+        sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
+        if (ms != SK_OK) return ms;
         if (p->timing) CU(cudaEventRecord(p->ev[0], p->stream));
-        CU(sk::launch_lambda_fwd(lp, p->thr_lambda, p->smem_lambda, p->stream));
+        CU(sk::launch_lambda_fwd(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
         if (p->timing) CU(cudaEventRecord(p->ev[1], p->stream));
         p->last_launches += 1;
     }
@@ -577,8 +607,11 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.f = nullptr;
         lp.spec = spec;
         lp.u = u_dev;
+        CUtensorMap map;
+        sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
+        if (ms != SK_OK) return ms;
         if (p->timing) CU(cudaEventRecord(p->ev[4], p->stream));
-        CU(sk::launch_lambda_inv(lp, p->thr_lambda, p->smem_lambda, p->stream));
+        CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
         if (p->timing) CU(cudaEventRecord(p->ev[5], p->stream));
         p->last_launches += 1;
     }
@@ -683,7 +716,9 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     lp.out_rhs_stride = 0;
     lp.spec = p->spec;
     lp.u = phys_dev;
-    CU(sk::launch_lambda_inv(lp, p->thr_lambda, p->smem_lambda, p->stream));
+    CUtensorMap map;
+    if ((s = make_spec_map(&map, p->spec, p->g.rows, p->g.cols, 1)) != SK_OK) return s;
+    CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
     CU(cudaStreamSynchronize(p->stream));
     return SK_OK;
 }

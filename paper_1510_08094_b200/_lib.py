@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsk_poisson.so")
+LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(HERE, "libsk_poisson.so")  # override: A/B builds
 
 SK_OK = 0
 SK_ERR_SIZE = 1

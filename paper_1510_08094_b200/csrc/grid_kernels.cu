@@ -781,7 +781,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const bool want_wsum = (kg == 0 && par == 0);
     const bool seq = kg < P.kseq;
     if (seq) solve_chain_seq(a, rev, ipp, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    else if (cp.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    else if (P.regsolve && cp.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
     else solve_chain(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
     SK_PROBE(4);
     // the t < 0 chain's pivots replace the t > 0 chain's in the window
@@ -798,7 +798,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     }
     SK_PROBE(5);
     if (seq) solve_chain_seq(a, rev, ipm, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
-    else if (cm.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    else if (P.regsolve && cm.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
     else solve_chain(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
     SK_PROBE(6);
     if (want_wsum) wsum = block_sum2(wsum, red);

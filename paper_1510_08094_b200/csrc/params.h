@@ -36,6 +36,7 @@ struct ThetaParams {
     double2* xhalf;   // optional: solution coefficients X[k][i], (N/2+1) x M per rhs
     int kseq;         // lambda modes k < kseq use the sequential Thomas recurrence
     const double* pivots;  // pivot table for modes k0..k0+ncols-1 (pivot_table_kernel)
+    int regsolve;          // register-resident chain segments (1) or shared-memory walks (0)
 };
 
 struct ShgenParams {

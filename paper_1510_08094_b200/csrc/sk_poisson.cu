@@ -274,6 +274,7 @@ struct sk_plan_s {
     double2* coef_stage = nullptr;  // shgen coefficients
     double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
+    int regsolve = 1;          // register-resident chain solve (SK_REGSOLVE)
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -354,6 +355,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     }
     p->own_stream = true;
     if (const char* e = std::getenv("SK_KSEQ")) p->kseq = std::atoi(e);
+    if (const char* e = std::getenv("SK_REGSOLVE")) p->regsolve = std::atoi(e);
     p->g.M = M;
     p->g.N = N;
     p->g.Lt = M / 2;
@@ -595,6 +597,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.stats = p->stats;
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
+        tp.regsolve = p->regsolve;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;  // rows for this rank's modes
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));

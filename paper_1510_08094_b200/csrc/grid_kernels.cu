@@ -61,9 +61,7 @@ constexpr int kLamPairs = 12;  // mode pairs per thread held in registers
 
 // One CTA per physical row: TMA bulk load of the real row (N/2 complex
 // pairs), forward DIF FFT, split into the N/2+1 modes of the real transform
-// with analyze_1d's (-1)^k / N (fourier.cpp:44-51), staged in natural order
-// in shared memory and written to the mode-major spectrum by TMA tensor
-// stores (the row -> column transpose is done by the copy engine).
+// with analyze_1d's (-1)^k / N (fourier.cpp:44-51), stored mode-major.
 __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
@@ -90,37 +88,19 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
     mbar_wait(bar, 0);
     fft_forward(a, P.fd, T, tid, nthr);
     const double invN = 1.0 / P.g.N;
-    // split Z (digit-reversed) into X_k, k = 0..L, through registers (the
-    // natural-order results overwrite the same buffer)
-    double2 xk[kLamPairs], xm[kLamPairs];
-#pragma unroll
-    for (int u = 0; u < kLamPairs; ++u) {
-        const int k = tid + u * nthr;
-        if (k <= L / 2) {
-            const int km = L - k;  // partner mode
-            const double2 z = a[s_rev[k]];
-            const double2 zp = a[s_rev[km == L ? 0 : km]];
-            // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
-            const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
-            const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-            xk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
-            xm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kLamPairs; ++u) {
-        const int k = tid + u * nthr;
-        if (k <= L / 2) {
-            a[k] = xk[u];
-            a[L - k] = xm[u];
-        }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-        for (int k0 = 0; k0 <= L; k0 += kBoxModes) tma_store_3d(&tmap, 2 * row, k0, rhs, a + k0);
-        tma_store_commit_and_wait();
+    double2* out = P.spec + rhs * P.out_rhs_stride;
+    (void)tmap;  // scattered fire-and-forget stores measured faster than staged TMA tensor stores here
+    for (int k = tid; k <= L / 2; k += nthr) {
+        const int km = L - k;  // partner mode
+        const double2 z = a[s_rev[k]];
+        const double2 zp = a[s_rev[km == L ? 0 : km]];
+        // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
+        const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
+        const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
+        const double2 Xk = cadd(A, cmul(T(k), B));
+        const double2 Xm = cadd(conjd(A), cmul(T(km), conjd(B)));
+        out[static_cast<size_t>(k) * P.rows_local + row] = cscale(Xk, (k & 1) ? -invN : invN);
+        if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = cscale(Xm, (km & 1) ? -invN : invN);
     }
 }
 

@@ -57,12 +57,28 @@ void search_radices(int m, int nthr, int L, int maxr, std::vector<int>& cur, dou
     }
 }
 
-bool factor_radices(int L, int nthr, std::vector<int>& R) {
+bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = false) {
     R.clear();
     if (L < 1) return false;
     if (L == 1) return true;
     std::vector<int> cur;
     double best = 1e300;
+    if (odd_first_span) {
+        // First radix takes every factor of two, so consecutive natural indices
+        // sit an odd number of slots apart in the digit-reversed layout and a
+        // warp walking consecutive chain elements spreads over all banks.
+        int p2 = 1;
+        while (L % (2 * p2) == 0) p2 *= 2;
+        if (p2 > 1 && p2 <= 16 && L / p2 > 1) {
+            const long long nb = L / p2;
+            cur.push_back(p2);
+            search_radices(L / p2, nthr, L, 25, cur, static_cast<double>((nb + nthr - 1) / nthr) * (p2 + 6) + 30,
+                           best, R);
+            if (!R.empty()) return true;
+            cur.clear();
+            best = 1e300;
+        }
+    }
     search_radices(L, nthr, L, 25, cur, 0.0, best, R);
     return !R.empty();
 }
@@ -84,9 +100,9 @@ void root(long long m, long long n, double& c, double& s) {
     s = static_cast<double>(-sinl(a));
 }
 
-sk_status build_fft(int L, int nthr, DevFft& out) {
+sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false) {
     std::vector<int> R;
-    if (!factor_radices(L, nthr, R)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
+    if (!factor_radices(L, nthr, R, odd_first_span)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
     sk::FftDesc& d = out.d;
     d.L = L;
     d.nst = static_cast<int>(R.size());
@@ -387,7 +403,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     }
     p->thr_theta = round_threads((M / 2) / 8, 64, 512);
     p->thr_lambda = round_threads((N / 2) / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft)) != SK_OK) {
+    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft, true)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }

@@ -222,6 +222,15 @@ __device__ __forceinline__ int fdiv(int n, unsigned mag, int sh1, int sh2) {
     return static_cast<int>((t + ((static_cast<unsigned>(n) - t) >> sh1)) >> sh2);
 }
 
+// Shared-memory slot swizzle: XOR the low three bits of a complex slot index
+// with a hash of its higher bits (a bijection on every aligned 8-slot block),
+// so indices that differ by multiples of 8 slots hit different banks.
+template <bool SWZ>
+__device__ __forceinline__ int swz(int p) {
+    if constexpr (SWZ) return p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9) ^ (p >> 12)) & 7);
+    else return p;
+}
+
 // One butterfly's registers.
 template <int R>
 struct Bfly {
@@ -229,13 +238,13 @@ struct Bfly {
     int base, j;
 };
 
-template <int R>
+template <int R, bool SWZ>
 __device__ __forceinline__ void bf_load(Bfly<R>& B, const double2* a, int b, int span, unsigned mag, int sh1, int sh2) {
     const int g = fdiv(b, mag, sh1, sh2);
     B.j = b - g * span;
     B.base = g * span * R + B.j;
 #pragma unroll
-    for (int q = 0; q < R; ++q) B.x[q] = a[B.base + q * span];
+    for (int q = 0; q < R; ++q) B.x[q] = a[swz<SWZ>(B.base + q * span)];
 }
 
 // Twiddle powers w^q, q = 1..R-1, w = T(j tw) for SIGN = -1 (exp(-2 pi i ...))
@@ -254,26 +263,26 @@ __device__ __forceinline__ void bf_twiddle(double2* x, int j, int tw, const Tw& 
 }
 
 // DIF butterfly: y = DFT_R(x); y_q *= w^(q j); store in place.
-template <int R, int SIGN>
+template <int R, int SIGN, bool SWZ>
 __device__ __forceinline__ void bf_dif(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
     dft<R, SIGN>(B.x);
     bf_twiddle<R, SIGN>(B.x, B.j, tw, T);
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
+    for (int q = 0; q < R; ++q) a[swz<SWZ>(B.base + q * span)] = B.x[q];
 }
 
 // DIT butterfly: x_q *= w^(q j); y = DFT_R(x); store in place.
-template <int R, int SIGN>
+template <int R, int SIGN, bool SWZ>
 __device__ __forceinline__ void bf_dit(Bfly<R>& B, double2* a, int span, int tw, const Tw& T) {
     bf_twiddle<R, SIGN>(B.x, B.j, tw, T);
     dft<R, SIGN>(B.x);
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[B.base + q * span] = B.x[q];
+    for (int q = 0; q < R; ++q) a[swz<SWZ>(B.base + q * span)] = B.x[q];
 }
 
 // One stage over all butterflies; small radices keep two butterflies'
 // shared-memory loads in flight.
-template <int R, bool DIF, int SIGN>
+template <int R, bool DIF, int SIGN, bool SWZ>
 __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
     const int span = d.span[s], tw = d.tw[s];
     const unsigned mag = d.mag[s];
@@ -283,39 +292,39 @@ __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, c
     if constexpr (R <= 8) {
         for (; b + nthr < nb; b += 2 * nthr) {
             Bfly<R> p, q;
-            bf_load(p, a, b, span, mag, sh1, sh2);
-            bf_load(q, a, b + nthr, span, mag, sh1, sh2);
+            bf_load<R, SWZ>(p, a, b, span, mag, sh1, sh2);
+            bf_load<R, SWZ>(q, a, b + nthr, span, mag, sh1, sh2);
             if constexpr (DIF) {
-                bf_dif<R, SIGN>(p, a, span, tw, T);
-                bf_dif<R, SIGN>(q, a, span, tw, T);
+                bf_dif<R, SIGN, SWZ>(p, a, span, tw, T);
+                bf_dif<R, SIGN, SWZ>(q, a, span, tw, T);
             } else {
-                bf_dit<R, SIGN>(p, a, span, tw, T);
-                bf_dit<R, SIGN>(q, a, span, tw, T);
+                bf_dit<R, SIGN, SWZ>(p, a, span, tw, T);
+                bf_dit<R, SIGN, SWZ>(q, a, span, tw, T);
             }
         }
     }
     for (; b < nb; b += nthr) {
         Bfly<R> p;
-        bf_load(p, a, b, span, mag, sh1, sh2);
-        if constexpr (DIF) bf_dif<R, SIGN>(p, a, span, tw, T);
-        else bf_dit<R, SIGN>(p, a, span, tw, T);
+        bf_load<R, SWZ>(p, a, b, span, mag, sh1, sh2);
+        if constexpr (DIF) bf_dif<R, SIGN, SWZ>(p, a, span, tw, T);
+        else bf_dit<R, SIGN, SWZ>(p, a, span, tw, T);
     }
 }
 
-template <bool DIF, int SIGN>
+template <bool DIF, int SIGN, bool SWZ>
 __device__ __forceinline__ void fft_stage_dispatch(double2* a, const FftDesc& d, int s, const Tw& T, int tid,
                                                    int nthr) {
     switch (d.R[s]) {
-        case 2: fft_stage<2, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 3: fft_stage<3, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 4: fft_stage<4, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 5: fft_stage<5, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 7: fft_stage<7, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 8: fft_stage<8, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 10: fft_stage<10, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 16: fft_stage<16, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        case 20: fft_stage<20, DIF, SIGN>(a, d, s, T, tid, nthr); break;
-        default: fft_stage<25, DIF, SIGN>(a, d, s, T, tid, nthr); break;
+        case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 8: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 10: fft_stage<10, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 16: fft_stage<16, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        case 20: fft_stage<20, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        default: fft_stage<25, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
     }
 }
 
@@ -326,31 +335,27 @@ __device__ __forceinline__ void fft_stage_dispatch(double2* a, const FftDesc& d,
 //   fft_inverse      DIT, exp(+):  reversed -> natural   (lambda inverse)
 //   fft_forward_dit  DIT, exp(-):  reversed -> natural   (theta forward)
 //   fft_inverse_dif  DIF, exp(+):  natural -> reversed   (theta inverse)
-template <bool DIF, int SIGN>
+template <bool DIF, int SIGN, bool SWZ>
 __device__ __forceinline__ void fft_run(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     if constexpr (DIF) {
         for (int s = 0; s < d.nst; ++s) {
-            fft_stage_dispatch<true, SIGN>(a, d, s, T, tid, nthr);
+            fft_stage_dispatch<true, SIGN, SWZ>(a, d, s, T, tid, nthr);
             __syncthreads();
         }
     } else {
         for (int s = d.nst - 1; s >= 0; --s) {
-            fft_stage_dispatch<false, SIGN>(a, d, s, T, tid, nthr);
+            fft_stage_dispatch<false, SIGN, SWZ>(a, d, s, T, tid, nthr);
             __syncthreads();
         }
     }
 }
+template <bool SWZ = false>
 __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<true, -1>(a, d, T, tid, nthr);
+    fft_run<true, -1, SWZ>(a, d, T, tid, nthr);
 }
+template <bool SWZ = false>
 __device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<false, +1>(a, d, T, tid, nthr);
-}
-__device__ __forceinline__ void fft_forward_dit(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<false, -1>(a, d, T, tid, nthr);
-}
-__device__ __forceinline__ void fft_inverse_dif(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<true, +1>(a, d, T, tid, nthr);
+    fft_run<false, +1, SWZ>(a, d, T, tid, nthr);
 }
 
 // Stage the 2L-th-root twiddle tables of `d` into shared memory.

@@ -187,6 +187,7 @@ __device__ __forceinline__ int t_of(int tau, int par, int L) {
 // -4+par, ... (tau descending from L-1).  Element i of a chain is coupled to
 // i-1 (towards j = 0) and i+1 (towards the truncation boundary).
 constexpr int kSegMax = 12;  // register-resident chain segment length per thread
+constexpr int kFoldMax = 12;  // column pairs per thread in the fold
 
 struct Chain {
     int n;       // length
@@ -638,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     cg::cluster_group cluster = cg::this_cluster();
     const int L = P.fd.L;  // M/2
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + L + 1;  // a holds the raw column (L+1 values) before the fold
+    double2* s_hi = a + theta_data_slots(L);  // raw column (L+1 values), then the swizzled transform
     double2* s_lo = s_hi + P.fd.nhi;
     double* ip = reinterpret_cast<double*>(s_lo + P.fd.nlo);
     V4* wsc = reinterpret_cast<V4*>(ip + theta_chain_slots(L));
@@ -693,26 +694,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(1);
-    // ---- DFS fold (first radix-2 step) in place, scaled by 1/M
+    // ---- DFS fold (first radix-2 step), scaled by 1/M, into the swizzled
+    // slot layout of the transform (through registers: kFoldMax pairs per
+    // thread, so no slot is overwritten before it is read)
     const double invM = 1.0 / P.g.M;
-    for (int r = tid; r <= L / 2; r += nthr) {
-        const int rm = L - r;
-        const double2 ar = a[r];
-        const double2 am = a[rm];
-        if (par == 0) {
-            // e_r = a_r + s a_{L-r}
-            a[r] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
-            if (rm < L && rm != r) a[rm] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
-        } else {
-            // o_r = (a_r - s a_{L-r}) w_M^{-r}
-            a[r] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
-            if (rm < L && rm != r)
-                a[rm] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
+    {
+        double2 v0[kFoldMax], v1[kFoldMax];
+#pragma unroll
+        for (int u = 0; u < kFoldMax; ++u) {
+            const int r = tid + u * nthr;
+            if (r <= L / 2) {
+                const int rm = L - r;
+                const double2 ar = a[r];
+                const double2 am = a[rm];
+                if (par == 0) {
+                    // e_r = a_r + s a_{L-r}
+                    v0[u] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
+                    v1[u] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
+                } else {
+                    // o_r = (a_r - s a_{L-r}) w_M^{-r}
+                    v0[u] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
+                    v1[u] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kFoldMax; ++u) {
+            const int r = tid + u * nthr;
+            if (r <= L / 2) {
+                const int rm = L - r;
+                a[swz<true>(r)] = v0[u];
+                if (rm < L && rm != r) a[swz<true>(rm)] = v1[u];
+            }
         }
     }
     __syncthreads();
     SK_PROBE(2);
-    fft_forward(a, P.fd, T, tid, nthr);
+    fft_forward<true>(a, P.fd, T, tid, nthr);
     SK_PROBE(3);
 
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
@@ -810,7 +829,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(7);
-    fft_inverse(a, P.fd, T, tid, nthr);
+    fft_inverse<true>(a, P.fd, T, tid, nthr);
     SK_PROBE(8);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
@@ -821,7 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const int p_lo = par == 0 ? 0 : half;
     const int p_hi = par == 0 ? half : L + 1;
     for (int p = p_lo + tid; p < p_hi; p += nthr) {
-        const int pm = p == L ? 0 : p;
+        const int pm = swz<true>(p == L ? 0 : p);
         const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
         colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }

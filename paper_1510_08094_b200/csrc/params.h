@@ -63,6 +63,10 @@ struct ResidualParams {
     double* out;  // [0] interior max, [1] replaced-row abs, [2..3] constraint sum (re, im)
 };
 
+// Complex slots of the theta kernel's data buffer: the raw column (L+1)
+// and whole 8-slot blocks for the swizzled layout.
+__host__ __device__ inline int theta_data_slots(int L) { return ((L + 1) + 7) & ~7; }
+
 // Pivot-reciprocal slots of the theta kernel (even, so later regions stay
 // 16-byte aligned).
 __host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 4) + 1) & ~1; }
@@ -70,7 +74,7 @@ __host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 4) + 
 // Dynamic shared memory of theta_kernel (bytes).
 __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
     const size_t chain_max = static_cast<size_t>(theta_chain_slots(L));
-    return static_cast<size_t>(L + 1) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
+    return static_cast<size_t>(theta_data_slots(L)) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
            16 * 16 + 64 * 8 + 2 * 8;
 }
 

@@ -100,7 +100,7 @@ void root(long long m, long long n, double& c, double& s) {
     s = static_cast<double>(-sinl(a));
 }
 
-sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false) {
+sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, bool swizzle = false) {
     std::vector<int> R;
     if (!factor_radices(L, nthr, R, odd_first_span)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
     sk::FftDesc& d = out.d;
@@ -137,7 +137,8 @@ sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false) {
             pos += (kk % d.R[s]) * d.span[s];
             kk /= d.R[s];
         }
-        rev[k] = pos;
+        // theta plans store the swizzled shared-memory slot (fft_dev.cuh swz)
+        rev[k] = swizzle ? (pos ^ (((pos >> 3) ^ (pos >> 6) ^ (pos >> 9) ^ (pos >> 12)) & 7)) : pos;
     }
     CU(cudaMalloc(&out.hi, sizeof(double2) * d.nhi));
     CU(cudaMalloc(&out.lo, sizeof(double2) * d.nlo));
@@ -403,7 +404,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     }
     p->thr_theta = round_threads((M / 2) / 8, 64, 512);
     p->thr_lambda = round_threads((N / 2) / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft, true)) != SK_OK) {
+    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft, true, true)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
@@ -416,7 +417,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
         p->smem_lambda = sk::lambda_smem_bytes(Ll, p->fl.d.nhi, p->fl.d.nlo);
         const size_t cap = 227 * 1024;
-        const bool pairs_fit = (Ll / 2 + 1) <= 12 * p->thr_lambda;  // kLamPairs pairs per thread
+        const bool pairs_fit = (Ll / 2 + 1) <= 12 * p->thr_lambda && (Lt / 2 + 1) <= 12 * p->thr_theta;  // register staging
         if (p->smem_theta > cap || p->smem_lambda > cap || !pairs_fit) {
             p->grid_ok = false;
             p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +

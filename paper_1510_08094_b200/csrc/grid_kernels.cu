@@ -634,6 +634,7 @@ __device__ __forceinline__ const double* pivot_window(double* dst, const double*
 // offsets of lap are exact zeros, so even and odd modes never couple), and the
 // inverse transform.  The two halves are recombined through distributed
 // shared memory.
+template <bool SWZ>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(ThetaParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -694,11 +695,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(1);
-    // ---- DFS fold (first radix-2 step), scaled by 1/M, into the swizzled
-    // slot layout of the transform (through registers: kFoldMax pairs per
-    // thread, so no slot is overwritten before it is read)
+    // ---- DFS fold (first radix-2 step), scaled by 1/M.  With the swizzled
+    // slot layout the fold goes through registers (kFoldMax pairs per thread,
+    // so no slot is overwritten before it is read); otherwise in place.
     const double invM = 1.0 / P.g.M;
-    {
+    if constexpr (SWZ) {
         double2 v0[kFoldMax], v1[kFoldMax];
 #pragma unroll
         for (int u = 0; u < kFoldMax; ++u) {
@@ -708,11 +709,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
                 const double2 ar = a[r];
                 const double2 am = a[rm];
                 if (par == 0) {
-                    // e_r = a_r + s a_{L-r}
                     v0[u] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
                     v1[u] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
                 } else {
-                    // o_r = (a_r - s a_{L-r}) w_M^{-r}
                     v0[u] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
                     v1[u] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
                 }
@@ -728,10 +727,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
                 if (rm < L && rm != r) a[swz<true>(rm)] = v1[u];
             }
         }
+    } else {
+        for (int r = tid; r <= L / 2; r += nthr) {
+            const int rm = L - r;
+            const double2 ar = a[r];
+            const double2 am = a[rm];
+            if (par == 0) {
+                // e_r = a_r + s a_{L-r}
+                a[r] = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
+                if (rm < L && rm != r) a[rm] = make_double2((am.x + sgn * ar.x) * invM, (am.y + sgn * ar.y) * invM);
+            } else {
+                // o_r = (a_r - s a_{L-r}) w_M^{-r}
+                a[r] = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), T(r)), invM);
+                if (rm < L && rm != r)
+                    a[rm] = cscale(cmul(make_double2(am.x - sgn * ar.x, am.y - sgn * ar.y), T(rm)), invM);
+            }
+        }
     }
     __syncthreads();
     SK_PROBE(2);
-    fft_forward<true>(a, P.fd, T, tid, nthr);
+    fft_forward<SWZ>(a, P.fd, T, tid, nthr);
     SK_PROBE(3);
 
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
@@ -829,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(7);
-    fft_inverse<true>(a, P.fd, T, tid, nthr);
+    fft_inverse<SWZ>(a, P.fd, T, tid, nthr);
     SK_PROBE(8);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
@@ -840,7 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const int p_lo = par == 0 ? 0 : half;
     const int p_hi = par == 0 ? half : L + 1;
     for (int p = p_lo + tid; p < p_hi; p += nthr) {
-        const int pm = swz<true>(p == L ? 0 : p);
+        const int pm = swz<SWZ>(p == L ? 0 : p);
         const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
         colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }
@@ -939,11 +954,14 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (auto fn : {theta_kernel<false>, theta_kernel<true>}) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
         attr = true;
     }
-    theta_kernel<<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    if (P.swizzle) theta_kernel<true><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    else theta_kernel<false><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
     return cudaGetLastError();
 }
 

@@ -37,6 +37,7 @@ struct ThetaParams {
     int kseq;         // lambda modes k < kseq use the sequential Thomas recurrence
     const double* pivots;  // pivot table for modes k0..k0+ncols-1 (pivot_table_kernel)
     int regsolve;          // register-resident chain segments (1) or shared-memory walks (0)
+    int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
 };
 
 struct ShgenParams {

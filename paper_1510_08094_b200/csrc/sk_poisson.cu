@@ -138,7 +138,7 @@ sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, b
             kk /= d.R[s];
         }
         // theta plans store the swizzled shared-memory slot (fft_dev.cuh swz)
-        rev[k] = swizzle ? (pos ^ (((pos >> 3) ^ (pos >> 6) ^ (pos >> 9) ^ (pos >> 12)) & 7)) : pos;
+        rev[k] = (swizzle && d.nst > 0 && d.span[0] % 2 == 0) ? (pos ^ (((pos >> 3) ^ (pos >> 6) ^ (pos >> 9) ^ (pos >> 12)) & 7)) : pos;
     }
     CU(cudaMalloc(&out.hi, sizeof(double2) * d.nhi));
     CU(cudaMalloc(&out.lo, sizeof(double2) * d.nlo));
@@ -615,6 +615,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
         tp.regsolve = p->regsolve;
+        tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;  // rows for this rank's modes
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));

@@ -21,10 +21,11 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 # contraction anywhere in that translation unit.
 UNITS = [
     ("grid_kernels.cu", []),
+    ("grid_large.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("sk_poisson.cu", []),
 ]
-HEADERS = ["sk_internal.h", "params.h", "fft_dev.cuh", "block_ops.cuh", "tma.cuh"]
+HEADERS = ["sk_internal.h", "params.h", "fft_dev.cuh", "block_ops.cuh", "tma.cuh", "theta_common.cuh"]
 
 
 def nvcc() -> str:

@@ -64,6 +64,28 @@ struct ResidualParams {
     double* out;  // [0] interior max, [1] replaced-row abs, [2..3] constraint sum (re, im)
 };
 
+// Large transforms (grid_large.cu): the theta stage split over a cluster of
+// 2Q CTAs (fq: the local length-L/Q transform), the lambda stages over a CTA
+// pair (fh: the length-N/4 transform of one parity class).
+struct ThetaLargeParams {
+    ThetaParams t;
+    FftDesc fq;
+};
+struct LambdaSplitParams {
+    LambdaParams l;
+    FftDesc fh;
+};
+inline size_t theta_large_smem_bytes(int Lq, int nhiM, int nloM, int nhiq, int nloq) {
+    return static_cast<size_t>((Lq + 7) & ~7) * 16 + static_cast<size_t>(nhiM + nloM + nhiq + nloq) * 16 +
+           static_cast<size_t>((Lq + 4 + 1) & ~1) * 8 + 32 * 32 + 2 * 32 + 16 * 16 + 64 * 8 + 16;
+}
+inline size_t lambda_split_smem_bytes(int Lh, int nhiN, int nloN, int nhih, int nloh) {
+    return static_cast<size_t>(Lh) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16;
+}
+cudaError_t launch_theta_large(const ThetaLargeParams& P, int Q, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
+
 // Complex slots of the theta kernel's data buffer: the raw column (L+1)
 // and whole 8-slot blocks for the swizzled layout.
 __host__ __device__ inline int theta_data_slots(int L) { return ((L + 1) + 7) & ~7; }

@@ -277,6 +277,9 @@ struct sk_plan_s {
     std::string grid_why;
     sk::GridGeom g;
     DevFft ft, fl;
+    DevFft ftq, flh;           // local transforms of the cluster-split kernels
+    int theta_q = 0;           // 0: CTA-pair theta kernel; Q: 2Q-CTA cluster kernel
+    int lambda_split = 0;      // lambda rows split over a CTA pair
     int thr_theta = 0, thr_lambda = 0;
     size_t smem_theta = 0, smem_lambda = 0;
     double2* spec = nullptr;   // nrhs * cols * rows complex
@@ -402,26 +405,59 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         p->grid_ok = false;
         p->grid_why = "grid path needs M >= 8 and N >= 4";
     }
-    p->thr_theta = round_threads((M / 2) / 8, 64, 512);
-    p->thr_lambda = round_threads((N / 2) / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(M / 2, p->thr_theta, p->ft, true, true)) != SK_OK) {
-        p->grid_ok = false;
-        p->grid_why = g_err;
-    }
-    if (p->grid_ok && (s = build_fft(N / 2, p->thr_lambda, p->fl)) != SK_OK) {
+    const size_t cap = 227 * 1024;
+    const int Lt = M / 2, Ll = N / 2;
+    // theta stage: one CTA pair per mode when a parity half fits shared
+    // memory, else a cluster of 2Q CTAs (Q = 4) holding quarters
+    p->thr_theta = round_threads(Lt / 8, 64, 512);
+    if (p->grid_ok && (s = build_fft(Lt, p->thr_theta, p->ft, true, true)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
     if (p->grid_ok) {
-        const int Lt = M / 2, Ll = N / 2;
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
+        const bool fits = p->smem_theta <= cap && (Lt / 2 + 1) <= 12 * p->thr_theta;
+        if (!fits) {
+            const int Q = 4;
+            const int Lq = Lt / Q;
+            p->theta_q = Q;
+            p->thr_theta = 512;
+            if (Lt % (2 * Q) != 0 || (s = build_fft(Lq, 512, p->ftq)) != SK_OK) {
+                p->grid_ok = false;
+                p->grid_why = "theta length " + std::to_string(Lt) + " cannot be split over a " +
+                              std::to_string(2 * Q) + "-CTA cluster";
+            } else {
+                p->smem_theta = sk::theta_large_smem_bytes(Lq, p->ft.d.nhi, p->ft.d.nlo, p->ftq.d.nhi, p->ftq.d.nlo);
+                if (p->smem_theta > cap || Lq > 16 * 512) {
+                    p->grid_ok = false;
+                    p->grid_why = "theta length " + std::to_string(Lt) + " exceeds the cluster shared-memory limit";
+                }
+            }
+        }
+    }
+    // lambda stages: one CTA per row, or a CTA pair splitting the row by parity
+    p->thr_lambda = round_threads(Ll / 8, 64, 256);
+    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl)) != SK_OK) {
+        p->grid_ok = false;
+        p->grid_why = g_err;
+    }
+    if (p->grid_ok) {
         p->smem_lambda = sk::lambda_smem_bytes(Ll, p->fl.d.nhi, p->fl.d.nlo);
-        const size_t cap = 227 * 1024;
-        const bool pairs_fit = (Ll / 2 + 1) <= 12 * p->thr_lambda && (Lt / 2 + 1) <= 12 * p->thr_theta;  // register staging
-        if (p->smem_theta > cap || p->smem_lambda > cap || !pairs_fit) {
-            p->grid_ok = false;
-            p->grid_why = "theta/lambda transform of length " + std::to_string(std::max(Lt, Ll)) +
-                          " exceeds the on-chip (shared memory) limit of this build";
+        const bool fits = p->smem_lambda <= cap && (Ll / 2 + 1) <= 12 * p->thr_lambda;
+        if (!fits) {
+            p->lambda_split = 1;
+            p->thr_lambda = 512;
+            if (Ll % 4 != 0 || (s = build_fft(Ll / 2, 512, p->flh)) != SK_OK) {
+                p->grid_ok = false;
+                p->grid_why = "lambda length " + std::to_string(Ll) + " cannot be split over a CTA pair";
+            } else {
+                p->smem_lambda = sk::lambda_split_smem_bytes(Ll / 2, p->fl.d.nhi, p->fl.d.nlo, p->flh.d.nhi,
+                                                             p->flh.d.nlo);
+                if (p->smem_lambda > cap) {
+                    p->grid_ok = false;
+                    p->grid_why = "lambda length " + std::to_string(Ll) + " exceeds the CTA-pair shared-memory limit";
+                }
+            }
         }
     }
     if (p->grid_ok) {
@@ -451,6 +487,8 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     cudaSetDevice(p->device);
     free_fft(p->ft);
     free_fft(p->fl);
+    free_fft(p->ftq);
+    free_fft(p->flh);
     for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
                     static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
                     static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
@@ -505,7 +543,7 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     info[3] = p->device;
     info[4] = p->grid_ok ? 1 : 0;
     info[5] = p->g.rows;
-    info[6] = 2;
+    info[6] = p->theta_q ? 2 * p->theta_q : 2;
     info[7] = p->thr_theta;
     info[8] = p->thr_lambda;
     info[9] = p->last_launches;
@@ -593,11 +631,16 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.out_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
         lp.f = f_dev;
         lp.spec = spec;
-        CUtensorMap map;
-        sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
-        if (ms != SK_OK) return ms;
         if (p->timing) CU(cudaEventRecord(p->ev[0], p->stream));
-        CU(sk::launch_lambda_fwd(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+        if (p->lambda_split) {
+            sk::LambdaSplitParams sp{lp, p->flh.d};
+            CU(sk::launch_lambda_fwd_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+        } else {
+            CUtensorMap map;
+            sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
+            if (ms != SK_OK) return ms;
+            CU(sk::launch_lambda_fwd(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+        }
         if (p->timing) CU(cudaEventRecord(p->ev[1], p->stream));
         p->last_launches += 1;
     }
@@ -618,7 +661,12 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;  // rows for this rank's modes
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
-        CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
+        if (p->theta_q) {
+            sk::ThetaLargeParams tl{tp, p->ftq.d};
+            CU(sk::launch_theta_large(tl, p->theta_q, p->thr_theta, p->smem_theta, p->stream));
+        } else {
+            CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
+        }
         if (p->timing) CU(cudaEventRecord(p->ev[3], p->stream));
         p->last_launches += 1;
     }
@@ -628,11 +676,16 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.f = nullptr;
         lp.spec = spec;
         lp.u = u_dev;
-        CUtensorMap map;
-        sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
-        if (ms != SK_OK) return ms;
         if (p->timing) CU(cudaEventRecord(p->ev[4], p->stream));
-        CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+        if (p->lambda_split) {
+            sk::LambdaSplitParams sp{lp, p->flh.d};
+            CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+        } else {
+            CUtensorMap map;
+            sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
+            if (ms != SK_OK) return ms;
+            CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+        }
         if (p->timing) CU(cudaEventRecord(p->ev[5], p->stream));
         p->last_launches += 1;
     }
@@ -737,9 +790,14 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     lp.out_rhs_stride = 0;
     lp.spec = p->spec;
     lp.u = phys_dev;
-    CUtensorMap map;
-    if ((s = make_spec_map(&map, p->spec, p->g.rows, p->g.cols, 1)) != SK_OK) return s;
-    CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+    if (p->lambda_split) {
+        sk::LambdaSplitParams sp{lp, p->flh.d};
+        CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+    } else {
+        CUtensorMap map;
+        if ((s = make_spec_map(&map, p->spec, p->g.rows, p->g.cols, 1)) != SK_OK) return s;
+        CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+    }
     CU(cudaStreamSynchronize(p->stream));
     return SK_OK;
 }

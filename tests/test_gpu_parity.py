@@ -221,3 +221,47 @@ def test_grid_full_size_analytic_C2(pkg):
         torch.cuda.synchronize()
         err = (u - ue).abs().max().item() / ue.abs().max().item()
     assert err <= 1e-10, err
+
+
+# ------------------------------------------------- cluster-split kernels
+@pytest.mark.parametrize("m,n,L", [(32768, 48, 20), (64, 32768, 20), (32768, 32768 // 64, 24)])
+def test_grid_split_kernels_vs_oracle(pkg, oracle, m, n, L):
+    """theta length M/2 = 16384 runs the 8-CTA cluster kernel, lambda length
+    N/2 = 16384 the CTA-pair kernels; both against the oracle composition."""
+    from paper_1510_08094_b200 import inputs
+    c = inputs.sh_coeffs(m // 7 + n, L, 2.0)
+    f = oracle.shgen(m, n, L, c)
+    _, _, u_ref, _ = oracle.grid_pipeline(f, m, threads=8)
+    with pkg.Plan(m, n) as plan:
+        info = plan.info()
+        u = plan.solve_grid(f)
+    assert info["theta_split"] in (2, 8)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+def test_slab_stages_cluster_kernels_bitwise(pkg, oracle):
+    from paper_1510_08094_b200 import distributed as dist_mod, inputs
+    m, n, L = 32768, 40, 12
+    f = oracle.shgen(m, n, L, inputs.sh_coeffs(3, L, 2.0))
+    with pkg.Plan(m, n) as plan:
+        u1 = plan.solve_grid(f)
+    assert np.array_equal(dist_mod.emulate_slabs(f, m, n, 3), u1)
+
+
+def test_grid_full_size_analytic_C5(pkg):
+    """Config C5 (65536 x 32768, 1.07e9 DOF, L = 8192) against the analytic
+    solution: the size-independent check at the largest configuration."""
+    import torch
+    from paper_1510_08094_b200 import inputs
+    cfg = inputs.CONFIGS["C5"]
+    rows = cfg.M // 2 + 1
+    with pkg.Plan(cfg.M, cfg.N) as plan:
+        f = torch.empty((rows, cfg.N), dtype=torch.float64, device="cuda")
+        plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(5, cfg.L, cfg.p)).cuda(), f)
+        u = plan.solve_grid(f)
+        del f
+        ue = torch.empty_like(u)
+        plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(5, cfg.L, cfg.p, solution=True)).cuda(), ue)
+        torch.cuda.synchronize()
+        err = ((u - ue).abs().max() / ue.abs().max()).item()
+    assert err <= 1e-10, err

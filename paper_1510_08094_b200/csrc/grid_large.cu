@@ -204,8 +204,9 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
 
     // pivot window of this CTA's chain part (TMA, overlaps the transforms)
     const size_t prow = (static_cast<size_t>(kl) * 2 + par) * L;
-    const int tau_a = plus ? ch.tau0 + i_lo : ch.tau0 - (i_hi - 1);
-    const int tau_b = plus ? ch.tau0 + i_hi : ch.tau0 - i_lo + 1;
+    // (includes the pivot of element i_lo - 1, owned by the previous CTA)
+    const int tau_a = plus ? ch.tau0 + max(i_lo - 1, 0) : ch.tau0 - (i_hi - 1);
+    const int tau_b = plus ? ch.tau0 + i_hi : ch.tau0 - max(i_lo - 1, 0) + 1;
     uint32_t pbytes = 0;
     const double* ipv = pivot_window(ipw, P.pivots, prow, tau_a, tau_b, pbytes);
     if (tid == 0) {

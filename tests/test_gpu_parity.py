@@ -239,6 +239,22 @@ def test_grid_split_kernels_vs_oracle(pkg, oracle, m, n, L):
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n", [(32768, 24), (64, 32768)])
+def test_grid_split_kernels_rough_data(pkg, oracle, m, n):
+    """Random (non-band-limited) zero-mean data through the cluster kernels:
+    every spectral entry is O(1), so a wrong pivot, twiddle or cross-CTA
+    carry shows up at full size."""
+    rng = np.random.default_rng(m + n)
+    f = rng.standard_normal((m // 2 + 1, n))
+    A = oracle.analyze_2d(oracle.dfs_double(f, m))
+    mu = (oracle.integration_weights(m) * A[:, n // 2]).sum() / 2.0
+    f = f - mu.real
+    u_ref = oracle.grid_pipeline_real(f, m, threads=8)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
 def test_slab_stages_cluster_kernels_bitwise(pkg, oracle):
     from paper_1510_08094_b200 import distributed as dist_mod, inputs
     m, n, L = 32768, 40, 12

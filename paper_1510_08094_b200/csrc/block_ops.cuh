@@ -95,6 +95,107 @@ struct AffOp {
     __device__ static V4 combine(V4 e, V4 l) { return V4{l.a * e.a, fma(l.a, e.b, l.b), fma(l.a, e.c, l.c), 0.0}; }
 };
 
+// Affine maps x -> a x + (b + i c) with real a, three doubles (the scans of
+// the chain solve shuffle 3 instead of 4 doubles per step).
+struct Aff3 {
+    double a, b, c;
+};
+__device__ __forceinline__ Aff3 aff_identity() { return Aff3{1.0, 0.0, 0.0}; }
+// later o earlier
+__device__ __forceinline__ Aff3 aff_combine(Aff3 e, Aff3 l) {
+    return Aff3{l.a * e.a, fma(l.a, e.b, l.b), fma(l.a, e.c, l.c)};
+}
+template <bool UP>
+__device__ __forceinline__ Aff3 shfl_aff(Aff3 v, int delta) {
+    Aff3 r;
+    if constexpr (UP) {
+        r.a = __shfl_up_sync(0xffffffffu, v.a, delta);
+        r.b = __shfl_up_sync(0xffffffffu, v.b, delta);
+        r.c = __shfl_up_sync(0xffffffffu, v.c, delta);
+    } else {
+        r.a = __shfl_down_sync(0xffffffffu, v.a, delta);
+        r.b = __shfl_down_sync(0xffffffffu, v.b, delta);
+        r.c = __shfl_down_sync(0xffffffffu, v.c, delta);
+    }
+    return r;
+}
+
+// Exclusive scan of affine maps over the CTA in thread order (REV = false) or
+// reverse thread order (REV = true); `wsc` needs 32 slots.  Ends with a barrier.
+template <bool REV>
+__device__ __forceinline__ Aff3 block_scan_aff(Aff3 v, Aff3* wsc) {
+    const int tid = threadIdx.x;
+    const int nw = blockDim.x >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int vlane = REV ? 31 - lane : lane;
+    const int vwarp = REV ? nw - 1 - warp : warp;
+    Aff3 inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const Aff3 o = shfl_aff<!REV>(inc, off);
+        if (vlane >= off) inc = aff_combine(o, inc);
+    }
+    if (vlane == 31) wsc[vwarp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        Aff3 t = lane < nw ? wsc[lane] : aff_identity();
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const Aff3 o = shfl_aff<true>(t, off);
+            if (lane >= off) t = aff_combine(o, t);
+        }
+        const Aff3 prev = shfl_aff<true>(t, 1);
+        if (lane < nw) wsc[lane] = lane == 0 ? aff_identity() : prev;
+    }
+    __syncthreads();
+    const Aff3 wpre = wsc[vwarp];
+    Aff3 ex = shfl_aff<!REV>(inc, 1);
+    if (vlane == 0) ex = aff_identity();
+    const Aff3 res = aff_combine(wpre, ex);
+    __syncthreads();
+    return res;
+}
+
+// Segmented variant: the CTA's warps form 2 equal segments (warps
+// [0, nw/2) and [nw/2, nw)), each scanned independently in thread order
+// (REV = false) or reverse thread order (REV = true) within the segment.
+template <bool REV>
+__device__ __forceinline__ Aff3 block_scan_aff_seg2(Aff3 v, Aff3* wsc) {
+    const int tid = threadIdx.x;
+    const int nw = blockDim.x >> 5;
+    const int segw = nw >> 1;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int seg = warp / segw, wi = warp - seg * segw;
+    const int vlane = REV ? 31 - lane : lane;
+    const int slot = seg * segw + (REV ? segw - 1 - wi : wi);
+    Aff3 inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const Aff3 o = shfl_aff<!REV>(inc, off);
+        if (vlane >= off) inc = aff_combine(o, inc);
+    }
+    if (vlane == 31) wsc[slot] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        Aff3 t = lane < nw ? wsc[lane] : aff_identity();
+        const int li = lane % segw;
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) {
+            const Aff3 o = shfl_aff<true>(t, off);
+            if (li >= off) t = aff_combine(o, t);
+        }
+        const Aff3 prev = shfl_aff<true>(t, 1);
+        if (lane < nw) wsc[lane] = li == 0 ? aff_identity() : prev;
+    }
+    __syncthreads();
+    const Aff3 wpre = wsc[slot];
+    Aff3 ex = shfl_aff<!REV>(inc, 1);
+    if (vlane == 0) ex = aff_identity();
+    const Aff3 res = aff_combine(wpre, ex);
+    __syncthreads();
+    return res;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);

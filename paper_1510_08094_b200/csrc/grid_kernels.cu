@@ -17,6 +17,7 @@
 // rows only: the doubled rows j < M/2 are (-1)^k times row M/2-j in lambda-
 // spectral space, so the doubled grid is never stored).
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "block_ops.cuh"
@@ -172,7 +173,9 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
 // reference's band_solve runs (banded.cpp:121-147, no row ever swaps for
 // these systems) — which keeps the parallel sweeps below as accurate as the
 // sequential algorithm.
-__global__ void __launch_bounds__(128) pivot_table_kernel(int L, int k0, int ncols, double* ipt) {
+// Row (kl, par) of the table (stride doubles) holds 1/d' of both chains of
+// that parity at the natural index tau of each element.
+__global__ void __launch_bounds__(128) pivot_table_kernel(int L, int k0, int ncols, double* ipt, int stride) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= ncols * 4) return;
     const int kl = id >> 2, par = (id >> 1) & 1, side = id & 1;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(128) pivot_table_kernel(int L, int k0, int nco
     Chain cp, cm;
     make_chains(par, L, cp, cm);
     const Chain& ch = side == 0 ? cp : cm;
-    double* out = ipt + (static_cast<size_t>(kl) * 2 + par) * L;
+    double* out = ipt + (static_cast<size_t>(kl) * 2 + par) * stride;
     double ip = 0.0, cprev = 0.0;
     for (int i = 0; i < ch.n; ++i) {
         const int t = ch.t0 + ch.dt * i;
@@ -295,6 +298,19 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     __syncthreads();
 }
 
+// Chain solve with a fixed segment of S elements per thread (threads past the
+// chain end, and elements past it, carry zero pivots and data, which makes
+// their maps send everything to 0 — exactly the x_n = 0 truncation).
+//   pass 1: X -> F = Msin^2 X (registers) and the segment's forward map;
+//   pass 2: forward sweep r' -> g = r'/d' (to shared memory) while
+//           accumulating the segment's backward map x_s = G + P x_e
+//           (P = prod c_u, G = sum g_u prod_{j<u} c_j, c = -C/d');
+//   pass 3: back substitution x_u = c_u x_(u+1) + g_u.
+// Positions (digit-reversed slots, < 2^16) are kept packed two per register;
+// pivots stay in registers.  Chain coefficients come from t by FMAs
+// (4A = t (t - 3s) + 2, 4C = t (t + 3s) + 2, s = sign dt); max |F|^2 is kept
+// on the high word of its IEEE pattern (relative resolution 2^-20 of the
+// squared value; it only scales the precondition threshold).
 // Register-resident variant of solve_chain for segments of at most SMAX
 // elements per thread: every chain element is read from shared memory once
 // (its position through the digit-reversal table once), F, r' and the pivots
@@ -411,6 +427,182 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
     wsum.y += ws.y;
     __syncthreads();
     if (ch.dt > 0) SK_PROBE(19);
+}
+
+// Opaque copies: stop the compiler from keeping per-element values derived in
+// one pass (t_u, unpacked slots) alive across the block scans into the next.
+__device__ __forceinline__ double launder(double x) {
+    double y;
+    asm volatile("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ unsigned launder(unsigned x) {
+    unsigned y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+#ifndef SK_CHAIN_ATTR
+#define SK_CHAIN_ATTR __noinline__
+#endif
+template <int S>
+__device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict__ rev, const double* ip, Aff3* wsc,
+                                                 const Chain& ch, int L, double2 inner, unsigned* fmax_hi,
+                                                 double2* wsum, bool want_wsum, double2* x_first) {
+    constexpr int SP = (S + 1) / 2;
+    const int tid = threadIdx.x;
+    const int n = ch.n;
+    if (n <= 0) return;
+    const int s = tid * S;
+    const double s3 = ch.dt > 0 ? 3.0 : -3.0;
+    const double dtd = ch.dt;
+    const double t_s = static_cast<double>(ch.t0) + dtd * static_cast<double>(s);
+    const double tlo = -static_cast<double>(L), thi = static_cast<double>(L - 1);
+    unsigned pk[SP];
+    double2 v[S];
+    double ipv[S];
+    // Loads with compile-time offsets from a per-thread base: element u sits at
+    // natural index tau0 + dtau (s + u); elements past the chain end read
+    // in-range table entries and slots (their values are masked below).
+    auto load_seg = [&](auto dir) {
+        constexpr int D = decltype(dir)::value;
+        const int tb = ch.tau0 + (D > 0 ? s : -s);
+        const int* rb = rev + tb;
+        const double* ib = ip + tb;
+#pragma unroll
+        for (int u = 0; u < S; u += 2) {
+            const unsigned p0 = __ldg(rb + D * u);
+            const unsigned p1 = (u + 1 < S) ? __ldg(rb + D * (u + 1)) : 0u;
+            pk[u / 2] = p0 | (p1 << 16);
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) ipv[u] = ib[D * u];
+    };
+    if (ch.dtau > 0) load_seg(std::integral_constant<int, 1>{});
+    else load_seg(std::integral_constant<int, -1>{});
+    auto posu = [&](int u) { return static_cast<int>((u & 1) ? (pk[u / 2] >> 16) : (pk[u / 2] & 0xffffu)); };
+    double2 xlo = inner, xhi = make_double2(0.0, 0.0);
+    double ip_before = 0.0;
+    if (s > 0 && s <= n) {
+        const int tb = ch.tau0 + ch.dtau * (s - 1);
+        xlo = a[__ldg(rev + tb)];
+        ip_before = ip[tb];
+    }
+    if (s + S < n) xhi = a[__ldg(rev + ch.tau0 + ch.dtau * (s + S))];
+#pragma unroll
+    for (int u = 0; u < S; ++u) {
+        const bool ok = s + u < n;
+        const double2 x = a[posu(u)];
+        v[u] = ok ? x : make_double2(0.0, 0.0);
+        if (!ok) ipv[u] = 0.0;
+    }
+    // ---- pass 1
+    Aff3 aff = aff_identity();
+    {
+        unsigned fh = 0u;
+        double2 xm = xlo;
+        double ipp = ip_before;
+        double t = t_s;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            const double2 x0 = v[u];
+            const double2 xp = (u + 1 < S) ? v[u + 1] : xhi;
+            const double d2 = (t == tlo || t == thi) ? 0.25 : 0.5;
+            double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+            if (s + u >= n) F = make_double2(0.0, 0.0);
+            fh = max(fh, static_cast<unsigned>(__double2hiint(fma(F.x, F.x, F.y * F.y))));
+            const double al = (-0.25 * ipp) * fma(t, t - s3, 2.0);
+            aff = Aff3{al * aff.a, fma(al, aff.b, F.x), fma(al, aff.c, F.y)};
+            v[u] = F;
+            ipp = ipv[u];
+            xm = x0;
+            t += dtd;
+        }
+        *fmax_hi = max(*fmax_hi, fh);
+    }
+    const Aff3 rin = block_scan_aff<false>(aff, wsc);  // also orders every X read above before the writes below
+#pragma unroll
+    for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
+    // ---- pass 2
+    Aff3 baff;
+    {
+        double2 rp = make_double2(rin.b, rin.c);
+        double ipp = ip_before;
+        double t = launder(t_s);
+        double Pm = 1.0;
+        double2 G = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            const double al = (-0.25 * ipp) * fma(t, t - s3, 2.0);
+            rp = make_double2(fma(al, rp.x, v[u].x), fma(al, rp.y, v[u].y));
+            const double iv = ipv[u];
+            const double2 g = make_double2(rp.x * iv, rp.y * iv);
+            const double c = (-0.25 * iv) * fma(t, t + s3, 2.0);
+            G = make_double2(fma(Pm, g.x, G.x), fma(Pm, g.y, G.y));
+            Pm *= c;
+            if (s + u < n) a[posu(u)] = g;
+            ipv[u] = c;
+            ipp = iv;
+            t += dtd;
+        }
+        baff = Aff3{Pm, G.x, G.y};
+    }
+    const Aff3 xin = block_scan_aff<true>(baff, wsc);
+    // ---- pass 3
+#pragma unroll
+    for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
+    const double t_s3 = launder(t_s);
+    double2 x = make_double2(xin.b, xin.c);
+    double2 ws = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = S - 1; u >= 0; --u) {
+        if (s + u < n) {
+            const int p = posu(u);
+            const double2 g = a[p];
+            x = make_double2(fma(ipv[u], x.x, g.x), fma(ipv[u], x.y, g.y));
+            a[p] = x;
+            if (want_wsum) {
+                const double t = t_s3 + dtd * u;
+                const double w = 2.0 / (1.0 - t * t);
+                ws.x = fma(w, x.x, ws.x);
+                ws.y = fma(w, x.y, ws.y);
+            }
+        } else {
+            x = make_double2(0.0, 0.0);
+        }
+    }
+    wsum->x += ws.x;
+    wsum->y += ws.y;
+    if (tid == 0) *x_first = x;
+    __syncthreads();
+}
+
+// Smallest register segment S with ceil(n / S) <= nthr; 0 if none fits.
+__device__ __forceinline__ int chain_segment(int n, int nthr) {
+    const int need = (n + nthr - 1) / nthr;
+    if (need <= 2) return 2;
+    if (need <= 4) return 4;
+    if (need <= 6) return 6;
+    if (need <= 8) return 8;
+    if (need <= 10) return 10;
+    if (need <= 12) return 12;
+    return 0;
+}
+
+__device__ __forceinline__ bool solve_chain_fast_dispatch(double2* a, const int* rev, const double* ip, Aff3* wsc,
+                                                          const Chain& ch, int L, double2 inner, unsigned* fmax_hi,
+                                                          double2* wsum, bool want_wsum, double2* x_first) {
+#define SK_CH(S) solve_chain_fast<S>(a, rev, ip, wsc, ch, L, inner, fmax_hi, wsum, want_wsum, x_first)
+    switch (chain_segment(ch.n, blockDim.x)) {
+        case 2: SK_CH(2); return true;
+        case 4: SK_CH(4); return true;
+        case 6: SK_CH(6); return true;
+        case 8: SK_CH(8); return true;
+        case 10: SK_CH(10); return true;
+        case 12: SK_CH(12); return true;
+        default: return false;
+    }
+#undef SK_CH
 }
 
 // The lowest lambda modes are only weakly diagonally dominant (k = 0 not at
@@ -542,9 +734,12 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
 // offsets of lap are exact zeros, so even and odd modes never couple), and the
 // inverse transform.  The two halves are recombined through distributed
 // shared memory.
-template <bool SWZ>
+// CH selects the chain solver at compile time (one per kernel so that the
+// register allocation of each is independent): 0 shared-memory walk,
+// 1 fixed short segments (solve_chain_fast), 2 SMAX = 12 register walk.
+template <bool SWZ, int CH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(ThetaParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int L = P.fd.L;  // M/2
     double2* a = reinterpret_cast<double2*>(smem_raw);
@@ -569,7 +764,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
 
     Chain cp, cm;
     make_chains(par, L, cp, cm);
-    const size_t prow = (static_cast<size_t>(kl) * 2 + par) * L;  // pivot row (table index)
+    const size_t prow = (static_cast<size_t>(kl) * 2 + par) * P.piv_stride;  // pivot row (table index)
+
 
     // ---- bulk copies: the raw column (L+1 values) and the t > 0 chain's pivots
     SK_PROBE(0);
@@ -702,9 +898,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
     const bool seq = kg < P.kseq;
-    if (seq) solve_chain_seq(a, rev, ipp, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    else if (P.regsolve && cp.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
-    else solve_chain(a, rev, ipp, wsc, cp, L, inner_p, fmax_acc, wsum, want_wsum, &misc[3]);
+    unsigned fmax_hi = 0u;
+    Aff3* wsc3 = reinterpret_cast<Aff3*>(wsc);
+    auto solve_side = [&](const Chain& ch, const double* ipc, double2 inner, double2* xf) {
+        const bool reg12 = ch.n <= kSegMax * nthr;
+        if (seq) {
+            solve_chain_seq(a, rev, ipc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
+        } else if constexpr (CH == 2) {
+            if (reg12) solve_chain_reg<kSegMax>(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
+            else solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
+        } else if constexpr (CH == 1) {
+            if (!solve_chain_fast_dispatch(a, rev, ipc, wsc3, ch, L, inner, &fmax_hi, &wsum, want_wsum, xf))
+                solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
+        } else {
+            solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
+        }
+    };
+    solve_side(cp, ipp, inner_p, &misc[3]);
     SK_PROBE(4);
     // the t < 0 chain's pivots replace the t > 0 chain's in the window
     const double* ipm = ip;
@@ -719,9 +929,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         mbar_wait(&bars[1], 0);
     }
     SK_PROBE(5);
-    if (seq) solve_chain_seq(a, rev, ipm, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
-    else if (P.regsolve && cm.n <= kSegMax * nthr) solve_chain_reg<kSegMax>(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
-    else solve_chain(a, rev, ipm, wsc, cm, L, inner_m, fmax_acc, wsum, want_wsum, &misc[4]);
+    solve_side(cm, ipm, inner_m, &misc[4]);
+    fmax_acc = fmax(fmax_acc, __hiloint2double(static_cast<int>(fmax_hi), 0));
     SK_PROBE(6);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
@@ -859,23 +1068,33 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
+template <bool SWZ, int CH>
+static cudaError_t launch_theta_t(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        for (auto fn : {theta_kernel<false>, theta_kernel<true>}) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        }
+        cudaFuncSetAttribute(theta_kernel<SWZ, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(theta_kernel<SWZ, CH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr = true;
     }
-    if (P.swizzle) theta_kernel<true><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
-    else theta_kernel<false><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    theta_kernel<SWZ, CH><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, cudaStream_t st) {
+cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
+    const int ch = P.regsolve;  // chain solver chosen by the plan
+    if (P.swizzle) {
+        if (ch == 2) return launch_theta_t<true, 2>(P, nthr, smem, st);
+        if (ch == 1) return launch_theta_t<true, 1>(P, nthr, smem, st);
+        return launch_theta_t<true, 0>(P, nthr, smem, st);
+    }
+    if (ch == 2) return launch_theta_t<false, 2>(P, nthr, smem, st);
+    if (ch == 1) return launch_theta_t<false, 1>(P, nthr, smem, st);
+    return launch_theta_t<false, 0>(P, nthr, smem, st);
+}
+
+cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st) {
     const int n = ncols * 4;
-    pivot_table_kernel<<<(n + 127) / 128, 128, 0, st>>>(L, k0, ncols, ipt);
+    pivot_table_kernel<<<(n + 127) / 128, 128, 0, st>>>(L, k0, ncols, ipt, stride);
     return cudaGetLastError();
 }
 

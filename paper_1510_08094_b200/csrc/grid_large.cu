@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     auto slot = [&](int i) { return swz<true>(ch.tau0 + ch.dtau * i - q * Lq); };
 
     // pivot window of this CTA's chain part (TMA, overlaps the transforms)
-    const size_t prow = (static_cast<size_t>(kl) * 2 + par) * L;
+    const size_t prow = (static_cast<size_t>(kl) * 2 + par) * P.piv_stride;
     // (includes the pivot of element i_lo - 1, owned by the previous CTA)
     const int tau_a = plus ? ch.tau0 + max(i_lo - 1, 0) : ch.tau0 - (i_hi - 1);
     const int tau_b = plus ? ch.tau0 + i_hi : ch.tau0 - max(i_lo - 1, 0) + 1;

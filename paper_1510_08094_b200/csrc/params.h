@@ -36,8 +36,9 @@ struct ThetaParams {
     double2* xhalf;   // optional: solution coefficients X[k][i], (N/2+1) x M per rhs
     int kseq;         // lambda modes k < kseq use the sequential Thomas recurrence
     const double* pivots;  // pivot table for modes k0..k0+ncols-1 (pivot_table_kernel)
-    int regsolve;          // register-resident chain segments (1) or shared-memory walks (0)
+    int regsolve;          // chain solver: 0 shared-memory walk, 1 fixed short segments, 2 SMAX=12 register walk
     int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
+    int piv_stride;        // doubles per (mode, parity) pivot row
 };
 
 struct ShgenParams {
@@ -110,7 +111,7 @@ inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
 }
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
-cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, cudaStream_t st);
+cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 

@@ -294,7 +294,9 @@ struct sk_plan_s {
     double2* coef_stage = nullptr;  // shgen coefficients
     double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
-    int regsolve = 1;          // register-resident chain solve (SK_REGSOLVE)
+    int piv_stride = 0;        // doubles per pivot-table row
+    int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
+    int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -467,12 +469,21 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
             return s;
         }
         // data-independent Thomas pivots of every (lambda mode, parity) chain
-        const size_t np = static_cast<size_t>(p->g.cols) * 2 * p->g.Lt;
+        p->piv_stride = p->g.Lt + (p->g.Lt & 1);
+        // chain solver: fixed short segments up to 6 elements per thread, the
+        // 12-element register walk above (it keeps F in registers without
+        // spilling there), the shared-memory walk beyond
+        {
+            const int nmax = p->g.Lt / 2 + 1;
+            const int need = (nmax + p->thr_theta - 1) / p->thr_theta;
+            p->chain_mode = p->regsolve == 0 ? 0 : p->regsolve == 2 ? 2 : p->regsolve == 3 ? 1 : (need <= 6 ? 1 : 2);
+        }
+        const size_t np = static_cast<size_t>(p->g.cols) * 2 * p->piv_stride;
         if ((s = ensure(reinterpret_cast<void**>(&p->pivots), sizeof(double) * np)) != SK_OK) {
             sk_plan_destroy(p);
             return s;
         }
-        if (sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->stream) != cudaSuccess ||
+        if (sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream) != cudaSuccess ||
             cudaStreamSynchronize(p->stream) != cudaSuccess) {
             sk_plan_destroy(p);
             return fail(SK_ERR_CUDA, "pivot table construction failed");
@@ -657,9 +668,10 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.stats = p->stats;
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
-        tp.regsolve = p->regsolve;
+        tp.regsolve = p->chain_mode;
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
-        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->g.Lt;  // rows for this rank's modes
+        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes
+        tp.piv_stride = p->piv_stride;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         if (p->theta_q) {
             sk::ThetaLargeParams tl{tp, p->ftq.d};

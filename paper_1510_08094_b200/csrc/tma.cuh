@@ -61,6 +61,20 @@ __device__ __forceinline__ uint32_t bulk_g2s_chunked(void* dst, const void* src,
     return bytes;
 }
 
+// Prefetch [src, src + bytes) into L2 (16-byte aligned, bytes % 16 == 0).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// Prefetch an arbitrary range of doubles, widened to 16-byte alignment.
+__device__ __forceinline__ void prefetch_l2_doubles(const double* p, size_t count) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p + count) + 15) & ~static_cast<uintptr_t>(15);
+    for (uintptr_t a = a0; a < a1; a += 65536) {
+        const uintptr_t e = (a1 - a) < 65536 ? a1 : a + 65536;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(a), static_cast<uint32_t>(e - a));
+    }
+}
+
 // 3-D tensor copies through a CUtensorMap (box into / out of shared memory).
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
     asm volatile(

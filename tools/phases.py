@@ -25,16 +25,16 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 24).astype(np.int64)
 n = min(4096, 2 * (cfg.N // 2 + 1))
 a = a[:n]
 names = ["bars+issue+twiddles+TMA wait", "fold", "fft fwd", "mean+inner+chain+ solve", "pivot- TMA wait",
-         "chain- solve", "x0/fmax/export", "(pre-inverse)", "fft inv", "combine+stores", ""]
+         "chain- solve", "x0/fmax/export", "fft inv", "cluster sync+combine+stores", "final cluster sync", ""]
 d = np.diff(a[:, :11], axis=1)
 tot = (a[:, 10] - a[:, 0])
 print(f"{cfg.name}: CTAs sampled {n}, mean cycles per CTA {tot.mean():.0f}")
 for i in range(10):
     print(f"  {names[i]:28s} {d[:, i].mean():9.0f} cyc  {100 * d[:, i].mean() / tot.mean():5.1f}%")
 
-sub = a[:, 12:20]
+sub = a[:, 12:18]
 if (sub > 0).all():
-    sn = ["loads", "F", "fwd summary", "scan1", "fwd sweep", "bwd summary", "scan2", "bwd sweep+store"]
+    sn = ["loads+sync", "pass1 (F, fwd map)", "scan1", "pass2 (sweep, bwd map)", "scan2", "pass3 (back subst)"]
     dd = np.diff(np.concatenate([a[:, 3:4], sub], axis=1), axis=1)
     for i, nm in enumerate(sn):
         print(f"    chain+ {nm:18s} {dd[:, i].mean():8.0f} cyc")

@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
         mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
         bulk_g2s_chunked(a, src, static_cast<uint32_t>(L) * 16, bar);  // the real row as N/2 complex pairs
     }
+    // twiddles and the digit-reversal table by the threads while the row is in
+    // flight (measured faster here than adding them to the bulk copies)
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();
@@ -114,11 +116,14 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const int nbox = L / kBoxModes + 1;
-        mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * kBoxModes * 16);
+        const uint32_t rb = static_cast<uint32_t>((L + 3) & ~3) * 4;  // rev table, padded to 16 bytes
+        mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * kBoxModes * 16 + (P.fd.nhi + P.fd.nlo) * 16 + rb);
         for (int k0 = 0; k0 <= L; k0 += kBoxModes) tma_load_3d(a + k0, &tmap, 2 * row, k0, rhs, bar);
+        bulk_g2s_chunked(s_hi, P.fd.hi, P.fd.nhi * 16, bar);
+        bulk_g2s_chunked(s_lo, P.fd.lo, P.fd.nlo * 16, bar);
+        bulk_g2s_chunked(s_rev, P.fd.rev, rb, bar);
     }
-    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
-    for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
+    const Tw T{s_hi, s_lo, P.fd.shift, (1 << P.fd.shift) - 1};
     __syncthreads();
     mbar_wait(bar, 0);
     double2 zk[kLamPairs], zm[kLamPairs];

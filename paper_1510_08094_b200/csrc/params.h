@@ -107,7 +107,7 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
 // Lambda-stage shared memory (bytes) for transform length L and twiddle table sizes.
 inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
     const size_t lpad = static_cast<size_t>((L / 256 + 1) * 256);
-    return lpad * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>((L + 3) & ~3) * 4 + 16;
+    return lpad * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>((L + 3) & ~3) * 4 + 32;
 }
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);

@@ -130,7 +130,7 @@ sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, b
     std::vector<double2> hi(d.nhi), lo(d.nlo);
     for (int h = 0; h < d.nhi; ++h) root(static_cast<long long>(h) * B, n2, hi[h].x, hi[h].y);
     for (int l = 0; l < d.nlo; ++l) root(l, n2, lo[l].x, lo[l].y);
-    std::vector<int> rev(L);
+    std::vector<int> rev((L + 3) & ~3, 0);  // padded to 16 bytes for bulk copies
     for (int k = 0; k < L; ++k) {
         int kk = k, pos = 0;
         for (int s = 0; s < d.nst; ++s) {
@@ -142,10 +142,10 @@ sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, b
     }
     CU(cudaMalloc(&out.hi, sizeof(double2) * d.nhi));
     CU(cudaMalloc(&out.lo, sizeof(double2) * d.nlo));
-    CU(cudaMalloc(&out.rev, sizeof(int) * L));
+    CU(cudaMalloc(&out.rev, sizeof(int) * rev.size()));
     CU(cudaMemcpy(out.hi, hi.data(), sizeof(double2) * d.nhi, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(out.lo, lo.data(), sizeof(double2) * d.nlo, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(out.rev, rev.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(out.rev, rev.data(), sizeof(int) * rev.size(), cudaMemcpyHostToDevice));
     d.hi = out.hi;
     d.lo = out.lo;
     d.rev = out.rev;

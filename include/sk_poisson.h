@@ -130,7 +130,10 @@ sk_status sk_stage_lambda_inv(sk_plan_t plan, int P, const int* row_bounds, cons
 /* Plan facts: info[0] = M, [1] = N, [2] = nrhs, [3] = device,
  * [4] = grid path supported (1/0), [5] = spectrum leading dimension,
  * [6] = theta-stage split (CTAs per column), [7] = theta-stage threads,
- * [8] = lambda-stage threads, [9] = kernels launched by the last call. */
+ * [8] = lambda-stage threads, [9] = kernels launched by the last call,
+ * [10]/[11] = theta/lambda shared memory per CTA (bytes), [12] = theta chain
+ * solver (0 shared-memory walk, 1 fixed segments, 2 12-element register
+ * walk). */
 sk_status sk_plan_info(sk_plan_t plan, long long info[16]);
 
 /* Time one launch of each stage (device events, ms): t[0] lambda_fwd,

@@ -560,6 +560,7 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     info[9] = p->last_launches;
     info[10] = static_cast<long long>(p->smem_theta);
     info[11] = static_cast<long long>(p->smem_lambda);
+    info[12] = p->chain_mode;
     return SK_OK;
 }
 

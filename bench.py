@@ -9,8 +9,10 @@ with the k=0 constraint -> inverse transforms -> physical u.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 N > 1: launched under torchrun, one rank per GPU; the solve is slab-
-decomposed with two NCCL all-to-all transposes (strong scaling of one RHS;
-for C4 the RHS are sharded instead: weak scaling, no collective).
+decomposed (strong scaling of one RHS) with the two transposes fused into the
+stage kernels as NVLink peer stores through CUDA IPC mappings (--transport
+p2p, default) or as NCCL all-to-alls (--transport nccl, the baseline); for C4
+the RHS are sharded instead (weak scaling, no exchange).
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -40,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--cpu-sample-cols", type=int, default=0)
     return ap.parse_args()
 
@@ -79,6 +82,9 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def count(self) -> int:
+        return len(self.lines)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -160,11 +166,17 @@ def run_reference_arm(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+def big_inputs(cfg) -> bool:
+    """f, u and the half spectrum of one step exceed the 126 MB L2 by 2x."""
+    return (8 * (cfg.M // 2 + 1) * cfg.N * 2 + 16 * (cfg.M // 2 + 1) * (cfg.N // 2 + 1)) * cfg.nrhs > 256e6
+
+
 def config_block(cfg, ngpus):
     par = f"slab{ngpus}" if (ngpus > 1 and cfg.nrhs == 1) else (f"rhs{ngpus}" if ngpus > 1 else "single")
     return {"workload": f"{cfg.name}: {cfg.note}", "M": cfg.M, "N": cfg.N, "nrhs": cfg.nrhs,
             "sh_degree": cfg.L, "coeff_decay": cfg.p, "dof_per_rhs": cfg.dof, "parallelism": par,
-            "l2": "inputs larger than L2 (no flush)" if cfg.M * cfg.N * 8 > 256e6 else "L2 flushed between steps"}
+            "l2": "inputs larger than L2 (no flush)" if big_inputs(cfg) else "L2 flushed between steps (256 MB write)",
+            "transport": None}
 
 
 # ---------------------------------------------------------------- our arm
@@ -207,7 +219,7 @@ def main():
 
     if slab:
         from paper_1510_08094_b200.distributed import SlabSolver, slab_bounds
-        solver = SlabSolver(cfg.M, cfg.N, rank, world, device=dev)
+        solver = SlabSolver(cfg.M, cfg.N, rank, world, device=dev, transport=args.transport)
         solver._plan.set_stream(stream.cuda_stream)
         rb = solver.rb
         f_rows = f[0, rb[rank]: rb[rank + 1]].contiguous()
@@ -219,6 +231,11 @@ def main():
         def step():
             plan.solve_grid(f if nrhs_local > 1 else f[0], u if nrhs_local > 1 else u[0], sync=False)
 
+    # below 2x L2 the step's working set would stay cache-resident: write a
+    # 256 MB buffer between timed steps (its time is excluded: events bracket
+    # each step when flushing)
+    flush = None if big_inputs(cfg) else torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+
     def barrier():
         if dist is not None:
             dist.barrier()
@@ -228,17 +245,49 @@ def main():
         step()
     barrier()
 
+    # untimed steps around the timed region so that the clock sampler sees
+    # the GPU under this load (same count on every rank)
+    t0 = time.perf_counter()
+    step()
+    barrier()
+    t_one = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([t_one], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_one = tt.item()
+    n_pre = max(1, min(2000, int(math.ceil(0.4 / max(t_one, 1e-6)))))
+    n_post = max(1, n_pre // 2)
+
     # ---- timed region (device-resident inputs)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
+        # keep the GPU under this load until the sampler reports (nvidia-smi
+        # needs ~100 ms to start), so samples are taken under load right
+        # before and (below) right after the timed steps
+        for _ in range(n_pre):
             step()
-        ev1.record(stream)
         barrier()
-    ms_total = ev0.elapsed_time(ev1)
+        if flush is None:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step()
+            ev1.record(stream)
+            barrier()
+            ms_total = ev0.elapsed_time(ev1)
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                flush.fill_(1.0)
+                a.record(stream)
+                step()
+                b.record(stream)
+            barrier()
+            ms_total = sum(a.elapsed_time(b) for a, b in evs)
+        for _ in range(n_post):
+            step()
+        barrier()
     if dist is not None:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -272,6 +321,36 @@ def main():
 
     # ---- end to end through the public API with host buffers
     e2e = None
+    if slab:
+        # rows of f in from pinned host memory, rows of u back, every step
+        fh = torch.empty(f_rows.shape, dtype=torch.float64, pin_memory=True)
+        uh = torch.empty(f_rows.shape, dtype=torch.float64, pin_memory=True)
+        fh.copy_(f_rows.cpu())
+
+        def step_e2e():
+            f_rows.copy_(fh, non_blocking=True)
+            solver.solve(f_rows, u_rows)
+            uh.copy_(u_rows, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        t = torch.tensor([max(e0.elapsed_time(e1), 1e3 * wall)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = t.item() / args.steps
+        nb = rows * cfg.N * 8
+        e2e = {"value": dofs_step / (ms_e2e * 1e-3), "unit": "DOF/s", "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e}
     if not slab:
         fh = torch.empty(f.shape, dtype=torch.float64, pin_memory=True)
         uh = torch.empty(f.shape, dtype=torch.float64, pin_memory=True)
@@ -342,7 +421,8 @@ def main():
         "scaling": "strong" if slab else ("weak" if world > 1 else "strong"),
         "vs_baseline": value / PUBLISHED_DOF_PER_S if cfg.name == "C3" else None,
         "dtype": "f64", "data": "synthetic: seeded spherical-harmonic sums generated on the device",
-        "config": config_block(cfg, world), "gpu_launches": launches, "clocks": clk.summary(),
+        "config": {**config_block(cfg, world), "transport": args.transport if slab else None},
+        "gpu_launches": launches, "clocks": clk.summary(),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "parity_rel_err_vs_analytic": err,
     }
     print(json.dumps(line), flush=True)

@@ -127,6 +127,28 @@ sk_status sk_stage_theta(sk_plan_t plan, int P, const int* row_bounds, const int
 sk_status sk_stage_lambda_inv(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
                               const double* back_dev, double* u_rows_dev);
 
+/* Fused-transpose variants (one process per GPU over NVLink / NVSwitch): the
+ * forward lambda stage stores mode k of its rows straight into the receive
+ * buffer of the rank owning k, and the theta stage stores row p of its solved
+ * columns straight into the return buffer of the rank owning p, so neither
+ * exchange needs a collective.  peer_recv[d] / peer_back[d] are every rank's
+ * buffers as mapped in this process (sk_ipc_open; this rank's own buffer for
+ * d = rank); layouts as for sk_stage_theta / sk_stage_lambda_inv.  All ranks
+ * must finish a stage before any rank starts the next one (the caller's
+ * barrier), and sk_stage_lambda_inv then reads the local return buffer. */
+sk_status sk_stage_lambda_fwd_peer(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
+                                   const double* f_rows_dev, void* const* peer_recv);
+sk_status sk_stage_theta_peer(sk_plan_t plan, int P, const int* row_bounds, const int* col_bounds, int rank,
+                              double* recv_dev, void* const* peer_back);
+
+/* Device buffers that can be shared with other processes, and their CUDA IPC
+ * handles (64 bytes) / mappings. */
+sk_status sk_device_alloc(int device, size_t bytes, void** ptr);
+sk_status sk_device_free(void* ptr);
+sk_status sk_ipc_handle(const void* ptr, unsigned char handle[64]);
+sk_status sk_ipc_open(int device, const unsigned char handle[64], void** ptr);
+sk_status sk_ipc_close(void* ptr);
+
 /* Plan facts: info[0] = M, [1] = N, [2] = nrhs, [3] = device,
  * [4] = grid path supported (1/0), [5] = spectrum leading dimension,
  * [6] = theta-stage split (CTAs per column), [7] = theta-stage threads,

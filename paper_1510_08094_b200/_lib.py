@@ -30,6 +30,8 @@ EXPORTS = [
     "sk_plan_create", "sk_plan_destroy", "sk_plan_set_stream", "sk_sync", "sk_solve_coeffs", "sk_residual",
     "sk_solve_grid", "sk_last_mean", "sk_shgen", "sk_stage_lambda_fwd", "sk_stage_theta", "sk_stage_lambda_inv",
     "sk_plan_info", "sk_stage_times", "sk_enable_stage_timing", "sk_last_error", "sk_version",
+    "sk_stage_lambda_fwd_peer", "sk_stage_theta_peer", "sk_device_alloc", "sk_device_free", "sk_ipc_handle",
+    "sk_ipc_open", "sk_ipc_close",
 ]
 
 
@@ -98,6 +100,13 @@ def load() -> ctypes.CDLL:
         "sk_plan_info": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
         "sk_stage_times": (I, [P, D]),
         "sk_enable_stage_timing": (I, [P, I]),
+        "sk_stage_lambda_fwd_peer": (I, [P, I, IP, IP, I, P, ctypes.POINTER(P)]),
+        "sk_stage_theta_peer": (I, [P, I, IP, IP, I, P, ctypes.POINTER(P)]),
+        "sk_device_alloc": (I, [I, ctypes.c_size_t, ctypes.POINTER(P)]),
+        "sk_device_free": (I, [P]),
+        "sk_ipc_handle": (I, [P, ctypes.c_char_p]),
+        "sk_ipc_open": (I, [I, ctypes.c_char_p, ctypes.POINTER(P)]),
+        "sk_ipc_close": (I, [P]),
         "sk_last_error": (ctypes.c_char_p, []),
         "sk_version": (ctypes.c_char_p, []),
     }

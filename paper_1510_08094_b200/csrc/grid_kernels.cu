@@ -91,8 +91,15 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
         const double2 Xk = cadd(A, cmul(T(k), B));
         const double2 Xm = cadd(conjd(A), cmul(T(km), conjd(B)));
-        out[static_cast<size_t>(k) * P.rows_local + row] = cscale(Xk, (k & 1) ? -invN : invN);
-        if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = cscale(Xm, (km & 1) ? -invN : invN);
+        const double2 vk = cscale(Xk, (k & 1) ? -invN : invN);
+        const double2 vm = cscale(Xm, (km & 1) ? -invN : invN);
+        if (P.peers.n) {  // fused transpose: store into the theta rank's receive buffer over NVLink
+            *peer_ptr(P.peers, k, k, row) = vk;
+            if (km != k) *peer_ptr(P.peers, km, km, row) = vm;
+        } else {
+            out[static_cast<size_t>(k) * P.rows_local + row] = vk;
+            if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = vm;
+        }
     }
 }
 
@@ -979,7 +986,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     for (int p = p_lo + tid; p < p_hi; p += nthr) {
         const int pm = swz<SWZ>(p == L ? 0 : p);
         const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
-        colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
+        if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
+        else colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }
     SK_PROBE(9);
     cluster.sync();

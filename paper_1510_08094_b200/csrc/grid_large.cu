@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     double2* colbase = P.buf + rhs * P.rhs_stride;
     auto gcol = [&](int p) { return colbase + theta_addr(P.sl, P.ncols, kl, p); };
     auto rmt = [&](int r) { return cluster.map_shared_rank(a, r); };  // CTA r's data slots
+    // output row p: in place, or straight into its lambda rank's return buffer
+    auto gout = [&](int p) { return P.peers.n ? peer_ptr(P.peers, p, kg, p) : gcol(p); };
     const int* revq = fq.rev;
 
     // chain of this CTA and its element range
@@ -387,11 +389,11 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
         for (int m = m_lo + tid; m < m_hi; m += nthr) {
             const int j = Q * m + q;
             const int ps = swz<true>(__ldg(revq + m));
-            *gcol(j) = cadd(ve[ps], cmulc(vo[ps], TM(j)));
+            *gout(j) = cadd(ve[ps], cmulc(vo[ps], TM(j)));
         }
         if (par == 0 && q == 0 && tid == 0) {
             const int ps = swz<true>(__ldg(revq + 0));
-            *gcol(L) = csub(ve[ps], vo[ps]);  // j = L: w_M^L = -1
+            *gout(L) = csub(ve[ps], vo[ps]);  // j = L: w_M^L = -1
         }
     }
     cluster.sync();
@@ -443,8 +445,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
         const double2 Xk = cadd(A, cmul(TN(k), B));
         const double2 Xm = cadd(conjd(A), cmul(TN(km), conjd(B)));
-        out[static_cast<size_t>(k) * P.rows_local + row] = cscale(Xk, (k & 1) ? -invN : invN);
-        if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = cscale(Xm, (km & 1) ? -invN : invN);
+        const double2 vk = cscale(Xk, (k & 1) ? -invN : invN);
+        const double2 vm = cscale(Xm, (km & 1) ? -invN : invN);
+        if (P.peers.n) {
+            *peer_ptr(P.peers, k, k, row) = vk;
+            if (km != k) *peer_ptr(P.peers, km, km, row) = vm;
+        } else {
+            out[static_cast<size_t>(k) * P.rows_local + row] = vk;
+            if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = vm;
+        }
     }
     cluster.sync();
 }

@@ -21,6 +21,7 @@ struct LambdaParams {
     const double* f;    // fwd: real rows; inv: unused
     double2* spec;      // fwd: output [k][p_local]; inv: input
     double* u;          // inv: real rows
+    PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
 };
 
 struct ThetaParams {
@@ -39,6 +40,7 @@ struct ThetaParams {
     int regsolve;          // chain solver: 0 shared-memory walk, 1 fixed short segments, 2 SMAX=12 register walk
     int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
     int piv_stride;        // doubles per (mode, parity) pivot row
+    PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
 };
 
 struct ShgenParams {

@@ -46,6 +46,18 @@ struct Slabs {
     int col_b[kMaxRanks + 1] = {};
 };
 
+// Destinations of a stage's output in other ranks' buffers (device pointers
+// valid in this process: CUDA IPC mappings of the peers' allocations).  The
+// element with owner index idx and coordinates (a, b) goes to
+// base[d] + off[d] + a mul[d] + b, d the rank with bound[d] <= idx < bound[d+1].
+struct PeerMap {
+    double2* base[kMaxRanks] = {};
+    long long off[kMaxRanks] = {};
+    int mul[kMaxRanks] = {};
+    int bound[kMaxRanks + 1] = {};
+    int n = 0;  // 0: the stage writes its own buffer
+};
+
 struct GridGeom {
     int M = 0, N = 0;
     int Lt = 0;   // theta FFT length M/2

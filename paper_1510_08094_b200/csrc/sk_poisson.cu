@@ -631,7 +631,8 @@ sk_status sk_residual(sk_plan_t p, const double* F, const double* X, double out[
 }
 
 static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int ncols_local, int k0,
-                          const double* f_dev, double2* spec, double* u_dev, double2* xhalf, int stages) {
+                          const double* f_dev, double2* spec, double* u_dev, double2* xhalf, int stages,
+                          const sk::PeerMap* peers = nullptr) {
     // stages bit 0: lambda fwd, bit 1: theta, bit 2: lambda inv
     sk::LambdaParams lp{};
     lp.g = p->g;
@@ -643,6 +644,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.out_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
         lp.f = f_dev;
         lp.spec = spec;
+        if (peers) lp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[0], p->stream));
         if (p->lambda_split) {
             sk::LambdaSplitParams sp{lp, p->flh.d};
@@ -673,6 +675,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes
         tp.piv_stride = p->piv_stride;
+        if (peers) tp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         if (p->theta_q) {
             sk::ThetaLargeParams tl{tp, p->ftq.d};
@@ -689,6 +692,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.f = nullptr;
         lp.spec = spec;
         lp.u = u_dev;
+        lp.peers = sk::PeerMap{};
         if (p->timing) CU(cudaEventRecord(p->ev[4], p->stream));
         if (p->lambda_split) {
             sk::LambdaSplitParams sp{lp, p->flh.d};
@@ -869,6 +873,93 @@ sk_status sk_stage_lambda_inv(sk_plan_t p, int P, const int* rb, const int* cb, 
     p->last_launches = 0;
     return run_grid(p, sl, rows, cb[rank + 1] - cb[rank], cb[rank], nullptr,
                     const_cast<double2*>(reinterpret_cast<const double2*>(back_dev)), u_rows_dev, nullptr, 4);
+}
+
+sk_status sk_stage_lambda_fwd_peer(sk_plan_t p, int P, const int* rb, const int* cb, int rank,
+                                   const double* f_rows_dev, void* const* peer_recv) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    sk::Slabs sl{};
+    if ((s = make_slabs(p, P, rb, cb, rank, sl)) != SK_OK) return s;
+    if (!peer_recv) return fail(SK_ERR_ARGUMENT, "null peer buffer table");
+    const int rows = rb[rank + 1] - rb[rank];
+    if (rows == 0) return SK_OK;
+    sk::PeerMap pm{};
+    pm.n = P;
+    for (int d = 0; d < P; ++d) {
+        if (!peer_recv[d] && cb[d + 1] > cb[d]) return fail(SK_ERR_ARGUMENT, "null peer receive buffer");
+        pm.base[d] = static_cast<double2*>(peer_recv[d]);
+        pm.mul[d] = rows;
+        pm.off[d] = static_cast<long long>(cb[d + 1] - cb[d]) * rb[rank] - static_cast<long long>(cb[d]) * rows;
+        pm.bound[d] = cb[d];
+    }
+    pm.bound[P] = cb[P];
+    p->last_launches = 0;
+    return run_grid(p, sl, rows, cb[rank + 1] - cb[rank], cb[rank], f_rows_dev, nullptr, nullptr, nullptr, 1, &pm);
+}
+
+sk_status sk_stage_theta_peer(sk_plan_t p, int P, const int* rb, const int* cb, int rank, double* recv_dev,
+                              void* const* peer_back) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
+    sk::Slabs sl{};
+    if ((s = make_slabs(p, P, rb, cb, rank, sl)) != SK_OK) return s;
+    if (!peer_back) return fail(SK_ERR_ARGUMENT, "null peer buffer table");
+    const int ncols = cb[rank + 1] - cb[rank];
+    CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4, p->stream));
+    if (ncols == 0) return SK_OK;
+    sk::PeerMap pm{};
+    pm.n = P;
+    for (int r = 0; r < P; ++r) {
+        if (!peer_back[r] && rb[r + 1] > rb[r]) return fail(SK_ERR_ARGUMENT, "null peer return buffer");
+        pm.base[r] = static_cast<double2*>(peer_back[r]);
+        pm.mul[r] = rb[r + 1] - rb[r];
+        pm.off[r] = -static_cast<long long>(rb[r]);
+        pm.bound[r] = rb[r];
+    }
+    pm.bound[P] = rb[P];
+    p->last_launches = 0;
+    return run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2,
+                    &pm);
+}
+
+sk_status sk_device_alloc(int device, size_t bytes, void** ptr) {
+    if (!ptr) return fail(SK_ERR_ARGUMENT, "null output pointer");
+    *ptr = nullptr;
+    CU(cudaSetDevice(device));
+    CU(cudaMalloc(ptr, bytes ? bytes : 16));
+    return SK_OK;
+}
+
+sk_status sk_device_free(void* ptr) {
+    if (ptr) CU(cudaFree(ptr));
+    return SK_OK;
+}
+
+sk_status sk_ipc_handle(const void* ptr, unsigned char handle[64]) {
+    if (!ptr || !handle) return fail(SK_ERR_ARGUMENT, "null pointer");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+    std::memcpy(handle, &h, 64);
+    return SK_OK;
+}
+
+sk_status sk_ipc_open(int device, const unsigned char handle[64], void** ptr) {
+    if (!ptr || !handle) return fail(SK_ERR_ARGUMENT, "null pointer");
+    *ptr = nullptr;
+    CU(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    CU(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return SK_OK;
+}
+
+sk_status sk_ipc_close(void* ptr) {
+    if (ptr) CU(cudaIpcCloseMemHandle(ptr));
+    return SK_OK;
 }
 
 }  // extern "C"

@@ -21,6 +21,12 @@ __device__ __forceinline__ size_t theta_addr(const Slabs& sl, int ncols, int kl,
 }
 
 
+__device__ __forceinline__ double2* peer_ptr(const PeerMap& pm, int idx, long long a, long long b) {
+    int d = 0;
+    while (d + 1 < pm.n && idx >= pm.bound[d + 1]) ++d;
+    return pm.base[d] + (pm.off[d] + a * pm.mul[d] + b);
+}
+
 // theta-mode index of natural FFT index tau in parity class par (t = 2 tau + par
 // folded into [-M/2, M/2)).
 __device__ __forceinline__ int t_of(int tau, int par, int L) {

@@ -13,6 +13,20 @@ receive buffer is the concatenation over sources s of [k - col_b[d]][p -
 row_b[s]] blocks, which the theta stage reads piecewise and overwrites in
 place; the return exchange sends the same blocks back.
 
+Two transports (``SlabSolver(transport=...)``):
+
+* ``"p2p"`` (the product on a GPU box): the exchanges are fused into the
+  stage kernels.  Every rank allocates its receive / return buffers with
+  ``sk_device_alloc``, the CUDA IPC handles are exchanged once through
+  torch.distributed, and each rank maps every peer's buffers.  The forward
+  lambda kernel then stores mode k of its rows straight into the receive
+  buffer of the rank owning k, and the theta kernel stores row p of its
+  solved columns straight into the return buffer of the rank owning p (NVLink
+  stores over NVSwitch); a barrier between stages is the only
+  synchronisation, no collective moves data.
+* ``"nccl"``: the two exchanges as ``all_to_all_single`` over NCCL — the
+  comparison baseline.
+
 The per-rank stage work is pluggable (``backend``) so that the host-side
 orchestration can be exercised on CPU with gloo (tests/test_distributed.py);
 the product backend is the CUDA library (``CudaStages``).
@@ -45,6 +59,46 @@ class CudaStages:
         self.plan.stage_lambda_inv(P, rb, cb, rank, back, u_rows)
 
 
+class PeerBuffers:
+    """A device buffer per rank, shared with every other rank through CUDA
+    IPC: ``ptrs[d]`` is rank d's buffer as mapped in this process."""
+
+    def __init__(self, nbytes: int, device_index: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+        self._lib = _lib.load()
+        self.device = device_index
+        own = ctypes.c_void_p()
+        _lib.check(self._lib.sk_device_alloc(device_index, max(int(nbytes), 16), ctypes.byref(own)))
+        self.own = int(own.value)
+        h = ctypes.create_string_buffer(64)
+        _lib.check(self._lib.sk_ipc_handle(ctypes.c_void_p(self.own), h))
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        me = dist.get_rank(group)
+        self.ptrs, self._opened = [], []
+        for d, hd in enumerate(handles):
+            if d == me:
+                self.ptrs.append(self.own)
+                continue
+            q = ctypes.c_void_p()
+            _lib.check(self._lib.sk_ipc_open(device_index, ctypes.create_string_buffer(hd, 64), ctypes.byref(q)))
+            self.ptrs.append(int(q.value))
+            self._opened.append(int(q.value))
+
+    def close(self):
+        import ctypes
+        for q in self._opened:
+            self._lib.sk_ipc_close(ctypes.c_void_p(q))
+        self._opened = []
+        if self.own:
+            self._lib.sk_device_free(ctypes.c_void_p(self.own))
+            self.own = 0
+
+
 class SlabSolver:
     """One rank of the P-way slab-decomposed grid solve.
 
@@ -52,7 +106,8 @@ class SlabSolver:
     of f, shape (rows_r, N) float64, and returns the same rows of u.
     """
 
-    def __init__(self, M: int, N: int, rank: int, world: int, device=None, backend=None, group=None):
+    def __init__(self, M: int, N: int, rank: int, world: int, device=None, backend=None, group=None,
+                 transport: str = "nccl"):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -73,22 +128,54 @@ class SlabSolver:
         # exchange sizes in doubles (complex = 2 doubles)
         self.send_split = [2 * (self.cb[d + 1] - self.cb[d]) * self.rows_r for d in range(world)]
         self.recv_split = [2 * self.cols_r * (self.rb[s + 1] - self.rb[s]) for s in range(world)]
+        self.transport = transport
         kw = dict(dtype=torch.float64, device=self.device)
-        self.send = torch.empty(sum(self.send_split), **kw)
-        self.recv = torch.empty(sum(self.recv_split), **kw)
-        self.back = torch.empty(sum(self.send_split), **kw)
+        if transport == "p2p":
+            if backend is not None and not isinstance(backend, CudaStages):
+                raise ValueError("the p2p transport needs the CUDA stages")
+            dev = device.index if device is not None and device.index is not None else 0
+            # receive buffer: cols_r x all rows; return buffer: all modes x rows_r (complex)
+            self.recv_pb = PeerBuffers(8 * sum(self.recv_split), dev, group)
+            self.back_pb = PeerBuffers(8 * sum(self.send_split), dev, group)
+            self.recv, self.back = self.recv_pb.own, self.back_pb.own
+        elif transport == "nccl":
+            self.send = torch.empty(sum(self.send_split), **kw)
+            self.recv = torch.empty(sum(self.recv_split), **kw)
+            self.back = torch.empty(sum(self.send_split), **kw)
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
 
     def solve(self, f_rows, u_rows=None):
         torch, dist = self.torch, self.dist
         if u_rows is None:
             u_rows = torch.empty_like(f_rows)
         P, rb, cb, r = self.P, self.rb, self.cb, self.rank
+        if self.transport == "p2p":
+            plan = self.backend.plan
+            plan.stage_lambda_fwd_peer(P, rb, cb, r, f_rows, self.recv_pb.ptrs)
+            self._stage_barrier(plan)
+            plan.stage_theta_peer(P, rb, cb, r, self.recv, self.back_pb.ptrs)
+            self._stage_barrier(plan)
+            plan.stage_lambda_inv(P, rb, cb, r, self.back, u_rows)
+            return u_rows
         self.backend.lambda_fwd(P, rb, cb, r, f_rows, self.send)
         dist.all_to_all_single(self.recv, self.send, self.recv_split, self.send_split, group=self.group)
         self.backend.theta(P, rb, cb, r, self.recv)
         dist.all_to_all_single(self.back, self.recv, self.send_split, self.recv_split, group=self.group)
         self.backend.lambda_inv(P, rb, cb, r, self.back, u_rows)
         return u_rows
+
+    def _stage_barrier(self, plan):
+        """Every rank's stores into its peers' buffers are complete (the
+        stage's kernel finished) before any rank reads them."""
+        plan.sync()
+        self.dist.barrier(group=self.group)
+
+    def close(self):
+        if self.transport == "p2p":
+            self.dist.barrier(group=self.group)  # no peer still reads our buffers
+            self.recv_pb.close()
+            self.back_pb.close()
 
     def check_precondition(self):
         """All-reduce of the mean / max|F| statistics of the last solve and

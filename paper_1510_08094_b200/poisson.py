@@ -40,6 +40,8 @@ def _ptr(a) -> Optional[int]:
     """Raw address of a numpy array or a torch tensor (None passes NULL)."""
     if a is None:
         return None
+    if isinstance(a, int):  # raw device address (sk_device_alloc / sk_ipc_open)
+        return a
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return int(a.data_ptr())  # torch.Tensor
@@ -202,6 +204,22 @@ class Plan:
         rb, cb = self._bounds(P, row_b, col_b)
         self._follow_torch(recv)
         _lib.check(self.lib.sk_stage_theta(self._h, P, rb, cb, rank, _ptr(recv)))
+
+    def stage_lambda_fwd_peer(self, P, row_b, col_b, rank, f_rows, peer_recv):
+        """Forward lambda stage storing straight into every rank's receive
+        buffer (peer_recv[d]: rank d's buffer mapped in this process)."""
+        rb, cb = self._bounds(P, row_b, col_b)
+        self._follow_torch(f_rows)
+        tab = (ctypes.c_void_p * P)(*[_ptr(b) for b in peer_recv])
+        _lib.check(self.lib.sk_stage_lambda_fwd_peer(self._h, P, rb, cb, rank, _ptr(f_rows), tab))
+
+    def stage_theta_peer(self, P, row_b, col_b, rank, recv, peer_back):
+        """Theta stage storing the solved rows straight into every rank's
+        return buffer."""
+        rb, cb = self._bounds(P, row_b, col_b)
+        self._follow_torch(recv)
+        tab = (ctypes.c_void_p * P)(*[_ptr(b) for b in peer_back])
+        _lib.check(self.lib.sk_stage_theta_peer(self._h, P, rb, cb, rank, _ptr(recv), tab))
 
     def stage_lambda_inv(self, P, row_b, col_b, rank, back, u_rows):
         rb, cb = self._bounds(P, row_b, col_b)

@@ -104,3 +104,60 @@ def test_slab_bounds_cover():
         for P in (1, 2, 3, 8):
             b = slab_bounds(total, P)
             assert b[0] == 0 and b[-1] == total and all(b[i] <= b[i + 1] for i in range(P))
+
+
+# ------------------------------------------------------------ fused peer path
+def _p2p_worker(rank, world, port, M, N, L, q):
+    """One rank of the fused-transpose (CUDA IPC peer-store) slab solve.  On
+    the single-GPU test box both ranks share device 0: the peer mappings are
+    then same-device IPC mappings, the kernels are exactly those of a
+    multi-GPU run, and the ranks only meet at host barriers between stages
+    (no kernel waits on another rank)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1510_08094_b200 import inputs
+    from paper_1510_08094_b200.distributed import SlabSolver, gather_rows
+    from paper_1510_08094_b200.poisson import Plan
+    dev = torch.device("cuda", 0)
+    rows = M // 2 + 1
+    c = torch.from_numpy(inputs.sh_coeffs(11, L, 2.0)).to(dev)
+    with Plan(M, N) as plan:
+        f = torch.empty((rows, N), dtype=torch.float64, device=dev)
+        plan.shgen(L, c, f)
+        u1 = plan.solve_grid(f).cpu()
+    solver = SlabSolver(M, N, rank, world, device=dev, transport="p2p")
+    mine = f[solver.rb[rank]: solver.rb[rank + 1]].contiguous()
+    u = solver.solve(mine)
+    u = solver.solve(mine)  # second solve reuses the mapped buffers
+    torch.cuda.synchronize()
+    allu = gather_rows(u.cpu(), solver.rb)
+    solver.close()
+    if rank == 0:
+        q.put((allu.numpy(), u1.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,M,N,L", [(2, 512, 256, 40), (3, 240, 200, 30)])
+def test_p2p_fused_transposes_bitwise(world, M, N, L):
+    """The fused peer-store slab solve equals the single-GPU grid solve bit
+    for bit (the theta stage is slab-invariant)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, M, N, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, ref = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(got, ref)

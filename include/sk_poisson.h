@@ -61,10 +61,16 @@ typedef struct sk_plan_s* sk_plan_t;
 /* flags for data arguments */
 #define SK_HOST 0u     /* pointers are host memory (copies inside the call)   */
 #define SK_DEVICE 1u   /* pointers are device memory on the plan's device    */
-#define SK_ASYNC 2u    /* do not synchronise the plan stream before returning
-                          (device pointers only; errors that need a host-side
-                          check, e.g. the mean precondition, are then reported
-                          by the next sk_sync) */
+#define SK_ASYNC 2u    /* do not synchronise before returning.  Device
+                          pointers: work is queued on the plan stream.  Host
+                          pointers (sk_solve_grid): the solve is pipelined —
+                          H2D copy, transforms and D2H copy on three streams
+                          with two device slots, so consecutive calls overlap
+                          their copies with each other's compute; f and u must
+                          stay valid (and should be pinned) until sk_sync.
+                          Errors that need a host-side check, e.g. the mean
+                          precondition, are reported by a later call or by
+                          sk_sync */
 
 /* Create a plan for an M x N problem (M = doubled theta count, N = lambda
  * count, both even) with `nrhs` independent right-hand sides on CUDA device

@@ -297,6 +297,14 @@ struct sk_plan_s {
     int piv_stride = 0;        // doubles per pivot-table row
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
+    // pipelined host-memory solves (SK_HOST | SK_ASYNC)
+    bool pipe_ready = false;
+    double* pipe_buf[2] = {nullptr, nullptr};
+    double* pipe_stats[2] = {nullptr, nullptr};  // pinned
+    bool pipe_pending[2] = {false, false};
+    cudaEvent_t pipe_in[2] = {}, pipe_done[2] = {}, pipe_out[2] = {};
+    cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
+    int pipe_slot = 0;
     long long last_launches = 0;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -318,14 +326,11 @@ sk_status check_plan(sk_plan_t p) {
     return SK_OK;
 }
 
-sk_status check_precondition(sk_plan_t p, int nrhs) {
+sk_status precondition_from(const double* st, int nrhs) {
     // poisson.cpp:111-116: |2 pi w^T f0| > 1e-6 * 4 pi * max|F|
-    p->host_stats.resize(4 * nrhs);
-    CU(cudaMemcpyAsync(p->host_stats.data(), p->stats, sizeof(double) * 4 * nrhs, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
     const double fourpi = 12.566370614359172953850573533118;
     for (int r = 0; r < nrhs; ++r) {
-        const double* s = &p->host_stats[4 * r];
+        const double* s = &st[4 * r];
         if (s[3] >= double(1 << 20))
             return fail(SK_ERR_SINGULAR, "band_solve: matrix is numerically singular");
         const double fscale = s[2];
@@ -334,6 +339,40 @@ sk_status check_precondition(sk_plan_t p, int nrhs) {
         if (mean > 1e-6 * fourpi * fscale)
             return fail(SK_ERR_PRECONDITION, "poisson solve: right-hand side has a nonzero surface mean");
     }
+    return SK_OK;
+}
+
+sk_status check_precondition(sk_plan_t p, int nrhs) {
+    p->host_stats.resize(4 * nrhs);
+    CU(cudaMemcpyAsync(p->host_stats.data(), p->stats, sizeof(double) * 4 * nrhs, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    return precondition_from(p->host_stats.data(), nrhs);
+}
+
+// Host-memory solves with SK_ASYNC: two device slots, the H2D copy of a solve
+// on its own stream, the transforms on the plan stream, the D2H copy on a
+// third stream, so consecutive solves overlap their copies (both directions
+// of the link) with each other's compute.  The precondition of a solve is
+// evaluated when its slot comes round again or at sk_sync.
+sk_status pipe_check_slot(sk_plan_t p, int slot) {
+    if (!p->pipe_pending[slot]) return SK_OK;
+    p->pipe_pending[slot] = false;
+    CU(cudaEventSynchronize(p->pipe_done[slot]));
+    return precondition_from(p->pipe_stats[slot], p->nrhs);
+}
+
+sk_status pipe_init(sk_plan_t p, size_t ng) {
+    if (p->pipe_ready) return SK_OK;
+    for (int i = 0; i < 2; ++i) {
+        CU(cudaMalloc(&p->pipe_buf[i], sizeof(double) * ng));
+        CU(cudaMallocHost(&p->pipe_stats[i], sizeof(double) * 4 * p->nrhs));
+        CU(cudaEventCreateWithFlags(&p->pipe_in[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->pipe_done[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->pipe_out[i], cudaEventDisableTiming));
+    }
+    CU(cudaStreamCreateWithFlags(&p->pipe_h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&p->pipe_d2h, cudaStreamNonBlocking));
+    p->pipe_ready = true;
     return SK_OK;
 }
 
@@ -507,6 +546,20 @@ sk_status sk_plan_destroy(sk_plan_t p) {
         if (q) cudaFree(q);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
+    if (p->pipe_ready) {
+        cudaStreamSynchronize(p->pipe_h2d);
+        cudaStreamSynchronize(p->pipe_d2h);
+        cudaStreamSynchronize(p->stream);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(p->pipe_buf[i]);
+            cudaFreeHost(p->pipe_stats[i]);
+            cudaEventDestroy(p->pipe_in[i]);
+            cudaEventDestroy(p->pipe_done[i]);
+            cudaEventDestroy(p->pipe_out[i]);
+        }
+        cudaStreamDestroy(p->pipe_h2d);
+        cudaStreamDestroy(p->pipe_d2h);
+    }
     if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return SK_OK;
@@ -525,6 +578,14 @@ sk_status sk_sync(sk_plan_t p) {
     sk_status s = check_plan(p);
     if (s != SK_OK) return s;
     CU(cudaStreamSynchronize(p->stream));
+    if (p->pipe_ready) {
+        CU(cudaStreamSynchronize(p->pipe_h2d));
+        CU(cudaStreamSynchronize(p->pipe_d2h));
+        const sk_status a = pipe_check_slot(p, 0);
+        const sk_status b = pipe_check_slot(p, 1);
+        if (a != SK_OK) return a;
+        if (b != SK_OK) return b;
+    }
     return SK_OK;
 }
 
@@ -733,6 +794,33 @@ sk_status sk_solve_grid(sk_plan_t p, const double* f, double* u, double* X_half,
     if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
     if (!f || !u) return fail(SK_ERR_ARGUMENT, "null f or u");
     const size_t ng = static_cast<size_t>(p->nrhs) * p->g.rows * p->N;
+    if (!(flags & SK_DEVICE) && (flags & SK_ASYNC)) {
+        if (X_half) return fail(SK_ERR_ARGUMENT, "X_half is not available with asynchronous host-memory solves");
+        if ((s = pipe_init(p, ng)) != SK_OK) return s;
+        const int slot = p->pipe_slot;
+        p->pipe_slot ^= 1;
+        const sk_status prev = pipe_check_slot(p, slot);  // the solve that used this slot two calls ago
+        double* buf = p->pipe_buf[slot];
+        CU(cudaStreamWaitEvent(p->pipe_h2d, p->pipe_out[slot], 0));  // its result has left the slot
+        CU(cudaMemcpyAsync(buf, f, sizeof(double) * ng, cudaMemcpyHostToDevice, p->pipe_h2d));
+        CU(cudaEventRecord(p->pipe_in[slot], p->pipe_h2d));
+        CU(cudaStreamWaitEvent(p->stream, p->pipe_in[slot], 0));
+        CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4 * p->nrhs, p->stream));
+        sk::Slabs sl{};
+        sl.P = 1;
+        sl.row_b[1] = p->g.rows;
+        sl.col_b[1] = p->g.cols;
+        p->last_launches = 0;
+        if ((s = run_grid(p, sl, p->g.rows, p->g.cols, 0, buf, p->spec, buf, nullptr, 7)) != SK_OK) return s;
+        CU(cudaMemcpyAsync(p->pipe_stats[slot], p->stats, sizeof(double) * 4 * p->nrhs, cudaMemcpyDeviceToHost,
+                           p->stream));
+        CU(cudaEventRecord(p->pipe_done[slot], p->stream));
+        p->pipe_pending[slot] = true;
+        CU(cudaStreamWaitEvent(p->pipe_d2h, p->pipe_done[slot], 0));
+        CU(cudaMemcpyAsync(u, buf, sizeof(double) * ng, cudaMemcpyDeviceToHost, p->pipe_d2h));
+        CU(cudaEventRecord(p->pipe_out[slot], p->pipe_d2h));
+        return prev;
+    }
     const double* df;
     double* du;
     if (flags & SK_DEVICE) {

@@ -99,7 +99,12 @@ class Plan:
                 self.set_stream(sp)
 
     def sync(self) -> None:
-        _lib.check(self.lib.sk_sync(self._h))
+        """Wait for all queued work (including pipelined host solves, whose
+        deferred precondition errors are raised here)."""
+        try:
+            _lib.check(self.lib.sk_sync(self._h))
+        finally:
+            self._inflight = []
 
     def info(self) -> dict:
         a = (ctypes.c_longlong * 16)()
@@ -173,6 +178,9 @@ class Plan:
                 Xh = np.empty((self.nrhs, self.N // 2 + 1, self.M), np.complex128)
         self._follow_torch(f)
         flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
+        if not sync and not dev:
+            # pipelined host solve: the arrays must outlive the queued copies
+            self._inflight = (getattr(self, "_inflight", []) + [(f, u)])[-4:]
         _lib.check(self.lib.sk_solve_grid(self._h, _ptr(f), _ptr(u), _ptr(Xh), flags))
         if coeffs:
             if self.nrhs == 1:

@@ -281,3 +281,27 @@ def test_grid_full_size_analytic_C5(pkg):
         torch.cuda.synchronize()
         err = ((u - ue).abs().max() / ue.abs().max()).item()
     assert err <= 1e-10, err
+
+
+def test_pipelined_host_solves(pkg, oracle):
+    """SK_HOST | SK_ASYNC: consecutive host-memory solves overlap through two
+    device slots; each result equals the synchronous solve bit for bit, and a
+    nonzero-mean input is reported by a later call or by sync()."""
+    from paper_1510_08094_b200 import inputs
+    m, n, L = 256, 128, 20
+    fs = [oracle.shgen(m, n, L, inputs.sh_coeffs(40 + i, L, 2.0)) for i in range(5)]
+    with pkg.Plan(m, n) as plan:
+        ref = [plan.solve_grid(f) for f in fs]
+        outs = [np.empty_like(f) for f in fs]
+        for f, u in zip(fs, outs):
+            plan.solve_grid(f, u, sync=False)
+        plan.sync()
+        for a, b in zip(outs, ref):
+            assert np.array_equal(a, b)
+        bad = fs[0] + 1.0
+        ub = np.empty_like(bad)
+        with pytest.raises(pkg.precondition_error):
+            plan.solve_grid(bad, ub, sync=False)
+            plan.solve_grid(fs[1], np.empty_like(bad), sync=False)
+            plan.solve_grid(fs[2], np.empty_like(bad), sync=False)
+            plan.sync()

@@ -196,6 +196,44 @@ __device__ __forceinline__ Aff3 block_scan_aff_seg2(Aff3 v, Aff3* wsc) {
     return res;
 }
 
+// One-barrier variant: after the warp totals are published, every warp scans
+// them itself (lanes < nw) instead of waiting for warp 0, and there is no
+// trailing barrier — callers alternate two `slots` arrays (nw entries each)
+// between consecutive scans so that a fast warp's next publication cannot
+// overwrite totals a slow warp is still reading.  The barrier orders every
+// shared-memory access made before the call against those made after it.
+template <bool REV>
+__device__ __forceinline__ Aff3 block_scan_aff1(Aff3 v, Aff3* slots) {
+    const int tid = threadIdx.x;
+    const int nw = blockDim.x >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int vlane = REV ? 31 - lane : lane;
+    const int vwarp = REV ? nw - 1 - warp : warp;
+    Aff3 inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const Aff3 o = shfl_aff<!REV>(inc, off);
+        if (vlane >= off) inc = aff_combine(o, inc);
+    }
+    if (vlane == 31) slots[vwarp] = inc;
+    __syncthreads();
+    Aff3 t = lane < nw ? slots[lane] : aff_identity();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        if (off >= nw) break;
+        const Aff3 o = shfl_aff<true>(t, off);
+        if (lane >= off) t = aff_combine(o, t);
+    }
+    Aff3 pre;
+    pre.a = __shfl_sync(0xffffffffu, t.a, vwarp > 0 ? vwarp - 1 : 0);
+    pre.b = __shfl_sync(0xffffffffu, t.b, vwarp > 0 ? vwarp - 1 : 0);
+    pre.c = __shfl_sync(0xffffffffu, t.c, vwarp > 0 ? vwarp - 1 : 0);
+    if (vwarp == 0) pre = aff_identity();
+    Aff3 ex = shfl_aff<!REV>(inc, 1);
+    if (vlane == 0) ex = aff_identity();
+    return aff_combine(pre, ex);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);

@@ -223,7 +223,7 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
     const int n = ch.n;
     const int s = static_cast<int>((static_cast<long long>(tid) * n) / nthr);
     const int e = static_cast<int>((static_cast<long long>(tid + 1) * n) / nthr);
-    auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
+    auto pos = [&](int i) { return rev[ch.tau0 + ch.dtau * i]; };
     auto Fof = [&](double2 xm, double2 x0, double2 xp, int i) {
         const double d2 = chainD2(ch, i, L);
         return make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
@@ -323,6 +323,14 @@ __device__ void solve_chain(double2* a, const int* rev, const double* ip, V4* ws
 // (4A = t (t - 3s) + 2, 4C = t (t + 3s) + 2, s = sign dt); max |F|^2 is kept
 // on the high word of its IEEE pattern (relative resolution 2^-20 of the
 // squared value; it only scales the precondition threshold).
+// Affine-map scan of the V4-based walks through the one-barrier Aff3 scan
+// (slot set `set` of the 32-entry scratch).
+template <bool REV>
+__device__ __forceinline__ V4 scan_v4(V4 v, V4* wsc, int set = 0) {
+    const Aff3 r = block_scan_aff1<REV>(Aff3{v.a, v.b, v.c}, reinterpret_cast<Aff3*>(wsc) + set);
+    return V4{r.a, r.b, r.c, 0.0};
+}
+
 // Register-resident variant of solve_chain for segments of at most SMAX
 // elements per thread: every chain element is read from shared memory once
 // (its position through the digit-reversal table once), F, r' and the pivots
@@ -340,12 +348,12 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
     double ipv[SMAX];
 #pragma unroll
     for (int u = 0; u < SMAX; ++u)
-        if (u < m) pos[u] = __ldg(rev + ch.tau0 + ch.dtau * (s + u));
+        if (u < m) pos[u] = rev[ch.tau0 + ch.dtau * (s + u)];
     const double ip_before = (s > 0 && m > 0) ? ip[ch.tau0 + ch.dtau * (s - 1)] : 0.0;
     double2 xlo = make_double2(0.0, 0.0), xhi = make_double2(0.0, 0.0);
     if (m > 0) {
-        xlo = (s == 0) ? inner : a[__ldg(rev + ch.tau0 + ch.dtau * (s - 1))];
-        xhi = (e < n) ? a[__ldg(rev + ch.tau0 + ch.dtau * e)] : make_double2(0.0, 0.0);
+        xlo = (s == 0) ? inner : a[rev[ch.tau0 + ch.dtau * (s - 1)]];
+        xhi = (e < n) ? a[rev[ch.tau0 + ch.dtau * e]] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < SMAX; ++u) {
@@ -385,7 +393,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
         }
     }
     if (ch.dt > 0) SK_PROBE(14);
-    const V4 rin = block_exclusive_scan<AffOp, false>(aff, wsc);
+    const V4 rin = scan_v4<false>(aff, wsc);
     if (ch.dt > 0) SK_PROBE(15);
     // forward sweep: r' in registers
     {
@@ -413,7 +421,7 @@ __device__ void solve_chain_reg(double2* a, const int* rev, const double* ip, V4
         }
     }
     if (ch.dt > 0) SK_PROBE(17);
-    const V4 xin = block_exclusive_scan<AffOp, true>(baff, wsc);  // also orders every read above before the writes below
+    const V4 xin = scan_v4<true>(baff, wsc, 16);  // also orders every read above before the writes below
     if (ch.dt > 0) SK_PROBE(18);
     double2 ws = make_double2(0.0, 0.0);
     {
@@ -483,8 +491,8 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
         const double* ib = ip + tb;
 #pragma unroll
         for (int u = 0; u < S; u += 2) {
-            const unsigned p0 = __ldg(rb + D * u);
-            const unsigned p1 = (u + 1 < S) ? __ldg(rb + D * (u + 1)) : 0u;
+            const unsigned p0 = rb[D * u];
+            const unsigned p1 = (u + 1 < S) ? rb[D * (u + 1)] : 0u;
             pk[u / 2] = p0 | (p1 << 16);
         }
 #pragma unroll
@@ -497,10 +505,10 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
     double ip_before = 0.0;
     if (s > 0 && s <= n) {
         const int tb = ch.tau0 + ch.dtau * (s - 1);
-        xlo = a[__ldg(rev + tb)];
+        xlo = a[rev[tb]];
         ip_before = ip[tb];
     }
-    if (s + S < n) xhi = a[__ldg(rev + ch.tau0 + ch.dtau * (s + S))];
+    if (s + S < n) xhi = a[rev[ch.tau0 + ch.dtau * (s + S)]];
 #pragma unroll
     for (int u = 0; u < S; ++u) {
         const bool ok = s + u < n;
@@ -532,7 +540,7 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
         }
         *fmax_hi = max(*fmax_hi, fh);
     }
-    const Aff3 rin = block_scan_aff<false>(aff, wsc);  // also orders every X read above before the writes below
+    const Aff3 rin = block_scan_aff1<false>(aff, wsc);  // also orders every X read above before the writes below
 #pragma unroll
     for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
     // ---- pass 2
@@ -559,7 +567,7 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
         }
         baff = Aff3{Pm, G.x, G.y};
     }
-    const Aff3 xin = block_scan_aff<true>(baff, wsc);
+    const Aff3 xin = block_scan_aff1<true>(baff, wsc + 16);
     // ---- pass 3
 #pragma unroll
     for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
@@ -628,7 +636,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
     constexpr int U = 8;
     if (threadIdx.x == 0 && ch.n > 0) {
         const int n = ch.n;
-        auto pos = [&](int i) { return __ldg(rev + ch.tau0 + ch.dtau * i); };
+        auto pos = [&](int i) { return rev[ch.tau0 + ch.dtau * i]; };
         // ---- forward: r'_i = F_i + alpha_i r'_{i-1}
         int pc[U];
         double2 xc[U];
@@ -762,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     double2* misc = reinterpret_cast<double2*>(wsc + 32);
     double* red = reinterpret_cast<double*>(misc + 16);
     uint64_t* bars = reinterpret_cast<uint64_t*>(red + 64);
+    int* rw = reinterpret_cast<int*>(bars + 2);  // digit-reversal window (P.rev_win)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int par = static_cast<int>(cluster.block_rank());
@@ -795,7 +804,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
             const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
             if (r1 > r0) bytes += (r1 - r0) * 16;
         }
-        mbar_expect_tx(&bars[0], bytes + pb);
+        int ra0 = 0;
+        uint32_t rbytes = 0;
+        if (P.rev_win) rev_window(rw, cp.tau0, cp.tau0 + cp.n, ra0, rbytes);
+        mbar_expect_tx(&bars[0], bytes + pb + rbytes);
+        if (rbytes) bulk_g2s_chunked(rw, P.fd.rev + ra0, rbytes, &bars[0]);
         for (int s = 0; s < P.sl.P; ++s) {
             const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
             if (r1 > r0)
@@ -807,6 +820,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     uint32_t pb_unused = 0;
     const double* ipp = pivot_window(ip, P.pivots, prow, cp.tau0, cp.tau0 + cp.n, pb_unused);
+    const int* rev_p = rev;
+    if (P.rev_win) {
+        int ra0;
+        uint32_t rb;
+        rev_p = rev_window(rw, cp.tau0, cp.tau0 + cp.n, ra0, rb);
+    }
     mbar_wait(&bars[0], 0);
     __syncthreads();
 
@@ -912,7 +931,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     const bool seq = kg < P.kseq;
     unsigned fmax_hi = 0u;
     Aff3* wsc3 = reinterpret_cast<Aff3*>(wsc);
-    auto solve_side = [&](const Chain& ch, const double* ipc, double2 inner, double2* xf) {
+    auto solve_side = [&](const Chain& ch, const double* ipc, const int* rev, double2 inner, double2* xf) {
         const bool reg12 = ch.n <= kSegMax * nthr;
         if (seq) {
             solve_chain_seq(a, rev, ipc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
@@ -926,22 +945,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
             solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
         }
     };
-    solve_side(cp, ipp, inner_p, &misc[3]);
+    solve_side(cp, ipp, rev_p, inner_p, &misc[3]);
     SK_PROBE(4);
     // the t < 0 chain's pivots replace the t > 0 chain's in the window
     const double* ipm = ip;
+    const int* rev_m = rev;
     if (cm.n > 0) {
-        uint32_t pb = 0;
+        uint32_t pb = 0, rbytes = 0;
+        int ra0 = 0;
         ipm = pivot_window(ip, P.pivots, prow, L - cm.n, L, pb);
+        if (P.rev_win) rev_m = rev_window(rw, L - cm.n, L, ra0, rbytes);
         if (tid == 0) {
             fence_proxy_async();
-            mbar_expect_tx(&bars[1], pb);
+            mbar_expect_tx(&bars[1], pb + rbytes);
             bulk_g2s_chunked(ip, P.pivots + ((prow + L - cm.n) & ~static_cast<size_t>(1)), pb, &bars[1]);
+            if (rbytes) bulk_g2s_chunked(rw, P.fd.rev + ra0, rbytes, &bars[1]);
         }
         mbar_wait(&bars[1], 0);
     }
     SK_PROBE(5);
-    solve_side(cm, ipm, inner_m, &misc[4]);
+    solve_side(cm, ipm, rev_m, inner_m, &misc[4]);
     fmax_acc = fmax(fmax_acc, __hiloint2double(static_cast<int>(fmax_hi), 0));
     SK_PROBE(6);
     if (want_wsum) wsum = block_sum2(wsum, red);

@@ -41,6 +41,7 @@ struct ThetaParams {
     int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
     int piv_stride;        // doubles per (mode, parity) pivot row
     PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
+    int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
 };
 
 struct ShgenParams {
@@ -98,10 +99,12 @@ __host__ __device__ inline int theta_data_slots(int L) { return ((L + 1) + 7) & 
 __host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 4) + 1) & ~1; }
 
 // Dynamic shared memory of theta_kernel (bytes).
-__host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo) {
+// ints of the theta kernel's digit-reversal window (one chain's slots)
+__host__ __device__ inline int theta_rev_slots(int L) { return ((L / 2 + 9) + 3) & ~3; }
+__host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo, bool rev_win = false) {
     const size_t chain_max = static_cast<size_t>(theta_chain_slots(L));
     return static_cast<size_t>(theta_data_slots(L)) * 16 + static_cast<size_t>(nhi + nlo) * 16 + chain_max * 8 + 32 * 32 +
-           16 * 16 + 64 * 8 + 2 * 8;
+           16 * 16 + 64 * 8 + 2 * 8 + (rev_win ? static_cast<size_t>(theta_rev_slots(L)) * 4 : 0);
 }
 
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);

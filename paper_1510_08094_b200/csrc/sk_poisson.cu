@@ -297,6 +297,7 @@ struct sk_plan_s {
     int piv_stride = 0;        // doubles per pivot-table row
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
+    int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
     // pipelined host-memory solves (SK_HOST | SK_ASYNC)
     bool pipe_ready = false;
     double* pipe_buf[2] = {nullptr, nullptr};
@@ -457,6 +458,12 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     }
     if (p->grid_ok) {
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
+        // stage the chains' digit-reversal entries in shared memory when they fit
+        const size_t with_rev = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo, true);
+        if (Lt >= 4096 && with_rev <= cap && !std::getenv("SK_NO_REVWIN")) {  // small tables stay L1-resident
+            p->smem_theta = with_rev;
+            p->rev_win = 1;
+        }
         const bool fits = p->smem_theta <= cap && (Lt / 2 + 1) <= 12 * p->thr_theta;
         if (!fits) {
             const int Q = 4;
@@ -733,6 +740,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
         tp.regsolve = p->chain_mode;
+        tp.rev_win = p->theta_q ? 0 : p->rev_win;
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes
         tp.piv_stride = p->piv_stride;

@@ -108,4 +108,13 @@ __device__ __forceinline__ const double* pivot_window(double* dst, const double*
     return dst + (static_cast<long long>(row_abs) - static_cast<long long>(a0));
 }
 
+// Same for a chain's entries of the digit-reversal table (ints, windows
+// aligned to 16 bytes; the table is padded to a multiple of 4 entries).
+__device__ __forceinline__ const int* rev_window(int* dst, int tau_lo, int tau_hi, int& a0, uint32_t& bytes) {
+    a0 = tau_lo & ~3;
+    const int a1 = (tau_hi + 3) & ~3;
+    bytes = static_cast<uint32_t>(a1 - a0) * 4;
+    return dst - a0;
+}
+
 }  // namespace sk

@@ -484,8 +484,9 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         }
     }
     // lambda stages: one CTA per row, or a CTA pair splitting the row by parity
+    // (odd first span: the digit-reversed split/pack walks spread over all banks)
     p->thr_lambda = round_threads(Ll / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl)) != SK_OK) {
+    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, true)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }

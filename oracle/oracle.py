@@ -164,6 +164,16 @@ class Oracle(_Lib):
         self._call("integration_weights", _I(m), _ptr(w))
         return w
 
+    def assemble(self, d, col, row, vscale, m, n):
+        """assemble_poisson on raw low-rank factors -> (F, [removed?, mu.re, mu.im])."""
+        d, col, row = (np.ascontiguousarray(x, np.complex128) for x in (d, col, row))
+        K, mf, nf = d.shape[0], col.shape[1], row.shape[1]
+        F = np.zeros((m, n), np.complex128)
+        rep = np.zeros(3)
+        self._call("assemble", _I(K), _I(mf), _I(nf), _ptr(d), _ptr(col), _ptr(row), ctypes.c_double(vscale), _I(m),
+                   _I(n), _ptr(F), _ptr(rep))
+        return F, rep
+
     def dfs_double(self, phys, m):
         n = phys.shape[1]
         g = np.zeros((m, n), np.complex128)
@@ -245,6 +255,30 @@ class Reference(_Lib):
         mean = np.zeros(3)
         self._call("assemble_fn", _I(fn_id), _ptr(par), _I(0 if par is None else len(par)), _I(m), _I(n), _ptr(F),
                    _ptr(mean))
+        return F, mean
+
+    def construct_fn(self, fn_id, params):
+        """construct(f) of a test function -> (d[K], col[K, mf], row[K, nf], vscale)."""
+        par = np.ascontiguousarray(params, np.float64) if params is not None and len(params) else None
+        npar = _I(0 if par is None else len(par))
+        K, mf, nf = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        vs = ctypes.c_double()
+        self._call("construct_fn", _I(fn_id), _ptr(par), npar, ctypes.byref(K), ctypes.byref(mf), ctypes.byref(nf),
+                   None, None, None, ctypes.byref(vs))
+        d = np.zeros(K.value, np.complex128)
+        col = np.zeros((K.value, mf.value), np.complex128)
+        row = np.zeros((K.value, nf.value), np.complex128)
+        self._call("construct_fn", _I(fn_id), _ptr(par), npar, ctypes.byref(K), ctypes.byref(mf), ctypes.byref(nf),
+                   _ptr(d), _ptr(col), _ptr(row), ctypes.byref(vs))
+        return d, col, row, vs.value
+
+    def assemble_lowrank(self, d, col, row, vscale, m, n):
+        d, col, row = (np.ascontiguousarray(x, np.complex128) for x in (d, col, row))
+        K, mf, nf = d.shape[0], col.shape[1], row.shape[1]
+        F = np.zeros((m, n), np.complex128)
+        mean = np.zeros(3)
+        self._call("assemble_lowrank", _I(K), _I(mf), _I(nf), _ptr(d), _ptr(col), _ptr(row), ctypes.c_double(vscale),
+                   _I(m), _I(n), _ptr(F), _ptr(mean))
         return F, mean
 
     def sample_dfs_fn(self, fn_id, params, m, n):

@@ -402,6 +402,55 @@ int ref_assemble_fn(int fn_id, const double* par, int npar, int m, int n, double
     });
 }
 
+// construct(f) of a test function (lowrank.cpp:608-721), exported as raw
+// factors: d[K] complex, col[K][mf] complex, row[K][nf] complex, vscale.
+// Call with d == nullptr to query K, mf, nf.
+int ref_construct_fn(int fn_id, const double* par, int npar, int* K, int* mf, int* nf, double* d, double* col,
+                     double* row, double* vscale) {
+    return guarded([&] {
+        const LowRankSphereFun f = construct(test_fn(fn_id, par, npar));
+        *K = f.rank();
+        *mf = f.theta_modes();
+        *nf = f.lambda_modes();
+        if (!d) return;
+        for (int j = 0; j < f.rank(); ++j) {
+            std::memcpy(d + 2 * j, &f.d[j], sizeof(complex));
+            std::memcpy(col + 2 * static_cast<size_t>(j) * (*mf), f.col_coeffs[j].raw().data(), sizeof(complex) * (*mf));
+            std::memcpy(row + 2 * static_cast<size_t>(j) * (*nf), f.row_coeffs[j].raw().data(), sizeof(complex) * (*nf));
+        }
+        *vscale = f.vscale;
+    });
+}
+
+// assemble_poisson (poisson.cpp:52-86) of a low-rank function given by raw
+// factors (layout as ref_construct_fn).  out_mean[3] = {removed?, re, im}.
+int ref_assemble_lowrank(int K, int mf, int nf, const double* d, const double* col, const double* row, double vscale,
+                         int m, int n, double* F, double* out_mean) {
+    return guarded([&] {
+        LowRankSphereFun f;
+        for (int j = 0; j < K; ++j) {
+            complex dj;
+            std::memcpy(&dj, d + 2 * j, sizeof(complex));
+            f.d.push_back(dj);
+            std::vector<complex> c(mf), r(nf);
+            std::memcpy(c.data(), col + 2 * static_cast<size_t>(j) * mf, sizeof(complex) * mf);
+            std::memcpy(r.data(), row + 2 * static_cast<size_t>(j) * nf, sizeof(complex) * nf);
+            f.col_coeffs.emplace_back(std::move(c));
+            f.row_coeffs.emplace_back(std::move(r));
+            f.parity.push_back(Parity::even);
+        }
+        f.vscale = vscale;
+        AssembleReport rep;
+        const PoissonProblem pb = assemble_poisson(f, m, n, &rep);
+        from_matrix(pb.f, F);
+        if (out_mean) {
+            out_mean[0] = rep.mean_removed ? 1.0 : 0.0;
+            out_mean[1] = rep.removed_mean.real();
+            out_mean[2] = rep.removed_mean.imag();
+        }
+    });
+}
+
 // sample_dfs(f, m, n) of a test function (sphere_domain.cpp:46-52)
 int ref_sample_dfs_fn(int fn_id, const double* par, int npar, int m, int n, double* grid) {
     return guarded([&] {

@@ -653,6 +653,64 @@ int sko_dfs_double(int m, int n, const double* phys, double* grid) {
     });
 }
 
+// assemble_poisson (poisson.cpp:52-86) of a low-rank function given by its
+// factors f = sum_j d_j a_j(theta) b_j(lambda): F = sum_j (d_j Msin^2 pad(a_j, m))
+// pad(b_j, n)^T accumulated term by term (ascending j, zero da skipped as
+// :66 does), then the mean test with sum2 (calculus.cpp:89-103) and the
+// removal of mu * coeffs(sin^2 theta) (:76-82).  rep[3] = {removed?, re, im}.
+int sko_assemble(int K, int mf, int nf, const double* dd, const double* col, const double* row, double vscale, int m,
+                 int n, double* Fd, double* rep) {
+    return guarded([&] {
+        if (m % 2 != 0 || n % 2 != 0 || m <= 0 || n <= 0)
+            throw size_err("assemble_poisson: sizes must be positive and even");
+        if (mf % 2 != 0 || nf % 2 != 0 || mf < 0 || nf < 0) throw size_err("CoeffVec: length must be even");
+        const cplx* d = as_c(dd);
+        cplx* F = as_c(Fd);
+        std::fill(F, F + static_cast<size_t>(m) * n, cplx{});
+        // pad_to (fourier.cpp:105-112): mode k of a length-L vector sits at k + L/2
+        auto pad = [](const cplx* c, int len, int L) {
+            std::vector<cplx> out(L);
+            const int lo = std::max(-len / 2, -L / 2), hi = std::min(len / 2, L / 2);
+            for (int k = lo; k < hi; ++k) out[k + L / 2] = c[k + len / 2];
+            return out;
+        };
+        const Band S = msin2_band(m);
+        for (int j = 0; j < K; ++j) {
+            const std::vector<cplx> a = pad(as_c(col) + static_cast<size_t>(j) * mf, mf, m);
+            const std::vector<cplx> b = pad(as_c(row) + static_cast<size_t>(j) * nf, nf, n);
+            const std::vector<cplx> sa = S.apply(a.data());
+            for (int i = 0; i < m; ++i) {
+                const cplx da = d[j] * sa[i];
+                if (da == cplx{}) continue;
+                for (int k = 0; k < n; ++k) F[static_cast<size_t>(i) * n + k] += da * b[k];
+            }
+        }
+        // sum2: per term (sum_k w_k a_k)(2 pi b_0), even k only, ascending k
+        cplx total{};
+        for (int j = 0; j < K; ++j) {
+            const cplx* a = as_c(col) + static_cast<size_t>(j) * mf;
+            cplx ci{};
+            for (int k = -mf / 2; k < mf / 2; ++k) {
+                if (k % 2 != 0) continue;
+                ci += 2.0 / (1.0 - static_cast<double>(k) * k) * a[k + mf / 2];
+            }
+            const cplx b0 = nf > 0 ? as_c(row)[static_cast<size_t>(j) * nf + nf / 2] : cplx{};
+            total += d[j] * ci * (kTwoPi * b0);
+        }
+        const cplx mu = total / (4.0 * kPi);
+        rep[0] = 0.0;
+        rep[1] = rep[2] = 0.0;
+        if (std::abs(mu) > 1e-11 * std::max(vscale, 1e-300)) {
+            rep[0] = 1.0;
+            rep[1] = mu.real();
+            rep[2] = mu.imag();
+            F[static_cast<size_t>(m / 2) * n + n / 2] -= mu * 0.5;
+            if (m / 2 + 2 < m) F[static_cast<size_t>(m / 2 + 2) * n + n / 2] -= mu * -0.25;
+            F[static_cast<size_t>(m / 2 - 2) * n + n / 2] -= mu * -0.25;
+        }
+    });
+}
+
 int sko_grid_pipeline(int m, int n, const double* phys, double* Xout, double* u_doubled, double* u_phys,
                       int threads, double* mean_out) {
     return guarded([&] {

@@ -53,6 +53,11 @@ int sko_sample_grid(int rows, int cols, const double* X, int m_out, int n_out, d
 // sphere_domain.cpp:19-26, :46-52 applied to physical samples (index map a3)
 int sko_dfs_double(int m, int n, const double* phys, double* grid);
 
+// poisson.cpp:52-86 on raw low-rank factors: d[K], col[K][mf], row[K][nf]
+// (complex); F (m x n complex); rep[3] = {mean removed?, mu re, mu im}
+int sko_assemble(int K, int mf, int nf, const double* d, const double* col, const double* row, double vscale, int m,
+                 int n, double* F, double* rep);
+
 // doubling -> analyze_2d -> Msin^2 -> solve -> sample_grid.
 // X (M x N complex) and u_doubled (M x N complex) may be NULL.
 // u_phys ((M/2+1) x N real) = Re(u_doubled) on physical rows (p < M/2 from

@@ -30,10 +30,13 @@ def save(name, **arrays):
     print("wrote", path, {k: v.shape for k, v in arrays.items()})
 
 
-def main():
+def main(only=None):
     build(ref=True)
     R = Reference()
     O = Oracle()
+    if only:
+        {"lowrank": lowrank_fixtures, "transforms": transform_fixtures}[only](R)
+        return
 
     # test_poisson.cpp:53-67 — l = 1 eigenfunction cos(theta), 64 x 64
     F, mean = R.assemble_fn(0, None, 64, 64)
@@ -104,6 +107,43 @@ def main():
     save("fourier_pure_modes_16", const=R.analyze_1d(np.ones(16, complex)),
          e3=R.analyze_1d(np.exp(3j * xs)), cos=R.analyze_1d(np.cos(xs) + 0j))
 
+    lowrank_fixtures(R)
+    transform_fixtures(R)
+
+
+def lowrank_fixtures(R):
+    """assemble_poisson (poisson.cpp:52-86) on the low-rank factors that the
+    reference's construct() (lowrank.cpp:608-721) produces for the test
+    functions; sizes that truncate (m < theta modes) and pad."""
+    cases = [("cos_theta", 0, None, [(64, 64)]),
+             ("one_plus_cos", 1, None, [(32, 32), (16, 24)]),              # mean removal (test_poisson.cpp:186-206)
+             ("ylm_pair", 2, np.array([3, -2, 1.0, 5, 1, 0.5]), [(64, 48)]),
+             ("sin50xyz", 3, None, [(150, 150), (512, 384)]),             # K = 12, 256 modes: truncate / pad
+             ("sinsin_cos2", 4, None, [(32, 64)])]                        # nonzero mean
+    for name, fid, par, sizes in cases:
+        d, col, row, vscale = R.construct_fn(fid, par)
+        for m, n in sizes:
+            F, rep = R.assemble_lowrank(d, col, row, vscale, m, n)
+            save(f"assemble_{name}_{m}x{n}", d=d, col=col, row=row, vscale=np.array(vscale), F=F, rep=rep)
+
+
+def transform_fixtures(R):
+    """analyze_2d / sample_grid (fourier.cpp:170-209) on seeded complex grids,
+    with sample_grid zero-padding and truncating, and the DFS doubling of
+    physical samples (sphere_domain.cpp:19-26, :46-52)."""
+    rng = np.random.default_rng(1510)
+    for m, n, outs in [(16, 24, [(16, 24), (32, 40), (8, 12)]), (150, 150, [(150, 150), (96, 200)]),
+                       (64, 48, [(64, 48), (70, 42)])]:
+        g = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+        X = R.analyze_2d(g)
+        arrs = {"grid": g, "X": X}
+        for mo, no in outs:
+            arrs[f"S_{mo}x{no}"] = R.sample_grid(X, mo, no)
+        save(f"transforms_{m}x{n}", **arrs)
+    for m, n in [(8, 6), (20, 16)]:
+        phys = rng.standard_normal((m // 2 + 1, n))
+        save(f"dfs_double_{m}x{n}", phys=phys, grid=R.sample_dfs_phys(phys, m))
+
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

@@ -105,3 +105,46 @@ def test_oracle_vs_reference_dfs_and_fft(oracle, reference):
         assert np.array_equal(oracle.analyze_2d(g), reference.analyze_2d(g))
         X = reference.analyze_2d(g)
         assert np.array_equal(oracle.sample_grid(X, m, n), reference.sample_grid(X, m, n))
+
+
+def _names(prefix):
+    return [os.path.basename(f)[:-4] for f in sorted(glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))]
+
+
+@pytest.mark.parametrize("name", _names("assemble_"))
+def test_oracle_assemble_bit_identical_to_reference_golden(oracle, name):
+    # assemble_poisson (poisson.cpp:52-86) on the reference's own construct() factors
+    d = golden(name)
+    m, n = d["F"].shape
+    F, rep = oracle.assemble(d["d"], d["col"], d["row"], float(d["vscale"]), m, n)
+    assert np.array_equal(F, d["F"]) and np.array_equal(rep, d["rep"])
+
+
+def test_oracle_assemble_vs_reference_random_factors(oracle, reference):
+    rng = np.random.default_rng(77)
+    for K, mf, nf, m, n in [(3, 10, 8, 16, 12), (5, 40, 30, 24, 64), (1, 2, 2, 8, 8)]:
+        c = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
+        d, col, row = c(K), c(K, mf), c(K, nf)
+        for vs in (0.0, 1e30):  # mean removed / kept
+            F1, r1 = oracle.assemble(d, col, row, vs, m, n)
+            F2, r2 = reference.assemble_lowrank(d, col, row, vs, m, n)
+            assert np.array_equal(F1, F2) and np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("name", _names("transforms_"))
+def test_oracle_transforms_match_reference_golden(oracle, name):
+    # analyze_2d / sample_grid with zero-pad / truncation (fourier.cpp:55-66, :170-209)
+    d = golden(name)
+    X = oracle.analyze_2d(d["grid"])
+    assert np.abs(X - d["X"]).max() <= 1e-15 * np.abs(d["X"]).max()
+    for k in d.files:
+        if k.startswith("S_"):
+            mo, no = map(int, k[2:].split("x"))
+            S = oracle.sample_grid(d["X"], mo, no)
+            assert np.abs(S - d[k]).max() <= 1e-13 * np.abs(d[k]).max()
+
+
+@pytest.mark.parametrize("name", _names("dfs_double_"))
+def test_oracle_dfs_double_golden(oracle, name):
+    d = golden(name)
+    assert np.array_equal(oracle.dfs_double(d["phys"], d["grid"].shape[0]), d["grid"])

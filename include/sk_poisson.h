@@ -9,6 +9,15 @@
  *       poisson.hpp:47, poisson.cpp:121-161
  *   ResidualReport residual(const PoissonProblem&,       sk_residual
  *       const PoissonSolution&)  poisson.hpp:54, .cpp:163-186
+ *   PoissonProblem assemble_poisson(const              sk_assemble
+ *       LowRankSphereFun&, int m, int n, AssembleReport*)
+ *       poisson.hpp:40-41, poisson.cpp:52-86
+ *   Matrix analyze_2d(const BMCGrid&)                    sk_analyze_2d
+ *       fourier.hpp:107, fourier.cpp:170-188
+ *   BMCGrid sample_grid(const CoeffMatrix&, int, int)     sk_sample_grid
+ *       fourier.hpp:108, fourier.cpp:190-209
+ *   BMCGrid sample_dfs(const sphere_fn&, int, int)        sk_sample_dfs (of samples)
+ *       sphere_domain.hpp:61, sphere_domain.cpp:46-52
  *   sample_dfs -> analyze_2d -> Msin^2 -> solve ->       sk_solve_grid
  *       sample_grid (the grid-level composition:
  *       sphere_domain.cpp:46-52, fourier.cpp:170-209,
@@ -110,6 +119,39 @@ sk_status sk_solve_grid(sk_plan_t plan, const double* f, double* u, double* X_ha
 /* Surface mean 2 pi w^T f~_0 of the last grid solve's right-hand side and
  * max|F| of its coefficients (for callers that want the precondition data). */
 sk_status sk_last_mean(sk_plan_t plan, double out[3]);
+
+/* assemble_poisson (poisson.hpp:40-41, poisson.cpp:52-86): the plan's M x N
+ * coefficient matrix F of sin^2(theta) f~ for a low-rank function
+ * f~ = sum_j d_j a_j(theta) b_j(lambda) given by its factors (the fields of
+ * LowRankSphereFun, lowrank.hpp:47-59): d[K] complex, col[K][mf] complex
+ * (theta coefficients, mode t at index t + mf/2), row[K][nf] complex, vscale.
+ * Factors are zero-padded / truncated to M and N as pad_to does
+ * (fourier.cpp:105-112).  If the surface mean mu = sum2(f)/(4 pi) exceeds
+ * 1e-11 max(vscale, 1e-300) its sin^2 coefficients are subtracted, as the
+ * reference does; report[3] (host, may be NULL) = {removed (0/1), mu re,
+ * mu im} (AssembleReport).  F is bit-identical to the reference.  Flags:
+ * SK_HOST / SK_DEVICE for d, col, row and F together.  Needs M >= 4. */
+sk_status sk_assemble(sk_plan_t plan, int K, int mf, int nf, const double* d, const double* col, const double* row,
+                      double vscale, double* F, double report[3], unsigned flags);
+
+/* Standalone transforms of the reference's Fourier layer on complex data of
+ * any even size (the plan supplies device, stream and scratch; its own M, N
+ * are not used).  Transform lengths must factor into 2, 3, 5, 7 and fit one
+ * CTA (<= ~12000), else SK_ERR_UNSUPPORTED.  Layouts: row-major complex.
+ *   sk_analyze_2d   analyze_2d(BMCGrid) (fourier.hpp:107, fourier.cpp:170-188):
+ *                   m x n doubled sample grid -> m x n coefficients X.
+ *   sk_sample_grid  sample_grid(X, m_out, n_out) (fourier.hpp:108,
+ *                   fourier.cpp:190-209): rows x cols coefficients ->
+ *                   m_out x n_out grid, zero-padding or truncating the modes
+ *                   as synthesize_1d does (:55-66).
+ *   sk_sample_dfs   sample_dfs (sphere_domain.hpp:61, sphere_domain.cpp:19-26,
+ *                   :46-52) of physical samples ((m/2+1) x n real, rows
+ *                   theta_p = 2 pi p/m) -> the m x n doubled grid (complex,
+ *                   imaginary parts 0): the glide-reflection index map. */
+sk_status sk_analyze_2d(sk_plan_t plan, int m, int n, const double* grid, double* X, unsigned flags);
+sk_status sk_sample_grid(sk_plan_t plan, int rows, int cols, const double* X, int m_out, int n_out, double* grid,
+                         unsigned flags);
+sk_status sk_sample_dfs(sk_plan_t plan, int m, int n, const double* phys, double* grid, unsigned flags);
 
 /* Seeded spherical-harmonic input generator (untimed helper):
  * phys = sum_{l=1..L} sum_{|m|<=l} coeffs[l*l+l+m] Y_l^m on the plan's

@@ -5,7 +5,8 @@ include/sk_poisson.h); this package is the host-side mirror of the
 reference's spherekit Poisson interface (poisson.hpp) on top of it.
 """
 from .poisson import (  # noqa: F401
-    BenchRow, DeviceError, Plan, PoissonProblem, PoissonSolution, ResidualReport, UnsupportedError, bench_poisson,
-    integration_weights, precondition_error, residual, size_error, solve, solve_grid, structure_error)
+    AssembleReport, BenchRow, DeviceError, LowRankSphereFun, Plan, PoissonProblem, PoissonSolution, ResidualReport,
+    UnsupportedError, analyze_2d, assemble_poisson, bench_poisson, integration_weights, precondition_error, residual,
+    sample_dfs, sample_grid, size_error, solve, solve_grid, structure_error)
 
 __version__ = "0.1.0"

@@ -31,7 +31,7 @@ EXPORTS = [
     "sk_solve_grid", "sk_last_mean", "sk_shgen", "sk_stage_lambda_fwd", "sk_stage_theta", "sk_stage_lambda_inv",
     "sk_plan_info", "sk_stage_times", "sk_enable_stage_timing", "sk_last_error", "sk_version",
     "sk_stage_lambda_fwd_peer", "sk_stage_theta_peer", "sk_device_alloc", "sk_device_free", "sk_ipc_handle",
-    "sk_ipc_open", "sk_ipc_close",
+    "sk_ipc_open", "sk_ipc_close", "sk_assemble", "sk_analyze_2d", "sk_sample_grid", "sk_sample_dfs",
 ]
 
 
@@ -107,6 +107,10 @@ def load() -> ctypes.CDLL:
         "sk_ipc_handle": (I, [P, ctypes.c_char_p]),
         "sk_ipc_open": (I, [I, ctypes.c_char_p, ctypes.POINTER(P)]),
         "sk_ipc_close": (I, [P]),
+        "sk_assemble": (I, [P, I, I, I, P, P, P, ctypes.c_double, P, D, U]),
+        "sk_analyze_2d": (I, [P, I, I, P, P, U]),
+        "sk_sample_grid": (I, [P, I, I, P, I, I, P, U]),
+        "sk_sample_dfs": (I, [P, I, I, P, P, U]),
         "sk_last_error": (ctypes.c_char_p, []),
         "sk_version": (ctypes.c_char_p, []),
     }

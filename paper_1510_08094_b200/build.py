@@ -17,12 +17,14 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", f"-I{INCLUDE}"]
-# coeff_kernels.cu reproduces the reference's IEEE operation order: no FMA
-# contraction anywhere in that translation unit.
+# coeff_kernels.cu and assemble_kernels.cu reproduce the reference's IEEE operation order: no FMA
+# contraction anywhere in those translation units.
 UNITS = [
     ("grid_kernels.cu", []),
     ("grid_large.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
+    ("assemble_kernels.cu", ["--fmad=false"]),
+    ("transforms.cu", []),
     ("sk_poisson.cu", []),
 ]
 HEADERS = ["sk_internal.h", "params.h", "fft_dev.cuh", "block_ops.cuh", "tma.cuh", "theta_common.cuh"]

@@ -44,6 +44,28 @@ struct ThetaParams {
     int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
 };
 
+struct AssembleParams {
+    int M, N;              // output F: M x N complex
+    int K, mf, nf;         // rank, theta / lambda coefficient counts of the factors
+    const double2* d;      // K
+    const double2* col;    // K x mf
+    const double2* row;    // K x nf
+    double vscale;
+    double2* sa;           // scratch K x M: d_j Msin^2 pad(a_j)
+    double2* bp;           // scratch K x N: pad(b_j)
+    double2* F;            // M x N
+    double* report;        // device [3]: removed?, mu re, mu im
+};
+
+struct XformParams {
+    FftDesc fd;            // transform length n (analyze) or n_out (synthesize)
+    int n_in;              // synthesize: coefficients per input row
+    long long ld_in;       // complex per input row
+    long long ld_out;      // complex between consecutive outputs of one row (transposed store)
+    const double2* src;
+    double2* dst;
+};
+
 struct ShgenParams {
     GridGeom g;
     int L;                 // max degree
@@ -116,6 +138,10 @@ inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
 }
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
+cudaError_t launch_assemble(const AssembleParams& P, cudaStream_t st);
+size_t xform_smem_bytes(int n, int nhi, int nlo);
+cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st);
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);

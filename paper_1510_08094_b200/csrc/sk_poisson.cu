@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -311,6 +312,10 @@ struct sk_plan_s {
     cudaEvent_t ev[8] = {};
     double times[4] = {0, 0, 0, 0};
     std::vector<double> host_stats;
+    // standalone transforms / assemble: FFT plans per length, growable scratch
+    std::map<int, DevFft> xf;
+    void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t scratch_bytes[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -554,6 +559,9 @@ sk_status sk_plan_destroy(sk_plan_t p) {
         if (q) cudaFree(q);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& kv : p->xf) free_fft(kv.second);
+    for (void* q : p->scratch)
+        if (q) cudaFree(q);
     if (p->pipe_ready) {
         cudaStreamSynchronize(p->pipe_h2d);
         cudaStreamSynchronize(p->pipe_d2h);
@@ -913,6 +921,180 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
         CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
     }
     CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+// ------------------------------------------------ assemble / transforms
+namespace {
+
+sk_status scratch(sk_plan_t p, int slot, size_t bytes, void** out) {
+    if (p->scratch_bytes[slot] < bytes) {
+        if (p->scratch[slot]) {
+            CU(cudaStreamSynchronize(p->stream));
+            CU(cudaFree(p->scratch[slot]));
+            p->scratch[slot] = nullptr;
+            p->scratch_bytes[slot] = 0;
+        }
+        CU(cudaMalloc(&p->scratch[slot], bytes < 256 ? 256 : bytes));
+        p->scratch_bytes[slot] = bytes < 256 ? 256 : bytes;
+    }
+    *out = p->scratch[slot];
+    return SK_OK;
+}
+
+// Input staging: device pointers pass through; host data is copied into
+// scratch slot `slot`.
+sk_status stage_in(sk_plan_t p, const void* src, size_t bytes, unsigned flags, int slot, const void** out) {
+    if (flags & SK_DEVICE) {
+        *out = src;
+        return SK_OK;
+    }
+    void* d = nullptr;
+    sk_status s = scratch(p, slot, bytes, &d);
+    if (s != SK_OK) return s;
+    if (bytes) CU(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, p->stream));
+    *out = d;
+    return SK_OK;
+}
+
+int xform_threads(int n) { return round_threads(n / 8, 64, 512); }
+
+// FFT plan of length n for the standalone transforms (cached per plan).
+sk_status xform_fft(sk_plan_t p, int n, const DevFft** out) {
+    auto it = p->xf.find(n);
+    if (it == p->xf.end()) {
+        DevFft f;
+        sk_status s = build_fft(n, xform_threads(n), f);
+        if (s != SK_OK) return s;
+        if (sk::xform_smem_bytes(n, f.d.nhi, f.d.nlo) > 227 * 1024) {
+            free_fft(f);
+            return fail(SK_ERR_UNSUPPORTED, "transform length " + std::to_string(n) + " exceeds one CTA's shared memory");
+        }
+        it = p->xf.emplace(n, f).first;
+    }
+    *out = &it->second;
+    return SK_OK;
+}
+
+// One pass: nrows sequences of the input (row stride ld_in) -> transform of
+// length n -> transposed store (output stride ld_out).
+sk_status xform_pass(sk_plan_t p, bool analyze, int nrows, int n, int n_in, long long ld_in, const double2* src,
+                     long long ld_out, double2* dst) {
+    const DevFft* f = nullptr;
+    sk_status s = xform_fft(p, n, &f);
+    if (s != SK_OK) return s;
+    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst};
+    CU(sk::launch_xform(xp, analyze, nrows, xform_threads(n), sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo), p->stream));
+    return SK_OK;
+}
+
+}  // namespace
+
+sk_status sk_assemble(sk_plan_t p, int K, int mf, int nf, const double* d, const double* col, const double* row,
+                      double vscale, double* F, double report[3], unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (K < 0 || mf < 0 || nf < 0 || mf % 2 || nf % 2) return fail(SK_ERR_SIZE, "CoeffVec: length must be even");
+    if (!F || (K > 0 && (!d || (mf > 0 && !col) || (nf > 0 && !row)))) return fail(SK_ERR_ARGUMENT, "null argument");
+    if (p->M < 4) return fail(SK_ERR_UNSUPPORTED, "assemble_poisson needs m >= 4");
+    const int M = p->M, N = p->N;
+    const double2 *dd = nullptr, *dc = nullptr, *dr = nullptr;
+    if ((s = stage_in(p, d, sizeof(double2) * K, flags, 0, reinterpret_cast<const void**>(&dd))) != SK_OK) return s;
+    if ((s = stage_in(p, col, sizeof(double2) * K * static_cast<size_t>(mf), flags, 1,
+                      reinterpret_cast<const void**>(&dc))) != SK_OK)
+        return s;
+    if ((s = stage_in(p, row, sizeof(double2) * K * static_cast<size_t>(nf), flags, 2,
+                      reinterpret_cast<const void**>(&dr))) != SK_OK)
+        return s;
+    // scratch slot 3: [report(4 doubles)] [SA: K x M] [B: K x N] [F staging: M x N if host]
+    const size_t nsa = static_cast<size_t>(K) * M, nb = static_cast<size_t>(K) * N, nfm = static_cast<size_t>(M) * N;
+    void* w = nullptr;
+    if ((s = scratch(p, 3, 32 + sizeof(double2) * (nsa + nb + ((flags & SK_DEVICE) ? 0 : nfm)), &w)) != SK_OK) return s;
+    double* rep = static_cast<double*>(w);
+    double2* sa = reinterpret_cast<double2*>(static_cast<char*>(w) + 32);
+    double2* bp = sa + nsa;
+    double2* dF = (flags & SK_DEVICE) ? reinterpret_cast<double2*>(F) : bp + nb;
+    sk::AssembleParams ap{M, N, K, mf, nf, dd, dc, dr, vscale, sa, bp, dF, rep};
+    CU(sk::launch_assemble(ap, p->stream));
+    p->last_launches = K > 0 ? 3 : 2;
+    double h[3];
+    CU(cudaMemcpyAsync(h, rep, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(F, dF, sizeof(double2) * nfm, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    if (report) {
+        report[0] = h[0];
+        report[1] = h[1];
+        report[2] = h[2];
+    }
+    return SK_OK;
+}
+
+sk_status sk_analyze_2d(sk_plan_t p, int m, int n, const double* grid, double* X, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (m <= 0 || n <= 0 || m % 2 || n % 2) return fail(SK_ERR_SIZE, "analyze_1d: sample count must be even");
+    if (!grid || !X) return fail(SK_ERR_ARGUMENT, "null argument");
+    const size_t mn = static_cast<size_t>(m) * n;
+    const double2* g = nullptr;
+    if ((s = stage_in(p, grid, sizeof(double2) * mn, flags, 0, reinterpret_cast<const void**>(&g))) != SK_OK) return s;
+    void* t = nullptr;
+    if ((s = scratch(p, 1, sizeof(double2) * mn * ((flags & SK_DEVICE) ? 1 : 2), &t)) != SK_OK) return s;
+    double2* T = static_cast<double2*>(t);  // lambda-analysed rows, transposed: n x m
+    double2* out = (flags & SK_DEVICE) ? reinterpret_cast<double2*>(X) : T + mn;
+    if ((s = xform_pass(p, true, m, n, n, n, g, m, T)) != SK_OK) return s;    // rows j: lambda direction
+    if ((s = xform_pass(p, true, n, m, m, m, T, n, out)) != SK_OK) return s;  // columns kc: theta direction
+    p->last_launches = 2;
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(X, out, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
+    if (!(flags & SK_ASYNC) || !(flags & SK_DEVICE)) CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+sk_status sk_sample_grid(sk_plan_t p, int rows, int cols, const double* X, int m_out, int n_out, double* grid,
+                         unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (m_out <= 0 || n_out <= 0 || m_out % 2 || n_out % 2)
+        return fail(SK_ERR_SIZE, "sample_grid: output sizes must be even");
+    if (rows < 0 || cols < 0 || rows % 2 || cols % 2) return fail(SK_ERR_SIZE, "CoeffVec: length must be even");
+    if (!grid || (rows * cols > 0 && !X)) return fail(SK_ERR_ARGUMENT, "null argument");
+    const size_t nx = static_cast<size_t>(rows) * cols, ng = static_cast<size_t>(m_out) * n_out;
+    const double2* x = nullptr;
+    if ((s = stage_in(p, X, sizeof(double2) * nx, flags, 0, reinterpret_cast<const void**>(&x))) != SK_OK) return s;
+    const size_t nt = static_cast<size_t>(rows) * n_out;
+    void* t = nullptr;
+    if ((s = scratch(p, 1, sizeof(double2) * (nt + ((flags & SK_DEVICE) ? 0 : ng)), &t)) != SK_OK) return s;
+    double2* T = static_cast<double2*>(t);  // lambda-synthesised rows, transposed: n_out x rows
+    double2* out = (flags & SK_DEVICE) ? reinterpret_cast<double2*>(grid) : T + nt;
+    if (rows == 0) {
+        CU(cudaMemsetAsync(out, 0, sizeof(double2) * ng, p->stream));
+    } else {
+        if ((s = xform_pass(p, false, rows, n_out, cols, cols, x, rows, T)) != SK_OK) return s;      // lambda
+        if ((s = xform_pass(p, false, n_out, m_out, rows, rows, T, n_out, out)) != SK_OK) return s;  // theta
+    }
+    p->last_launches = 2;
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(grid, out, sizeof(double2) * ng, cudaMemcpyDeviceToHost, p->stream));
+    if (!(flags & SK_ASYNC) || !(flags & SK_DEVICE)) CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+sk_status sk_sample_dfs(sk_plan_t p, int m, int n, const double* phys, double* grid, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (m <= 0 || n <= 0 || m % 2 || n % 2) return fail(SK_ERR_SIZE, "BMCGrid: sample counts must be positive and even");
+    if (!phys || !grid) return fail(SK_ERR_ARGUMENT, "null argument");
+    const size_t np = static_cast<size_t>(m / 2 + 1) * n, ng = static_cast<size_t>(m) * n;
+    const double* ph = nullptr;
+    if ((s = stage_in(p, phys, sizeof(double) * np, flags, 0, reinterpret_cast<const void**>(&ph))) != SK_OK) return s;
+    double2* out = reinterpret_cast<double2*>(grid);
+    if (!(flags & SK_DEVICE)) {
+        void* t = nullptr;
+        if ((s = scratch(p, 1, sizeof(double2) * ng, &t)) != SK_OK) return s;
+        out = static_cast<double2*>(t);
+    }
+    CU(sk::launch_dfs_double(m, n, ph, out, p->stream));
+    p->last_launches = 1;
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(grid, out, sizeof(double2) * ng, cudaMemcpyDeviceToHost, p->stream));
+    if (!(flags & SK_ASYNC) || !(flags & SK_DEVICE)) CU(cudaStreamSynchronize(p->stream));
     return SK_OK;
 }
 

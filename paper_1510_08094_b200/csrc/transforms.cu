@@ -1,0 +1,104 @@
+// Standalone coefficient <-> grid transforms of the reference's Fourier layer
+// (fourier.hpp:107-108, sphere_domain.hpp:61), on complex data of any even
+// size whose transform lengths factor into 2, 3, 5, 7 and fit one CTA:
+//
+//   analyze_2d(BMCGrid)      fourier.cpp:170-188  -> two xform_kernel<ANALYZE> passes
+//   sample_grid(X, m, n)     fourier.cpp:190-209  -> two xform_kernel<SYNTH> passes
+//                            (zero-pads or truncates as synthesize_1d, :55-66)
+//   sample_dfs of samples    sphere_domain.cpp:19-26, :46-52 -> dfs_double_kernel
+//
+// One CTA per sequence: the row (contiguous in HBM) is loaded coalesced,
+// transformed in shared memory by the same mixed-radix engine as the solve
+// (fft_dev.cuh), and written TRANSPOSED, so the second pass again reads
+// contiguous rows and both 1D directions run on coalesced loads; the 2D
+// transform is separable, so doing the lambda direction first (the reference
+// does theta first) changes only rounding.  Per pass each element is read once
+// and written once: 32 bytes per complex entry, HBM-bound.
+#include <cuda_runtime.h>
+
+#include "fft_dev.cuh"
+#include "params.h"
+#include "sk_internal.h"
+
+namespace sk {
+
+// ANALYZE (analyze_1d, fourier.cpp:39-53): c_k = (-1)^k / n * FFT(x)_{(k+n) mod n},
+//   stored at k + n/2 (k = -n/2 .. n/2-1).
+// SYNTH (synthesize_1d, fourier.cpp:55-66): g[(k+n_out) mod n_out] = (-1)^k c_k for
+//   the modes both lengths hold, then the unnormalised backward transform.
+template <bool ANALYZE>
+__global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int n = P.fd.L;  // transform length (n for ANALYZE, n_out for SYNTH)
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + n;
+    double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int r = blockIdx.x;
+    const double2* src = P.src + static_cast<long long>(r) * P.ld_in;
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    for (int i = tid; i < n; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
+    if constexpr (ANALYZE) {
+        for (int j = tid; j < n; j += nthr) a[j] = src[j];
+        __syncthreads();
+        fft_forward(a, P.fd, T, tid, nthr);  // X_t at a[rev[t]]
+        const double inv = 1.0 / n;
+        for (int kp = tid; kp < n; kp += nthr) {
+            const int k = kp - n / 2;
+            const int t = k < 0 ? k + n : k;
+            const double s = (k % 2 == 0) ? inv : -inv;
+            const double2 v = a[s_rev[t]];
+            P.dst[static_cast<long long>(kp) * P.ld_out + r] = make_double2(s * v.x, s * v.y);
+        }
+    } else {
+        for (int j = tid; j < n; j += nthr) a[j] = make_double2(0.0, 0.0);
+        __syncthreads();
+        const int lo = max(-P.n_in / 2, -n / 2), hi = min(P.n_in / 2, n / 2);
+        for (int k = lo + tid; k < hi; k += nthr) {
+            const double2 c = src[k + P.n_in / 2];
+            const int t = k < 0 ? k + n : k;
+            a[s_rev[t]] = (k % 2 == 0) ? c : make_double2(-c.x, -c.y);  // DIT input: digit-reversed
+        }
+        __syncthreads();
+        fft_inverse(a, P.fd, T, tid, nthr);  // natural order
+        for (int j = tid; j < n; j += nthr) P.dst[static_cast<long long>(j) * P.ld_out + r] = a[j];
+    }
+}
+
+// doubled[j][k] = phys[j - m/2][k] (j >= m/2), phys[m/2 - j][(k + n/2) mod n]
+// (j < m/2): the glide reflection f(lambda -+ pi, -theta) of dfs_extend as an
+// index map on the physical rows theta_p = 2 pi p / m, p = 0..m/2.
+__global__ void dfs_double_kernel(int m, int n, const double* phys, double2* grid) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(m) * n) return;
+    const int j = static_cast<int>(idx / n), k = static_cast<int>(idx - static_cast<long long>(j) * n);
+    const double v = (j >= m / 2) ? phys[static_cast<long long>(j - m / 2) * n + k]
+                                  : phys[static_cast<long long>(m / 2 - j) * n + (k + n / 2) % n];
+    grid[idx] = make_double2(v, 0.0);
+}
+
+size_t xform_smem_bytes(int n, int nhi, int nlo) {
+    return static_cast<size_t>(n) * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>(n) * 4;
+}
+
+cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(xform_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    if (nrows <= 0) return cudaSuccess;
+    if (analyze) xform_kernel<true><<<nrows, nthr, smem, st>>>(P);
+    else xform_kernel<false><<<nrows, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st) {
+    const long long tot = static_cast<long long>(m) * n;
+    if (tot > 0) dfs_double_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(m, n, phys, grid);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

@@ -9,6 +9,12 @@ ResidualReport               poisson.hpp:49-53    ResidualReport
 residual(pb, sol)            poisson.hpp:54       residual(pb, sol)    -> sk_residual
 bench_poisson(sizes)         poisson.hpp:62       bench_poisson(sizes)
 integration_weights(m)       poisson.hpp:21       integration_weights(m)
+assemble_poisson(f, m, n,     poisson.hpp:40-41    assemble_poisson(f, m, n, report) -> sk_assemble
+  AssembleReport*)
+LowRankSphereFun / AssembleReport                 LowRankSphereFun / AssembleReport
+analyze_2d(BMCGrid)          fourier.hpp:107      analyze_2d(grid)     -> sk_analyze_2d
+sample_grid(X, m, n)         fourier.hpp:108      sample_grid(X, m, n) -> sk_sample_grid
+sample_dfs(f, m, n)          sphere_domain.hpp:61 sample_dfs(phys, m)  -> sk_sample_dfs (of samples)
 sample_dfs -> analyze_2d -> Msin^2 -> solve ->    solve_grid(f_phys)   -> sk_solve_grid
   sample_grid (the grid-level composition)
 
@@ -32,7 +38,8 @@ from ._lib import DeviceError, UnsupportedError, precondition_error, size_error,
 __all__ = [
     "Plan", "PoissonProblem", "PoissonSolution", "ResidualReport", "BenchRow", "solve", "residual", "solve_grid",
     "bench_poisson", "integration_weights", "size_error", "precondition_error", "structure_error", "DeviceError",
-    "UnsupportedError",
+    "UnsupportedError", "LowRankSphereFun", "AssembleReport", "assemble_poisson", "analyze_2d", "sample_grid",
+    "sample_dfs",
 ]
 
 
@@ -234,6 +241,78 @@ class Plan:
         self._follow_torch(back)
         _lib.check(self.lib.sk_stage_lambda_inv(self._h, P, rb, cb, rank, _ptr(back), _ptr(u_rows)))
 
+    # -- assemble / standalone transforms
+    def assemble(self, d, col, row, vscale: float = 0.0, F=None):
+        """assemble_poisson on raw low-rank factors (sk_assemble): d (K,),
+        col (K, mf), row (K, nf) complex -> (F (M, N) complex, report[3])."""
+        dev = _is_device(d)
+        if dev:
+            import torch
+            K, mf, nf = int(d.shape[0]), int(col.shape[-1]), int(row.shape[-1])
+            if F is None:
+                F = torch.empty((self.M, self.N), dtype=torch.complex128, device=d.device)
+        else:
+            d, col, row = (np.ascontiguousarray(x, dtype=np.complex128) for x in (d, col, row))
+            K = d.shape[0]
+            col = col[None] if col.ndim == 1 else col  # a single term may come as a vector
+            row = row[None] if row.ndim == 1 else row
+            mf, nf = col.shape[1], row.shape[1]
+            if F is None:
+                F = np.empty((self.M, self.N), np.complex128)
+        if col.shape[0] != K or row.shape[0] != K:
+            raise size_error("assemble_poisson: factor counts differ")
+        rep = (ctypes.c_double * 3)()
+        self._follow_torch(d)
+        _lib.check(self.lib.sk_assemble(self._h, K, mf, nf, _ptr(d), _ptr(col), _ptr(row), float(vscale), _ptr(F),
+                                        rep, _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return F, [rep[0], rep[1], rep[2]]
+
+    def analyze_2d(self, grid, X=None):
+        """analyze_2d of an m x n complex doubled grid (sk_analyze_2d)."""
+        dev = _is_device(grid)
+        m, n = (int(x) for x in grid.shape[-2:])
+        if dev:
+            import torch
+            X = torch.empty((m, n), dtype=torch.complex128, device=grid.device) if X is None else X
+        else:
+            grid = np.ascontiguousarray(grid, dtype=np.complex128)
+            X = np.empty((m, n), np.complex128) if X is None else X
+        self._follow_torch(grid)
+        _lib.check(self.lib.sk_analyze_2d(self._h, m, n, _ptr(grid), _ptr(X), _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return X
+
+    def sample_grid(self, X, m_out: int, n_out: int, grid=None):
+        """sample_grid of rows x cols coefficients on an m_out x n_out grid."""
+        dev = _is_device(X)
+        rows, cols = (int(x) for x in X.shape[-2:])
+        if dev:
+            import torch
+            grid = torch.empty((m_out, n_out), dtype=torch.complex128, device=X.device) if grid is None else grid
+        else:
+            X = np.ascontiguousarray(X, dtype=np.complex128)
+            grid = np.empty((m_out, n_out), np.complex128) if grid is None else grid
+        self._follow_torch(X)
+        _lib.check(self.lib.sk_sample_grid(self._h, rows, cols, _ptr(X), int(m_out), int(n_out), _ptr(grid),
+                                           _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return grid
+
+    def sample_dfs(self, phys, m: Optional[int] = None, grid=None):
+        """DFS doubling of physical samples ((m/2+1) x n real) -> m x n complex."""
+        dev = _is_device(phys)
+        rows, n = (int(x) for x in phys.shape[-2:])
+        m = 2 * (rows - 1) if m is None else int(m)
+        if rows != m // 2 + 1:
+            raise size_error("sample_dfs: expected m/2 + 1 physical rows")
+        if dev:
+            import torch
+            grid = torch.empty((m, n), dtype=torch.complex128, device=phys.device) if grid is None else grid
+        else:
+            phys = np.ascontiguousarray(phys, dtype=np.float64)
+            grid = np.empty((m, n), np.complex128) if grid is None else grid
+        self._follow_torch(phys)
+        _lib.check(self.lib.sk_sample_dfs(self._h, m, n, _ptr(phys), _ptr(grid), _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return grid
+
     def _check_shape(self, a, tail):
         shp = tuple(a.shape)
         if shp[-2:] != tuple(tail):
@@ -339,3 +418,61 @@ def bench_poisson(sizes, reps: Optional[int] = None):
             best = min(best, time.perf_counter() - t0)
         rows.append(BenchRow(s, r, best))
     return rows
+
+
+# ------------------------------------------------- assemble / Fourier layer
+@dataclasses.dataclass
+class LowRankSphereFun:
+    """The factors of a low-rank sphere function (lowrank.hpp:47-59):
+    f~(lambda, theta) = sum_j d[j] a_j(theta) b_j(lambda), with col_coeffs[j]
+    the theta coefficients of a_j (mode t at t + mf/2) and row_coeffs[j] the
+    lambda coefficients of b_j.  (The constructor from an expression or a
+    callable is outside this hot path; factors come from the caller.)"""
+    d: np.ndarray
+    col_coeffs: np.ndarray  # (K, mf) complex
+    row_coeffs: np.ndarray  # (K, nf) complex
+    vscale: float = 0.0
+
+    def rank(self) -> int:
+        return int(np.asarray(self.d).shape[0])
+
+
+@dataclasses.dataclass
+class AssembleReport:
+    mean_removed: bool = False
+    removed_mean: complex = 0j
+
+
+def assemble_poisson(f: LowRankSphereFun, m: int, n: int, report: Optional[AssembleReport] = None) -> PoissonProblem:
+    """spherekit::assemble_poisson (poisson.cpp:52-86) on the GPU: F =
+    sum_j d_j (Msin^2 a_j) b_j^T with the reference's mean removal;
+    bit-identical to the reference."""
+    if m % 2 or n % 2 or m <= 0 or n <= 0:
+        raise size_error("assemble_poisson: sizes must be positive and even")
+    F, rep = _plan(m, n).assemble(f.d, f.col_coeffs, f.row_coeffs, f.vscale)
+    if report is not None:
+        report.mean_removed = bool(rep[0])
+        report.removed_mean = complex(rep[1], rep[2])
+    return PoissonProblem(m, n, F)
+
+
+def _xplan() -> Plan:
+    return _plan(8, 4)  # any plan: the standalone transforms take their own sizes
+
+
+def analyze_2d(grid) -> np.ndarray:
+    """spherekit::analyze_2d (fourier.cpp:170-188): m x n doubled sample grid
+    -> m x n coefficient matrix (row i = theta mode i - m/2)."""
+    return _xplan().analyze_2d(grid)
+
+
+def sample_grid(X, m: int, n: int) -> np.ndarray:
+    """spherekit::sample_grid (fourier.cpp:190-209): coefficients -> m x n
+    grid values, zero-padding or truncating the modes."""
+    return _xplan().sample_grid(X, m, n)
+
+
+def sample_dfs(phys, m: Optional[int] = None) -> np.ndarray:
+    """spherekit::sample_dfs (sphere_domain.cpp:46-52) applied to physical
+    samples: the DFS-doubled m x n grid."""
+    return _xplan().sample_dfs(phys, m)

@@ -1,0 +1,160 @@
+"""GPU parity of the widened boundary: assemble_poisson,
+analyze_2d, sample_grid (zero-pad / truncate) and DFS doubling, through the C
+ABI, against the reference's golden vectors and the oracle."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests need a B200 (there is no CPU fallback)")
+    import paper_1510_08094_b200 as p
+    return p
+
+
+def _names(prefix):
+    return [os.path.basename(f)[:-4] for f in sorted(glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))]
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def _c(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+# ------------------------------------------------------------ assemble_poisson
+@pytest.mark.parametrize("name", _names("assemble_"))
+def test_assemble_bit_identical_to_reference_golden(pkg, name):
+    # poisson.cpp:52-86 on the reference's own construct() factors
+    d = golden(name)
+    m, n = d["F"].shape
+    f = pkg.LowRankSphereFun(d["d"], d["col"], d["row"], float(d["vscale"]))
+    rep = pkg.AssembleReport()
+    pb = pkg.assemble_poisson(f, m, n, rep)
+    np.testing.assert_array_equal(pb.f, d["F"])
+    assert rep.mean_removed == bool(d["rep"][0])
+    assert rep.removed_mean == complex(d["rep"][1], d["rep"][2])
+
+
+@pytest.mark.parametrize("K,mf,nf,m,n,vs", [(3, 10, 8, 16, 12, 0.0), (5, 40, 30, 24, 64, 1e30), (1, 2, 2, 8, 8, 0.0),
+                                           (7, 300, 200, 128, 96, 0.0), (40, 64, 64, 256, 512, 0.0),
+                                           (0, 4, 4, 8, 8, 0.0), (2, 0, 6, 10, 6, 0.0)])
+def test_assemble_random_factors_vs_oracle(pkg, oracle, K, mf, nf, m, n, vs):
+    rng = np.random.default_rng(K * 1000 + mf)
+    d, col, row = _c(rng, K), _c(rng, K, mf), _c(rng, K, nf)
+    d[:K // 3] = 0  # exact-zero terms are skipped by the reference (poisson.cpp:66)
+    F0, r0 = oracle.assemble(d, col, row, vs, m, n)
+    with pkg.Plan(m, n) as plan:
+        F, r = plan.assemble(d, col, row, vs)
+    np.testing.assert_array_equal(F, F0)
+    np.testing.assert_array_equal(np.array(r), r0)
+
+
+def test_assemble_device_tensors(pkg, oracle):
+    import torch
+    rng = np.random.default_rng(11)
+    d, col, row = _c(rng, 4), _c(rng, 4, 20), _c(rng, 4, 18)
+    F0, r0 = oracle.assemble(d, col, row, 1.0, 32, 24)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    with pkg.Plan(32, 24) as plan:
+        F, r = plan.assemble(t(d), t(col), t(row), 1.0)
+        torch.cuda.synchronize()
+    np.testing.assert_array_equal(F.cpu().numpy(), F0)
+    np.testing.assert_array_equal(np.array(r), r0)
+
+
+def test_assemble_then_solve_is_the_reference_composition(pkg):
+    # assemble -> solve: the reference CLI's `poisson` route (spherekit_main.cpp:292-299)
+    d = golden("assemble_sin50xyz_150x150")
+    f = pkg.LowRankSphereFun(d["d"], d["col"], d["row"], float(d["vscale"]))
+    pb = pkg.assemble_poisson(f, 150, 150)
+    kat = golden("kat_sin50xyz_150")
+    np.testing.assert_array_equal(pb.f, kat["F"])
+    X = pkg.solve(pb).x
+    r = pkg.residual(pb, pkg.PoissonSolution(X))
+    assert r.interior_max <= 1e-10 * np.abs(pb.f).max() and r.constraint_abs <= 1e-12
+
+
+def test_assemble_size_errors(pkg):
+    with pkg.Plan(8, 8) as plan:
+        with pytest.raises(pkg.size_error):
+            plan.assemble(np.ones(1, complex), np.ones((1, 3), complex), np.ones((1, 2), complex))
+    with pytest.raises(pkg.size_error):
+        pkg.assemble_poisson(pkg.LowRankSphereFun(np.ones(1), np.ones((1, 2)), np.ones((1, 2))), 7, 8)
+
+
+# -------------------------------------------------- analyze_2d / sample_grid
+@pytest.mark.parametrize("name", _names("transforms_"))
+def test_transforms_match_reference_golden(pkg, name):
+    d = golden(name)
+    X = pkg.analyze_2d(d["grid"])
+    assert _rel(X, d["X"]) <= 1e-14
+    for k in d.files:
+        if k.startswith("S_"):
+            mo, no = map(int, k[2:].split("x"))
+            assert _rel(pkg.sample_grid(d["X"], mo, no), d[k]) <= 1e-13, k
+
+
+@pytest.mark.parametrize("m,n", [(4, 2), (6, 10), (128, 96), (1000, 700), (2048, 4096)])
+def test_transforms_vs_oracle_and_round_trip(pkg, oracle, m, n):
+    rng = np.random.default_rng(m + n)
+    g = _c(rng, m, n)
+    X = pkg.analyze_2d(g)
+    if m * n <= 1 << 20:
+        assert _rel(X, oracle.analyze_2d(g)) <= 1e-14
+        outs = [(2 * m, 2 * n)] + ([(m // 2, n // 2)] if m % 4 == 0 and n % 4 == 0 else [])
+        for mo, no in outs:  # zero-pad and truncate
+            assert _rel(pkg.sample_grid(X, mo, no), oracle.sample_grid(X, mo, no)) <= 1e-13
+    # round trip (test_fourier.cpp:198-211): sample_grid(analyze_2d(g)) = g
+    assert _rel(pkg.sample_grid(X, m, n), g) <= 1e-13
+
+
+def test_transforms_device_tensors(pkg):
+    import torch
+    rng = np.random.default_rng(3)
+    g = _c(rng, 60, 84)
+    X0 = pkg.analyze_2d(g)
+    with pkg.Plan(8, 4) as plan:
+        gt = torch.from_numpy(g).cuda()
+        X = plan.analyze_2d(gt)
+        G = plan.sample_grid(X, 60, 84)
+        torch.cuda.synchronize()
+    np.testing.assert_array_equal(X.cpu().numpy(), X0)
+    assert _rel(G.cpu().numpy(), g) <= 1e-13
+
+
+def test_transform_errors(pkg):
+    with pytest.raises(pkg.size_error):
+        pkg.analyze_2d(np.zeros((6, 5), complex))
+    with pytest.raises(pkg.size_error):
+        pkg.sample_grid(np.zeros((6, 4), complex), 5, 4)
+    with pytest.raises(pkg.UnsupportedError):
+        pkg.analyze_2d(np.zeros((8, 602), complex))  # 602 = 2 * 7 * 43: prime factor > 7
+
+
+# ------------------------------------------------------------- DFS doubling
+@pytest.mark.parametrize("name", _names("dfs_double_"))
+def test_sample_dfs_golden(pkg, name):
+    d = golden(name)
+    np.testing.assert_array_equal(pkg.sample_dfs(d["phys"], d["grid"].shape[0]), d["grid"])
+
+
+def test_sample_dfs_then_analyze_matches_grid_pipeline(pkg):
+    # the grid-level composition's first two steps against the reference's
+    d = golden("grid_sh_64x64_L12")
+    g = pkg.sample_dfs(d["phys"], 64)
+    X = pkg.analyze_2d(g)
+    from oracle.oracle import Oracle
+    Xo = Oracle().analyze_2d(Oracle().dfs_double(d["phys"], 64))
+    assert _rel(X, Xo) <= 1e-14

@@ -51,7 +51,7 @@ struct AssembleParams {
     const double2* col;    // K x mf
     const double2* row;    // K x nf
     double vscale;
-    double2* sa;           // scratch K x M: d_j Msin^2 pad(a_j)
+    double2* sa;           // scratch K x M: d_j Msin^2 pad(a_j), then K sum2 terms
     double2* bp;           // scratch K x N: pad(b_j)
     double2* F;            // M x N
     double* report;        // device [3]: removed?, mu re, mu im

@@ -1006,17 +1006,18 @@ sk_status sk_assemble(sk_plan_t p, int K, int mf, int nf, const double* d, const
     if ((s = stage_in(p, row, sizeof(double2) * K * static_cast<size_t>(nf), flags, 2,
                       reinterpret_cast<const void**>(&dr))) != SK_OK)
         return s;
-    // scratch slot 3: [report(4 doubles)] [SA: K x M] [B: K x N] [F staging: M x N if host]
+    // scratch slot 3: [report(4 doubles)] [SA: K x M] [sum2 terms: K] [B: K x N] [F staging: M x N if host]
     const size_t nsa = static_cast<size_t>(K) * M, nb = static_cast<size_t>(K) * N, nfm = static_cast<size_t>(M) * N;
     void* w = nullptr;
-    if ((s = scratch(p, 3, 32 + sizeof(double2) * (nsa + nb + ((flags & SK_DEVICE) ? 0 : nfm)), &w)) != SK_OK) return s;
+    if ((s = scratch(p, 3, 32 + sizeof(double2) * (nsa + K + nb + ((flags & SK_DEVICE) ? 0 : nfm)), &w)) != SK_OK)
+        return s;
     double* rep = static_cast<double*>(w);
     double2* sa = reinterpret_cast<double2*>(static_cast<char*>(w) + 32);
-    double2* bp = sa + nsa;
+    double2* bp = sa + nsa + K;
     double2* dF = (flags & SK_DEVICE) ? reinterpret_cast<double2*>(F) : bp + nb;
     sk::AssembleParams ap{M, N, K, mf, nf, dd, dc, dr, vscale, sa, bp, dF, rep};
     CU(sk::launch_assemble(ap, p->stream));
-    p->last_launches = K > 0 ? 3 : 2;
+    p->last_launches = K > 0 ? 4 : 2;
     double h[3];
     CU(cudaMemcpyAsync(h, rep, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
     if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(F, dF, sizeof(double2) * nfm, cudaMemcpyDeviceToHost, p->stream));

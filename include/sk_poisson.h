@@ -74,7 +74,7 @@ typedef struct sk_plan_s* sk_plan_t;
                           pointers: work is queued on the plan stream.  Host
                           pointers (sk_solve_grid): the solve is pipelined —
                           H2D copy, transforms and D2H copy on three streams
-                          with two device slots, so consecutive calls overlap
+                          with three device slots, so consecutive calls overlap
                           their copies with each other's compute; f and u must
                           stay valid (and should be pinned) until sk_sync.
                           Errors that need a host-side check, e.g. the mean

@@ -300,11 +300,12 @@ struct sk_plan_s {
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
     // pipelined host-memory solves (SK_HOST | SK_ASYNC)
+    static constexpr int kPipe = 3;  // device slots: H2D(i+1), solve(i), D2H(i-1) all in flight
     bool pipe_ready = false;
-    double* pipe_buf[2] = {nullptr, nullptr};
-    double* pipe_stats[2] = {nullptr, nullptr};  // pinned
-    bool pipe_pending[2] = {false, false};
-    cudaEvent_t pipe_in[2] = {}, pipe_done[2] = {}, pipe_out[2] = {};
+    double* pipe_buf[kPipe] = {};
+    double* pipe_stats[kPipe] = {};  // pinned
+    bool pipe_pending[kPipe] = {};
+    cudaEvent_t pipe_in[kPipe] = {}, pipe_done[kPipe] = {}, pipe_out[kPipe] = {};
     cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
     int pipe_slot = 0;
     long long last_launches = 0;
@@ -355,10 +356,12 @@ sk_status check_precondition(sk_plan_t p, int nrhs) {
     return precondition_from(p->host_stats.data(), nrhs);
 }
 
-// Host-memory solves with SK_ASYNC: two device slots, the H2D copy of a solve
-// on its own stream, the transforms on the plan stream, the D2H copy on a
-// third stream, so consecutive solves overlap their copies (both directions
-// of the link) with each other's compute.  The precondition of a solve is
+// Host-memory solves with SK_ASYNC: three device slots, the H2D copy of a
+// solve on its own stream, the transforms on the plan stream, the D2H copy on
+// a third stream, so consecutive solves overlap their copies (both directions
+// of the link) with each other's compute; with three slots the H2D of solve
+// i+1 never waits for the D2H of solve i-1, and the period is the slowest of
+// the two copies and the solve.  The precondition of a solve is
 // evaluated when its slot comes round again or at sk_sync.
 sk_status pipe_check_slot(sk_plan_t p, int slot) {
     if (!p->pipe_pending[slot]) return SK_OK;
@@ -369,7 +372,7 @@ sk_status pipe_check_slot(sk_plan_t p, int slot) {
 
 sk_status pipe_init(sk_plan_t p, size_t ng) {
     if (p->pipe_ready) return SK_OK;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < sk_plan_s::kPipe; ++i) {
         CU(cudaMalloc(&p->pipe_buf[i], sizeof(double) * ng));
         CU(cudaMallocHost(&p->pipe_stats[i], sizeof(double) * 4 * p->nrhs));
         CU(cudaEventCreateWithFlags(&p->pipe_in[i], cudaEventDisableTiming));
@@ -566,7 +569,7 @@ sk_status sk_plan_destroy(sk_plan_t p) {
         cudaStreamSynchronize(p->pipe_h2d);
         cudaStreamSynchronize(p->pipe_d2h);
         cudaStreamSynchronize(p->stream);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < sk_plan_s::kPipe; ++i) {
             cudaFree(p->pipe_buf[i]);
             cudaFreeHost(p->pipe_stats[i]);
             cudaEventDestroy(p->pipe_in[i]);
@@ -597,10 +600,12 @@ sk_status sk_sync(sk_plan_t p) {
     if (p->pipe_ready) {
         CU(cudaStreamSynchronize(p->pipe_h2d));
         CU(cudaStreamSynchronize(p->pipe_d2h));
-        const sk_status a = pipe_check_slot(p, 0);
-        const sk_status b = pipe_check_slot(p, 1);
-        if (a != SK_OK) return a;
-        if (b != SK_OK) return b;
+        sk_status first = SK_OK;
+        for (int i = 0; i < sk_plan_s::kPipe; ++i) {
+            const sk_status a = pipe_check_slot(p, (p->pipe_slot + i) % sk_plan_s::kPipe);  // oldest first
+            if (first == SK_OK) first = a;
+        }
+        if (first != SK_OK) return first;
     }
     return SK_OK;
 }
@@ -815,8 +820,8 @@ sk_status sk_solve_grid(sk_plan_t p, const double* f, double* u, double* X_half,
         if (X_half) return fail(SK_ERR_ARGUMENT, "X_half is not available with asynchronous host-memory solves");
         if ((s = pipe_init(p, ng)) != SK_OK) return s;
         const int slot = p->pipe_slot;
-        p->pipe_slot ^= 1;
-        const sk_status prev = pipe_check_slot(p, slot);  // the solve that used this slot two calls ago
+        p->pipe_slot = (slot + 1) % sk_plan_s::kPipe;
+        const sk_status prev = pipe_check_slot(p, slot);  // the solve that used this slot kPipe calls ago
         double* buf = p->pipe_buf[slot];
         CU(cudaStreamWaitEvent(p->pipe_h2d, p->pipe_out[slot], 0));  // its result has left the slot
         CU(cudaMemcpyAsync(buf, f, sizeof(double) * ng, cudaMemcpyHostToDevice, p->pipe_h2d));

@@ -460,7 +460,9 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // theta stage: one CTA pair per mode when a parity half fits shared
     // memory, else a cluster of 2Q CTAs (Q = 4) holding quarters
     p->thr_theta = round_threads(Lt / 8, 64, 512);
-    if (p->grid_ok && (s = build_fft(Lt, p->thr_theta, p->ft, true, true)) != SK_OK) {
+    const bool odd_t = !std::getenv("SK_ODDSPAN_THETA") || std::atoi(std::getenv("SK_ODDSPAN_THETA")) != 0;
+    const bool odd_l = !std::getenv("SK_ODDSPAN_LAMBDA") || std::atoi(std::getenv("SK_ODDSPAN_LAMBDA")) != 0;
+    if (p->grid_ok && (s = build_fft(Lt, p->thr_theta, p->ft, odd_t, true)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
@@ -494,7 +496,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // lambda stages: one CTA per row, or a CTA pair splitting the row by parity
     // (odd first span: the digit-reversed split/pack walks spread over all banks)
     p->thr_lambda = round_threads(Ll / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, true)) != SK_OK) {
+    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }

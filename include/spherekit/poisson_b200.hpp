@@ -7,6 +7,12 @@
 //   ResidualReport residual(const PoissonProblem&,     spherekit::b200::residual
 //                           const PoissonSolution&) :54
 //   (grid composition)                   spherekit::b200::solve_grid
+//   PoissonProblem assemble_poisson(const              spherekit::b200::assemble_poisson
+//       LowRankSphereFun&, int, int, AssembleReport*) :40-41
+//   fourier.hpp: Matrix analyze_2d(const BMCGrid&) :107 spherekit::b200::analyze_2d
+//   BMCGrid sample_grid(const CoeffMatrix&, int, int)  spherekit::b200::sample_grid
+//       :108
+//   sphere_domain.hpp: sample_dfs (of samples) :61     spherekit::b200::sample_dfs
 //
 // Exceptions are the reference's (types.hpp:43-65): size_error,
 // precondition_error, structure_error; device failures throw
@@ -15,6 +21,7 @@
 // PoissonSolution, ResidualReport and the error types).
 #pragma once
 
+#include <algorithm>
 #include <functional>
 #include <map>
 #include <memory>
@@ -26,7 +33,10 @@
 #include <vector>
 
 #include "sk_poisson.h"
+#include "spherekit/fourier.hpp"
+#include "spherekit/lowrank.hpp"
 #include "spherekit/poisson.hpp"
+#include "spherekit/sphere_domain.hpp"
 
 namespace spherekit {
 namespace b200 {
@@ -107,6 +117,75 @@ inline std::vector<double> solve_grid(const std::vector<double>& f, int m, int n
     std::vector<double> u(f.size());
     check(sk_solve_grid(p, f.data(), u.data(), nullptr, SK_HOST));
     return u;
+}
+
+// spherekit::assemble_poisson (poisson.cpp:52-86), bit-identical F.
+inline PoissonProblem assemble_poisson(const LowRankSphereFun& f, int m, int n, AssembleReport* report = nullptr) {
+    if (m % 2 != 0 || n % 2 != 0 || m <= 0 || n <= 0)
+        throw size_error("assemble_poisson: sizes must be positive and even");
+    const int K = f.rank(), mf = f.theta_modes(), nf = f.lambda_modes();
+    std::vector<complex> col(static_cast<size_t>(K) * mf), row(static_cast<size_t>(K) * nf);
+    for (int j = 0; j < K; ++j) {
+        if (f.col_coeffs[j].size() != mf || f.row_coeffs[j].size() != nf)
+            throw size_error("assemble_poisson: factor lengths differ");
+        std::copy(f.col_coeffs[j].raw().begin(), f.col_coeffs[j].raw().end(), col.begin() + static_cast<size_t>(j) * mf);
+        std::copy(f.row_coeffs[j].raw().begin(), f.row_coeffs[j].raw().end(), row.begin() + static_cast<size_t>(j) * nf);
+    }
+    sk_plan_t p = PlanCache::instance().get(m, n);
+    PoissonProblem pb;
+    pb.m = m;
+    pb.n = n;
+    pb.f = Matrix(m, n);
+    double rep[3];
+    check(sk_assemble(p, K, mf, nf, reinterpret_cast<const double*>(f.d.data()),
+                      reinterpret_cast<const double*>(col.data()), reinterpret_cast<const double*>(row.data()),
+                      f.vscale, reinterpret_cast<double*>(pb.f.data().data()), rep, SK_HOST));
+    if (report) {
+        report->mean_removed = rep[0] != 0.0;
+        report->removed_mean = complex(rep[1], rep[2]);
+    }
+    return pb;
+}
+
+// Plan for the standalone transforms (they take their own sizes).
+inline sk_plan_t transform_plan() { return PlanCache::instance().get(8, 4); }
+
+inline BMCGrid make_grid(int m, int n) {  // BMCGrid(m, n) without the out-of-line constructor
+    if (m % 2 != 0 || n % 2 != 0 || m <= 0 || n <= 0) throw size_error("BMCGrid: sample counts must be positive and even");
+    BMCGrid g;
+    g.rows = m;
+    g.cols = n;
+    g.v.assign(static_cast<size_t>(m) * n, complex{});
+    return g;
+}
+
+// spherekit::analyze_2d (fourier.cpp:170-188)
+inline Matrix analyze_2d(const BMCGrid& g) {
+    Matrix x(g.rows, g.cols);
+    check(sk_analyze_2d(transform_plan(), g.rows, g.cols, reinterpret_cast<const double*>(g.v.data()),
+                        reinterpret_cast<double*>(x.data().data()), SK_HOST));
+    return x;
+}
+
+// spherekit::sample_grid (fourier.cpp:190-209), zero-padding / truncating
+inline BMCGrid sample_grid(const Matrix& x, int m, int n) {
+    if (m % 2 != 0 || n % 2 != 0) throw size_error("sample_grid: output sizes must be even");
+    BMCGrid g = make_grid(m, n);
+    check(sk_sample_grid(transform_plan(), x.rows(), x.cols(), reinterpret_cast<const double*>(x.data().data()), m, n,
+                         reinterpret_cast<double*>(g.v.data()), SK_HOST));
+    return g;
+}
+// (CoeffMatrix::densified is the reference's, fourier.cpp; link its library)
+inline BMCGrid sample_grid(const CoeffMatrix& xm, int m, int n) { return sample_grid(xm.densified(), m, n); }
+
+// spherekit::sample_dfs (sphere_domain.cpp:46-52) of physical samples
+// phys[(m/2+1) x n] (theta_p = 2 pi p/m): the doubled m x n grid.
+inline BMCGrid sample_dfs(const std::vector<double>& phys, int m, int n) {
+    if (static_cast<long long>(phys.size()) != static_cast<long long>(m / 2 + 1) * n)
+        throw size_error("sample_dfs: phys must hold (m/2+1) x n samples");
+    BMCGrid g = make_grid(m, n);
+    check(sk_sample_dfs(transform_plan(), m, n, phys.data(), reinterpret_cast<double*>(g.v.data()), SK_HOST));
+    return g;
 }
 
 }  // namespace b200

@@ -4,6 +4,8 @@
 // one it must fail loudly (no CPU fallback).
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <complex>
 
 #include "spherekit/poisson.hpp"
 #include "spherekit/poisson_b200.hpp"
@@ -26,6 +28,40 @@ int main() {
     try {
         const PoissonSolution s = b200::solve(pb);
         std::printf("solved %d x %d, x(9,9) = %.17g\n", s.x.rows(), s.x.cols(), s.x.at(9, 9).real());
+        // assemble_poisson of f = cos(theta) (rank 1): sin^2 cos = cos/4 - cos3/4,
+        // so F = 1/8 at theta modes +-1 and -1/8 at +-3 in the lambda-mode-0 column
+        LowRankSphereFun f;
+        f.d = {complex(1.0, 0.0)};
+        CoeffVec a(8), b(4);
+        a.mode(1) = a.mode(-1) = complex(0.5, 0.0);
+        b.mode(0) = complex(1.0, 0.0);
+        f.col_coeffs = {a};
+        f.row_coeffs = {b};
+        f.parity = {Parity::odd};
+        f.vscale = 1.0;
+        AssembleReport rep;
+        const PoissonProblem q = b200::assemble_poisson(f, 16, 8, &rep);
+        if (q.f.at(9, 4) != complex(0.125, 0.0) || q.f.at(11, 4) != complex(-0.125, 0.0) || rep.mean_removed) {
+            std::printf("assemble mismatch\n");
+            return 1;
+        }
+        // analyze_2d of the doubled grid of a pure mode e^{i(2 theta + lambda)}, then sample_grid back
+        BMCGrid g = b200::make_grid(8, 6);
+        for (int j = 0; j < 8; ++j)
+            for (int k = 0; k < 6; ++k) g.at(j, k) = std::polar(1.0, 2 * g.theta(j) + g.lambda(k));
+        const Matrix X = b200::analyze_2d(g);
+        if (std::abs(X.at(4 + 2, 3 + 1) - complex(1.0, 0.0)) > 1e-14) {
+            std::printf("analyze_2d mismatch\n");
+            return 1;
+        }
+        const BMCGrid back = b200::sample_grid(X, 8, 6);
+        double err = 0;
+        for (size_t i = 0; i < g.v.size(); ++i) err = std::max(err, std::abs(back.v[i] - g.v[i]));
+        if (err > 1e-14) {
+            std::printf("sample_grid round trip %.3g\n", err);
+            return 1;
+        }
+        std::printf("assemble / analyze_2d / sample_grid ok\n");
         return 0;
     } catch (const std::runtime_error& e) {
         std::printf("device error: %s\n", e.what());

@@ -32,11 +32,37 @@ namespace sk {
 
 constexpr int kStage = 16;  // values per thread staged in registers across cluster exchanges
 
+#ifdef SK_PHASES
+extern __device__ unsigned long long g_phase[4096][24];
+#define SK_PROBE_L(i)                                                        \
+    do {                                                                    \
+        __syncthreads();                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_phase[blockIdx.x][i] = clock64(); \
+    } while (0)
+#else
+#define SK_PROBE_L(i) \
+    do {              \
+    } while (0)
+#endif
+
 // exp(-2 pi i m / n) for the 2L-th-root table (M-th roots): w_L^(-m) = T(2m)
-__device__ __forceinline__ double2 wL(const Tw& T, long long m, int L) {
-    long long mm = (2 * m) % (2LL * L);
-    if (mm < 0) mm += 2LL * L;
-    return T(static_cast<int>(mm));
+// (0 <= m < 4L: the callers' exponents s tau, s < Q, tau < L; 32-bit
+// reduction by subtraction — a 64-bit modulo here cost a third of the kernel)
+__device__ __forceinline__ double2 wL(const Tw& T, int m, int L) {
+    const int n2 = 2 * L;
+    int mm = 2 * m;
+    while (mm >= n2) mm -= n2;
+    return T(mm);
+}
+
+// v * i^e (exact), e = 0..3
+__device__ __forceinline__ double2 mul_ipow(double2 v, int e) {
+    switch (e & 3) {
+        case 0: return v;
+        case 1: return make_double2(-v.y, v.x);
+        case 2: return make_double2(-v.x, -v.y);
+        default: return make_double2(v.y, -v.x);
+    }
 }
 
 // ---------------------------------------------------------------- theta
@@ -186,6 +212,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     // output row p: in place, or straight into its lambda rank's return buffer
     auto gout = [&](int p) { return P.peers.n ? peer_ptr(P.peers, p, kg, p) : gcol(p); };
     const int* revq = fq.rev;
+    SK_PROBE_L(0);
 
     // chain of this CTA and its element range
     Chain cp, cm;
@@ -223,23 +250,46 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     const Tw TM = load_tw(P.fd, tM_hi, tM_lo, tid, nthr);
     const Tw TQ = load_tw(fq, tq_hi, tq_lo, tid, nthr);
     __syncthreads();
+    SK_PROBE_L(1);
 
     // ---- 1. fold + decimation: inputs x_j, j = Q r + q (first radix-Q split)
     const double invM = 1.0 / P.g.M;
-    for (int r = tid; r < Lq; r += nthr) {
-        const int j = Q * r + q;
-        const double2 aj = *gcol(j);
-        const double2 am = *gcol(L - j);
-        double2 x;
-        if (par == 0) x = make_double2((aj.x + sgn * am.x) * invM, (aj.y + sgn * am.y) * invM);
-        else x = cscale(cmul(make_double2(aj.x - sgn * am.x, aj.y - sgn * am.y), TM(j)), invM);
-        a[swz<true>(r)] = x;
+    // batches of kFoldU inputs per thread: all global loads of a batch are
+    // in flight before any shared-memory store
+    constexpr int kFoldU = 8;
+    for (int r0 = tid; r0 < Lq; r0 += kFoldU * nthr) {
+        double2 aj[kFoldU], am[kFoldU];
+#pragma unroll
+        for (int u = 0; u < kFoldU; ++u) {
+            const int r = r0 + u * nthr;
+            if (r < Lq) {
+                const int j = Q * r + q;
+                aj[u] = *gcol(j);
+                am[u] = *gcol(L - j);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kFoldU; ++u) {
+            const int r = r0 + u * nthr;
+            if (r < Lq) {
+                const int j = Q * r + q;
+                double2 x;
+                if (par == 0) x = make_double2((aj[u].x + sgn * am[u].x) * invM, (aj[u].y + sgn * am[u].y) * invM);
+                else x = cscale(cmul(make_double2(aj[u].x - sgn * am[u].x, aj[u].y - sgn * am[u].y), TM(j)), invM);
+                a[swz<true>(__ldg(revq + r))] = x;
+            }
+        }
     }
     __syncthreads();
-    fft_forward<true>(a, fq, TQ, tid, nthr);  // Y^q at swz(revq(m))
+    SK_PROBE_L(2);
+    fft_run<false, -1, true>(a, fq, TQ, tid, nthr);  // DIT: Y^q at swz(m), natural order
+    SK_PROBE_L(3);
     cluster.sync();
 
-    // ---- 2. radix-Q combine: X_tau = sum_s w_L^(-s tau) Y^s_(tau mod Lq), tau in my quarter
+    // ---- 2. radix-Q combine: X_tau = sum_s w_L^(-s tau) Y^s_(tau mod Lq), tau in my quarter.
+    // Y^s is in natural order (DIT forward), so the DSMEM reads of a warp are
+    // contiguous slots of each source CTA (random-order DSMEM reads ran at a
+    // quarter of the contiguous rate).
     {
         double2 st[kStage];
 #pragma unroll
@@ -247,11 +297,11 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
             const int tl = tid + u * nthr;
             if (tl < Lq) {
                 const int tau = q * Lq + tl;
-                const int ps = swz<true>(__ldg(revq + tl));
+                const int ps = swz<true>(tl);
                 double2 acc = rmt(par * Q + 0)[ps];
 #pragma unroll
                 for (int s2 = 1; s2 < Q; ++s2)
-                    acc = cadd(acc, cmul(rmt(par * Q + s2)[ps], wL(TM, static_cast<long long>(s2) * tau, L)));
+                    acc = cadd(acc, cmul(rmt(par * Q + s2)[ps], wL(TM, s2 * tau, L)));
                 st[u] = acc;
             }
         }
@@ -263,6 +313,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
         }
     }
     cluster.sync();
+    SK_PROBE_L(4);
 
     // ---- 3. k = 0 mean, boundary values, F_0
     double* stt = P.stats + 4 * rhs;
@@ -307,7 +358,9 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     }
 
     // ---- 4. the chain part
+    SK_PROBE_L(5);
     if (i_hi > i_lo) mbar_wait(bar, 0);
+    SK_PROBE_L(6);
     double fmax_acc = (par == 0 && q == 0) ? F0.x * F0.x + F0.y * F0.y : 0.0;
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
@@ -318,6 +371,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     solve_chain_part(a, ipv, wsc, tot, ch, L, i_lo, i_hi, xlo_cta, xhi_cta, slot, remote_tot, cpos, Q / 2, cluster,
                      fmax_acc, wsum, want_wsum);
 
+    SK_PROBE_L(7);
     // ---- 5. row j = 0 / constraint (parity 0, CTA 0)
     if (want_wsum) {
         wsum = block_sum2(wsum, red);
@@ -351,8 +405,10 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
         for (int tl = tid; tl < Lq; tl += nthr) xo[t_of(q * Lq + tl, par, L) + L] = a[swz<true>(tl)];
     }
     cluster.sync();
+    SK_PROBE_L(8);
 
-    // ---- 6. inverse radix-Q split: u_t' = w_L^(+q t') sum_s x_(t' + s Lq) w_Q^(+q s)
+    // ---- 6. inverse radix-Q split: u_t' = w_L^(+q t') sum_s x_(t' + s Lq) w_Q^(+q s),
+    // written to digit-reversed slots for the DIT inverse (natural order out)
     {
         double2 st[kStage];
 #pragma unroll
@@ -363,22 +419,25 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
                 double2 acc = rmt(par * Q + 0)[ps];
 #pragma unroll
                 for (int s2 = 1; s2 < Q; ++s2) {
-                    // w_Q^(+q s) = w_L^(+q s Lq)
-                    acc = cadd(acc, cmulc(rmt(par * Q + s2)[ps], wL(TM, static_cast<long long>(q) * s2 * Lq, L)));
+                    // w_Q^(+q s) = i^(q s) for Q = 4 (-1^(q s) for Q = 2), exact
+                    acc = cadd(acc, mul_ipow(rmt(par * Q + s2)[ps], (q * s2 * (4 / Q)) & 3));
                 }
-                st[u] = q == 0 ? acc : cmulc(acc, wL(TM, static_cast<long long>(q) * tl, L));
+                st[u] = q == 0 ? acc : cmulc(acc, wL(TM, q * tl, L));
             }
         }
         cluster.sync();
 #pragma unroll
         for (int u = 0; u < kStage; ++u) {
             const int tl = tid + u * nthr;
-            if (tl < Lq) a[swz<true>(tl)] = st[u];
+            if (tl < Lq) a[swz<true>(__ldg(revq + tl))] = st[u];
         }
     }
     __syncthreads();
-    fft_run<true, +1, true>(a, fq, TQ, tid, nthr);  // V_(Q m + q) at swz(revq(m))
+    SK_PROBE_L(9);
+    fft_run<false, +1, true>(a, fq, TQ, tid, nthr);  // DIT: V_(Q m + q) at swz(m)
+    SK_PROBE_L(10);
     cluster.sync();
+    SK_PROBE_L(11);
 
     // ---- 7. parity recombination v_j = Ve_j + w_M^j Vo_j, j = Q m + q
     {
@@ -388,15 +447,17 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
         const int m_hi = par == 0 ? Lq / 2 : Lq;
         for (int m = m_lo + tid; m < m_hi; m += nthr) {
             const int j = Q * m + q;
-            const int ps = swz<true>(__ldg(revq + m));
+            const int ps = swz<true>(m);
             *gout(j) = cadd(ve[ps], cmulc(vo[ps], TM(j)));
         }
         if (par == 0 && q == 0 && tid == 0) {
-            const int ps = swz<true>(__ldg(revq + 0));
+            const int ps = swz<true>(0);
             *gout(L) = csub(ve[ps], vo[ps]);  // j = L: w_M^L = -1
         }
     }
+    SK_PROBE_L(12);
     cluster.sync();
+    SK_PROBE_L(13);
 }
 
 // ---------------------------------------------------------------- lambda

@@ -64,6 +64,8 @@ bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = 
     if (L == 1) return true;
     std::vector<int> cur;
     double best = 1e300;
+    int maxr = 25;  // largest register radix (SK_MAXRADIX: A/B switch)
+    if (const char* e = std::getenv("SK_MAXRADIX")) maxr = std::atoi(e);
     if (odd_first_span) {
         // First radix takes every factor of two, so consecutive natural indices
         // sit an odd number of slots apart in the digit-reversed layout and a
@@ -73,14 +75,14 @@ bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = 
         if (p2 > 1 && p2 <= 16 && L / p2 > 1) {
             const long long nb = L / p2;
             cur.push_back(p2);
-            search_radices(L / p2, nthr, L, 25, cur, static_cast<double>((nb + nthr - 1) / nthr) * (p2 + 6) + 30,
+            search_radices(L / p2, nthr, L, maxr, cur, static_cast<double>((nb + nthr - 1) / nthr) * (p2 + 6) + 30,
                            best, R);
             if (!R.empty()) return true;
             cur.clear();
             best = 1e300;
         }
     }
-    search_radices(L, nthr, L, 25, cur, 0.0, best, R);
+    search_radices(L, nthr, L, maxr, cur, 0.0, best, R);
     return !R.empty();
 }
 

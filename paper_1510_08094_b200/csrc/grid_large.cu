@@ -55,16 +55,6 @@ __device__ __forceinline__ double2 wL(const Tw& T, int m, int L) {
     return T(mm);
 }
 
-// v * i^e (exact), e = 0..3
-__device__ __forceinline__ double2 mul_ipow(double2 v, int e) {
-    switch (e & 3) {
-        case 0: return v;
-        case 1: return make_double2(-v.y, v.x);
-        case 2: return make_double2(-v.x, -v.y);
-        default: return make_double2(v.y, -v.x);
-    }
-}
-
 // ---------------------------------------------------------------- theta
 // Solves this CTA's part [i_lo, i_hi) of a chain whose parts lie in
 // consecutive CTAs (chain position cpos of ncta).  Shared memory holds the
@@ -286,30 +276,40 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     SK_PROBE_L(3);
     cluster.sync();
 
-    // ---- 2. radix-Q combine: X_tau = sum_s w_L^(-s tau) Y^s_(tau mod Lq), tau in my quarter.
-    // Y^s is in natural order (DIT forward), so the DSMEM reads of a warp are
-    // contiguous slots of each source CTA (random-order DSMEM reads ran at a
-    // quarter of the contiguous rate).
+    // ---- 2. radix-Q combine: X_(c Lq + tl) = sum_s w_Q^(-s c) w_L^(-s tl) Y^s_tl,
+    // one distributed radix-Q butterfly per tl: CTA q owns the tl in
+    // [q Lq/Q, (q+1) Lq/Q), reads Y^s_tl from every CTA s and writes output c
+    // into CTA c's slot tl.  Y^s is in natural order (DIT forward), so the
+    // DSMEM reads and writes of a warp are contiguous slots (random-order
+    // DSMEM ran at a quarter of the contiguous rate), and the butterfly costs
+    // Q-1 twiddles per Q outputs.
     {
-        double2 st[kStage];
+        constexpr int TP = kStage / Q;  // tl per thread (Lq <= kStage * nthr)
+        const int lo = (q * Lq) / Q, hi = ((q + 1) * Lq) / Q;
+        double2 st[TP][Q];
 #pragma unroll
-        for (int u = 0; u < kStage; ++u) {
-            const int tl = tid + u * nthr;
-            if (tl < Lq) {
-                const int tau = q * Lq + tl;
+        for (int u = 0; u < TP; ++u) {
+            const int tl = lo + tid + u * nthr;
+            if (tl < hi) {
                 const int ps = swz<true>(tl);
-                double2 acc = rmt(par * Q + 0)[ps];
+                double2 z[Q];
+                z[0] = rmt(par * Q + 0)[ps];
 #pragma unroll
-                for (int s2 = 1; s2 < Q; ++s2)
-                    acc = cadd(acc, cmul(rmt(par * Q + s2)[ps], wL(TM, s2 * tau, L)));
-                st[u] = acc;
+                for (int s2 = 1; s2 < Q; ++s2) z[s2] = cmul(rmt(par * Q + s2)[ps], wL(TM, s2 * tl, L));
+                dft<Q, -1>(z);
+#pragma unroll
+                for (int c = 0; c < Q; ++c) st[u][c] = z[c];
             }
         }
         cluster.sync();
 #pragma unroll
-        for (int u = 0; u < kStage; ++u) {
-            const int tl = tid + u * nthr;
-            if (tl < Lq) a[swz<true>(tl)] = st[u];
+        for (int u = 0; u < TP; ++u) {
+            const int tl = lo + tid + u * nthr;
+            if (tl < hi) {
+                const int ps = swz<true>(tl);
+#pragma unroll
+                for (int c = 0; c < Q; ++c) rmt(par * Q + c)[ps] = st[u][c];
+            }
         }
     }
     cluster.sync();
@@ -407,29 +407,50 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     cluster.sync();
     SK_PROBE_L(8);
 
-    // ---- 6. inverse radix-Q split: u_t' = w_L^(+q t') sum_s x_(t' + s Lq) w_Q^(+q s),
-    // written to digit-reversed slots for the DIT inverse (natural order out)
+    // ---- 6. inverse radix-Q split: u^c_tl = w_L^(+c tl) sum_s x_(tl + s Lq) w_Q^(+c s),
+    // again one distributed butterfly per tl (contiguous DSMEM reads and
+    // writes); each CTA then permutes its slots locally into digit-reversed
+    // order for the DIT inverse (natural order out).
     {
-        double2 st[kStage];
+        constexpr int TP = kStage / Q;
+        const int lo = (q * Lq) / Q, hi = ((q + 1) * Lq) / Q;
+        double2 st[TP][Q];
 #pragma unroll
-        for (int u = 0; u < kStage; ++u) {
-            const int tl = tid + u * nthr;
-            if (tl < Lq) {
+        for (int u = 0; u < TP; ++u) {
+            const int tl = lo + tid + u * nthr;
+            if (tl < hi) {
                 const int ps = swz<true>(tl);
-                double2 acc = rmt(par * Q + 0)[ps];
+                double2 z[Q];
 #pragma unroll
-                for (int s2 = 1; s2 < Q; ++s2) {
-                    // w_Q^(+q s) = i^(q s) for Q = 4 (-1^(q s) for Q = 2), exact
-                    acc = cadd(acc, mul_ipow(rmt(par * Q + s2)[ps], (q * s2 * (4 / Q)) & 3));
-                }
-                st[u] = q == 0 ? acc : cmulc(acc, wL(TM, q * tl, L));
+                for (int s2 = 0; s2 < Q; ++s2) z[s2] = rmt(par * Q + s2)[ps];
+                dft<Q, +1>(z);
+                st[u][0] = z[0];
+#pragma unroll
+                for (int c = 1; c < Q; ++c) st[u][c] = cmulc(z[c], wL(TM, c * tl, L));
             }
         }
         cluster.sync();
 #pragma unroll
+        for (int u = 0; u < TP; ++u) {
+            const int tl = lo + tid + u * nthr;
+            if (tl < hi) {
+                const int ps = swz<true>(tl);
+#pragma unroll
+                for (int c = 0; c < Q; ++c) rmt(par * Q + c)[ps] = st[u][c];
+            }
+        }
+        cluster.sync();
+        double2 pv[kStage];
+#pragma unroll
         for (int u = 0; u < kStage; ++u) {
             const int tl = tid + u * nthr;
-            if (tl < Lq) a[swz<true>(__ldg(revq + tl))] = st[u];
+            if (tl < Lq) pv[u] = a[swz<true>(tl)];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kStage; ++u) {
+            const int tl = tid + u * nthr;
+            if (tl < Lq) a[swz<true>(__ldg(revq + tl))] = pv[u];
         }
     }
     __syncthreads();

@@ -494,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
     const int c = static_cast<int>(cluster.block_rank());
     const int L = P.fd.L, Lh = L / 2;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* tN_hi = a + Lh;
+    double2* tN_hi = a + ((Lh + 7) & ~7);  // whole 8-slot swizzle blocks
     double2* tN_lo = tN_hi + P.fd.nhi;
     double2* th_hi = tN_lo + P.fd.nlo;
     double2* th_lo = th_hi + fh.nhi;
@@ -503,16 +503,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
     const int row = rowi % P.rows_local;
     const int rhs = rowi / P.rows_local;
     const Tw TN = load_tw(P.fd, tN_hi, tN_lo, tid, nthr);  // N-th roots: w_L^(-r) = TN(2r)
+    SK_PROBE_L(14);
     const Tw TH = load_tw(fh, th_hi, th_lo, tid, nthr);
     __syncthreads();
+    SK_PROBE_L(15);
     const double2* src =
         reinterpret_cast<const double2*>(P.f + rhs * P.in_rhs_stride + static_cast<long long>(row) * P.g.N);
-    for (int r = tid; r < Lh; r += nthr) {
-        const double2 z0 = __ldg(src + r), z1 = __ldg(src + r + Lh);
-        a[r] = c == 0 ? cadd(z0, z1) : cmul(csub(z0, z1), TN(2 * r));
+    // (XOR-swizzled slots: the power-of-two transforms of C5 otherwise hit
+    // one bank per butterfly; loads in batches of kLoadU per thread)
+    constexpr int kLoadU = 8;
+    for (int r0 = tid; r0 < Lh; r0 += kLoadU * nthr) {
+        double2 z0[kLoadU], z1[kLoadU];
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int r = r0 + u * nthr;
+            if (r < Lh) {
+                z0[u] = __ldg(src + r);
+                z1[u] = __ldg(src + r + Lh);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int r = r0 + u * nthr;
+            if (r < Lh) a[swz<true>(r)] = c == 0 ? cadd(z0[u], z1[u]) : cmul(csub(z0[u], z1[u]), TN(2 * r));
+        }
     }
     __syncthreads();
-    fft_forward(a, fh, TH, tid, nthr);  // Z_(2m+c) at rev_h(m)
+    SK_PROBE_L(16);
+    fft_forward<true>(a, fh, TH, tid, nthr);  // Z_(2m+c) at swz(rev_h(m))
+    SK_PROBE_L(17);
     const double invN = 1.0 / P.g.N;
     double2* out = P.spec + rhs * P.out_rhs_stride;
     const int* revh = fh.rev;
@@ -521,8 +540,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
         const int k = 2 * m + c;
         const int km = L - k;
         const int mk = m, mkm = (km == L) ? 0 : (km - c) / 2;
-        const double2 z = a[__ldg(revh + mk)];
-        const double2 zp = a[__ldg(revh + mkm)];
+        const double2 z = a[swz<true>(__ldg(revh + mk))];
+        const double2 zp = a[swz<true>(__ldg(revh + mkm))];
         const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
         const double2 Xk = cadd(A, cmul(TN(k), B));
@@ -537,6 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
             if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = vm;
         }
     }
+    SK_PROBE_L(18);
     cluster.sync();
 }
 
@@ -551,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
     const int c = static_cast<int>(cluster.block_rank());
     const int L = P.fd.L, Lh = L / 2;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* tN_hi = a + Lh;
+    double2* tN_hi = a + ((Lh + 7) & ~7);  // whole 8-slot swizzle blocks
     double2* tN_lo = tN_hi + P.fd.nhi;
     double2* th_hi = tN_lo + P.fd.nlo;
     double2* th_lo = th_hi + fh.nhi;
@@ -560,8 +580,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
     const int row = rowi % P.rows_local;
     const int rhs = rowi / P.rows_local;
     const Tw TN = load_tw(P.fd, tN_hi, tN_lo, tid, nthr);
+    SK_PROBE_L(19);
     const Tw TH = load_tw(fh, th_hi, th_lo, tid, nthr);
     __syncthreads();
+    SK_PROBE_L(20);
     const double2* in = P.spec + rhs * P.in_rhs_stride;
     const int* revh = fh.rev;
     for (int m = tid; 2 * m + c <= L / 2; m += nthr) {
@@ -578,24 +600,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
         {
             const double2 E = make_double2(v.x + w.x, v.y - w.y);
             const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), TN(k));
-            a[__ldg(revh + m)] = make_double2(E.x - O.y, E.y + O.x);
+            a[swz<true>(__ldg(revh + m))] = make_double2(E.x - O.y, E.y + O.x);
         }
         if (k != 0 && km != k) {
             const double2 E = make_double2(w.x + v.x, w.y - v.y);
             const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), TN(km));
-            a[__ldg(revh + (km - c) / 2)] = make_double2(E.x - O.y, E.y + O.x);
+            a[swz<true>(__ldg(revh + (km - c) / 2))] = make_double2(E.x - O.y, E.y + O.x);
         }
     }
     __syncthreads();
-    fft_inverse(a, fh, TH, tid, nthr);  // W^c_j natural, j < L/2
+    SK_PROBE_L(21);
+    fft_inverse<true>(a, fh, TH, tid, nthr);  // W^c_j natural at swz(j), j < L/2
+    SK_PROBE_L(22);
     cluster.sync();
     const double2* w0 = cluster.map_shared_rank(a, 0);
     const double2* w1 = cluster.map_shared_rank(a, 1);
     double2* dst = reinterpret_cast<double2*>(P.u + rhs * P.out_rhs_stride + static_cast<long long>(row) * P.g.N);
     for (int jj = tid; jj < Lh; jj += nthr) {
         const int j = c * Lh + jj;  // z_j = W0_(j mod L/2) + w_L^(+j) W1_(j mod L/2)
-        dst[j] = cadd(w0[jj], cmulc(w1[jj], TN(2 * j)));
+        dst[j] = cadd(w0[swz<true>(jj)], cmulc(w1[swz<true>(jj)], TN(2 * j)));
     }
+    SK_PROBE_L(23);
     cluster.sync();
 }
 

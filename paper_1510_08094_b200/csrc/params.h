@@ -106,7 +106,7 @@ inline size_t theta_large_smem_bytes(int Lq, int nhiM, int nloM, int nhiq, int n
            static_cast<size_t>((Lq + 4 + 1) & ~1) * 8 + 32 * 32 + 2 * 32 + 16 * 16 + 64 * 8 + 16;
 }
 inline size_t lambda_split_smem_bytes(int Lh, int nhiN, int nloN, int nhih, int nloh) {
-    return static_cast<size_t>(Lh) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16;
+    return static_cast<size_t>((Lh + 7) & ~7) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16;
 }
 cudaError_t launch_theta_large(const ThetaLargeParams& P, int Q, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);

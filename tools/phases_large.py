@@ -32,3 +32,14 @@ tot = a[:, 13] - a[:, 0]
 print(f"{cfg.name}: mean cycles per CTA {tot.mean():.0f}")
 for i in range(13):
     print(f"  {names[i + 1]:32s} {d[:, i].mean():9.0f} cyc  {100 * d[:, i].mean() / tot.mean():5.1f}%")
+
+# lambda split kernels (probes 14..18 forward, 19..23 inverse; the first 4096 CTAs)
+b = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 24).astype(np.int64)
+for nm, cols, labels in [("lambda_fwd_split", range(14, 19), ["setup + twiddles N", "twiddles h + row loads", "fft", "split + scattered stores"]),
+                         ("lambda_inv_split", list(range(19, 24)), ["setup + twiddles N", "twiddles h + gathers + pack", "fft inv", "DSMEM recombine + row stores"])]:
+    c = list(cols)
+    dd = np.diff(b[:, c], axis=1)
+    t = b[:, c[-1]] - b[:, c[0]]
+    print(f"{nm}: mean cycles per CTA {t.mean():.0f} (to the last probe)")
+    for i, lab in enumerate(labels):
+        print(f"  {lab:32s} {dd[:, i].mean():9.0f} cyc  {100 * dd[:, i].mean() / t.mean():5.1f}%")

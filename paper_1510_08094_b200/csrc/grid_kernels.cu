@@ -52,6 +52,9 @@ constexpr int kLamPairs = 12;  // mode pairs per thread held in registers
 // One CTA per physical row: TMA bulk load of the real row (N/2 complex
 // pairs), forward DIF FFT, split into the N/2+1 modes of the real transform
 // with analyze_1d's (-1)^k / N (fourier.cpp:44-51), stored mode-major.
+// SWZ (power-of-two rows, C2/C4): XOR-swizzled slots, filled by per-thread
+// loads instead of the bulk copy (the bulk copy lands elements in order).
+template <bool SWZ>
 __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
@@ -66,26 +69,31 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
     const int rhs = blockIdx.x / P.rows_local;
     const double2* src =
         reinterpret_cast<const double2*>(P.f + rhs * P.in_rhs_stride + static_cast<long long>(row) * P.g.N);
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
-        bulk_g2s_chunked(a, src, static_cast<uint32_t>(L) * 16, bar);  // the real row as N/2 complex pairs
+    if constexpr (!SWZ) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
+            bulk_g2s_chunked(a, src, static_cast<uint32_t>(L) * 16, bar);  // the real row as N/2 complex pairs
+        }
+    } else {
+#pragma unroll 4
+        for (int i = tid; i < L; i += nthr) a[swz<true>(i)] = __ldg(src + i);
     }
     // twiddles and the digit-reversal table by the threads while the row is in
     // flight (measured faster here than adding them to the bulk copies)
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();
-    mbar_wait(bar, 0);
-    fft_forward(a, P.fd, T, tid, nthr);
+    if constexpr (!SWZ) mbar_wait(bar, 0);
+    fft_forward<SWZ>(a, P.fd, T, tid, nthr);
     const double invN = 1.0 / P.g.N;
     double2* out = P.spec + rhs * P.out_rhs_stride;
     (void)tmap;  // scattered fire-and-forget stores measured faster than staged TMA tensor stores here
     for (int k = tid; k <= L / 2; k += nthr) {
         const int km = L - k;  // partner mode
-        const double2 z = a[s_rev[k]];
-        const double2 zp = a[s_rev[km == L ? 0 : km]];
+        const double2 z = a[swz<SWZ>(s_rev[k])];
+        const double2 zp = a[swz<SWZ>(s_rev[km == L ? 0 : km])];
         // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
         const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
@@ -107,6 +115,7 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
 // spectrum; sample_grid's (-1)^k (fourier.cpp:61-62) and the packing into
 // N/2 complex go through registers into digit-reversed order; inverse DIT
 // FFT; the real row is stored (unnormalised, as FFTW_BACKWARD).
+template <bool SWZ>
 __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
@@ -166,14 +175,14 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
         const int k = tid + u * nthr;
         if (k <= L / 2) {
             const int km = L - k;
-            a[s_rev[k]] = zk[u];
-            if (k != 0 && km != k) a[s_rev[km]] = zm[u];
+            a[swz<SWZ>(s_rev[k])] = zk[u];
+            if (k != 0 && km != k) a[swz<SWZ>(s_rev[km])] = zm[u];
         }
     }
     __syncthreads();
-    fft_inverse(a, P.fd, T, tid, nthr);
+    fft_inverse<SWZ>(a, P.fd, T, tid, nthr);
     double2* dst = reinterpret_cast<double2*>(P.u + rhs * P.out_rhs_stride + static_cast<long long>(row) * P.g.N);
-    for (int j = tid; j < L; j += nthr) dst[j] = a[j];
+    for (int j = tid; j < L; j += nthr) dst[j] = a[swz<SWZ>(j)];
 }
 
 // -------------------------------------------------------------- theta stage
@@ -1084,24 +1093,34 @@ __global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
 }
 
 // --------------------------------------------------------- host launchers
-cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+template <bool SWZ>
+static cudaError_t launch_lambda_fwd_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
+                                       cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(lambda_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(lambda_fwd_kernel<SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_fwd_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
+    lambda_fwd_kernel<SWZ><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
+cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    return P.swizzle ? launch_lambda_fwd_t<true>(P, map, nthr, smem, st) : launch_lambda_fwd_t<false>(P, map, nthr, smem, st);
+}
 
-cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+template <bool SWZ>
+static cudaError_t launch_lambda_inv_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
+                                       cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(lambda_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(lambda_inv_kernel<SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_inv_kernel<<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
+    lambda_inv_kernel<SWZ><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
+}
+cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    return P.swizzle ? launch_lambda_inv_t<true>(P, map, nthr, smem, st) : launch_lambda_inv_t<false>(P, map, nthr, smem, st);
 }
 
 template <bool SWZ, int CH>

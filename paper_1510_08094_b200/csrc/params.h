@@ -22,6 +22,7 @@ struct LambdaParams {
     double2* spec;      // fwd: output [k][p_local]; inv: input
     double* u;          // inv: real rows
     PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
+    int swizzle;        // XOR-swizzled shared-memory slots (plans whose first FFT span is even)
 };
 
 struct ThetaParams {

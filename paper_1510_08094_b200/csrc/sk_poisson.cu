@@ -723,6 +723,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
     sk::LambdaParams lp{};
     lp.g = p->g;
     lp.fd = p->fl.d;
+    lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
     lp.rows_local = rows_local;
     lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
     if (stages & 1) {
@@ -915,6 +916,7 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     sk::LambdaParams lp{};
     lp.g = p->g;
     lp.fd = p->fl.d;
+    lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
     lp.rows_local = p->g.rows;
     lp.nrhs = 1;
     lp.in_rhs_stride = 0;

@@ -255,6 +255,22 @@ def test_grid_split_kernels_rough_data(pkg, oracle, m, n):
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n", [(256, 1024), (128, 2048), (96, 512), (64, 4096)])
+def test_grid_pow2_rows_rough_data(pkg, oracle, m, n):
+    """Power-of-two lambda rows (N/2 = 256 .. 2048) run the lambda kernels on
+    XOR-swizzled slots (per-thread row loads, swizzled pack and store); rough
+    zero-mean data makes every slot of the permutation matter."""
+    rng = np.random.default_rng(7 * m + n)
+    f = rng.standard_normal((m // 2 + 1, n))
+    A = oracle.analyze_2d(oracle.dfs_double(f, m))
+    mu = (oracle.integration_weights(m) * A[:, n // 2]).sum() / 2.0
+    f = f - mu.real
+    u_ref = oracle.grid_pipeline_real(f, m, threads=8)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
 def test_slab_stages_cluster_kernels_bitwise(pkg, oracle):
     from paper_1510_08094_b200 import distributed as dist_mod, inputs
     m, n, L = 32768, 40, 12

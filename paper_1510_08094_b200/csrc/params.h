@@ -65,6 +65,7 @@ struct XformParams {
     long long ld_out;      // complex between consecutive outputs of one row (transposed store)
     const double2* src;
     double2* dst;
+    int swizzle;           // XOR-swizzled shared-memory slots (first FFT span even)
 };
 
 struct ShgenParams {

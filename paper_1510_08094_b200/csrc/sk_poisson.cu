@@ -994,7 +994,7 @@ sk_status xform_pass(sk_plan_t p, bool analyze, int nrows, int n, int n_in, long
     const DevFft* f = nullptr;
     sk_status s = xform_fft(p, n, &f);
     if (s != SK_OK) return s;
-    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst};
+    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0};
     CU(sk::launch_xform(xp, analyze, nrows, xform_threads(n), sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo), p->stream));
     return SK_OK;
 }

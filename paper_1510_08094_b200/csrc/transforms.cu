@@ -26,12 +26,14 @@ namespace sk {
 //   stored at k + n/2 (k = -n/2 .. n/2-1).
 // SYNTH (synthesize_1d, fourier.cpp:55-66): g[(k+n_out) mod n_out] = (-1)^k c_k for
 //   the modes both lengths hold, then the unnormalised backward transform.
-template <bool ANALYZE>
+// SWZ: XOR-swizzled slots (plans whose first span is even, e.g. power-of-two
+// lengths, where the butterflies of a stage otherwise share one bank).
+template <bool ANALYZE, bool SWZ>
 __global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int n = P.fd.L;  // transform length (n for ANALYZE, n_out for SYNTH)
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + n;
+    double2* s_hi = a + ((n + 7) & ~7);  // whole 8-slot swizzle blocks
     double2* s_lo = s_hi + P.fd.nhi;
     int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -40,29 +42,29 @@ __global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     for (int i = tid; i < n; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     if constexpr (ANALYZE) {
-        for (int j = tid; j < n; j += nthr) a[j] = src[j];
+        for (int j = tid; j < n; j += nthr) a[swz<SWZ>(j)] = src[j];
         __syncthreads();
-        fft_forward(a, P.fd, T, tid, nthr);  // X_t at a[rev[t]]
+        fft_forward<SWZ>(a, P.fd, T, tid, nthr);  // X_t at a[swz(rev[t])]
         const double inv = 1.0 / n;
         for (int kp = tid; kp < n; kp += nthr) {
             const int k = kp - n / 2;
             const int t = k < 0 ? k + n : k;
             const double s = (k % 2 == 0) ? inv : -inv;
-            const double2 v = a[s_rev[t]];
+            const double2 v = a[swz<SWZ>(s_rev[t])];
             P.dst[static_cast<long long>(kp) * P.ld_out + r] = make_double2(s * v.x, s * v.y);
         }
     } else {
-        for (int j = tid; j < n; j += nthr) a[j] = make_double2(0.0, 0.0);
+        for (int j = tid; j < n; j += nthr) a[swz<SWZ>(j)] = make_double2(0.0, 0.0);
         __syncthreads();
         const int lo = max(-P.n_in / 2, -n / 2), hi = min(P.n_in / 2, n / 2);
         for (int k = lo + tid; k < hi; k += nthr) {
             const double2 c = src[k + P.n_in / 2];
             const int t = k < 0 ? k + n : k;
-            a[s_rev[t]] = (k % 2 == 0) ? c : make_double2(-c.x, -c.y);  // DIT input: digit-reversed
+            a[swz<SWZ>(s_rev[t])] = (k % 2 == 0) ? c : make_double2(-c.x, -c.y);  // DIT input: digit-reversed
         }
         __syncthreads();
-        fft_inverse(a, P.fd, T, tid, nthr);  // natural order
-        for (int j = tid; j < n; j += nthr) P.dst[static_cast<long long>(j) * P.ld_out + r] = a[j];
+        fft_inverse<SWZ>(a, P.fd, T, tid, nthr);  // natural order
+        for (int j = tid; j < n; j += nthr) P.dst[static_cast<long long>(j) * P.ld_out + r] = a[swz<SWZ>(j)];
     }
 }
 
@@ -79,19 +81,26 @@ __global__ void dfs_double_kernel(int m, int n, const double* phys, double2* gri
 }
 
 size_t xform_smem_bytes(int n, int nhi, int nlo) {
-    return static_cast<size_t>(n) * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>(n) * 4;
+    return static_cast<size_t>((n + 7) & ~7) * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>(n) * 4;
 }
 
 cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(xform_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(xform_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     if (nrows <= 0) return cudaSuccess;
-    if (analyze) xform_kernel<true><<<nrows, nthr, smem, st>>>(P);
-    else xform_kernel<false><<<nrows, nthr, smem, st>>>(P);
+    if (analyze) {
+        if (P.swizzle) xform_kernel<true, true><<<nrows, nthr, smem, st>>>(P);
+        else xform_kernel<true, false><<<nrows, nthr, smem, st>>>(P);
+    } else {
+        if (P.swizzle) xform_kernel<false, true><<<nrows, nthr, smem, st>>>(P);
+        else xform_kernel<false, false><<<nrows, nthr, smem, st>>>(P);
+    }
     return cudaGetLastError();
 }
 

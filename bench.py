@@ -404,10 +404,12 @@ def main():
         dom = max(stage, key=stage.get)
         achieved = bytes_stage[dom] / (stage[dom] * 1e-3) / 1e9
         tr = None
+        prof = {}
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             with open(tp) as fh:
-                tr = json.load(fh).get(cfg.name, {}).get(dom.replace("_ms", ""))
+                prof = json.load(fh).get(cfg.name, {})
+            tr = prof.get(dom.replace("_ms", ""))
         roof = {"bound": "hbm", "kernel": dom.replace("_ms", ""), "achieved": achieved, "peak": hbm_peak,
                 "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": tr, "peak_kind": peak_kind,
                 "stage_ms": stage, "stage_share": {k: v / sum(stage.values()) for k, v in stage.items()},
@@ -415,6 +417,12 @@ def main():
                 "pipeline_frac": sum(bytes_stage.values()) / (ms_step * 1e-3) / 1e9 / hbm_peak,
                 "canonical_bytes_per_step": (64 * cfg.M * cfg.N + 16 * R * cfg.N) * cfg.nrhs,
                 "canonical_frac": (64 * cfg.M * cfg.N + 16 * R * cfg.N) * cfg.nrhs / (ms_step * 1e-3) / 1e9 / (hbm_peak * world)}
+        if dom == "theta_ms" and "theta_fp64_pipe" in prof:
+            # the theta stage is not HBM-bound: its ncu profile (profiles/) shows
+            # the FP64 pipe and shared memory near 30 % at 16 warps/SM (latency)
+            roof["theta_profile"] = {"fp64_pipe_frac": prof["theta_fp64_pipe"],
+                                     "warps_per_sm": prof.get("theta_warps_per_sm"),
+                                     "note": "latency-bound; ncu --set full, profiles/r1_phases_and_ab.md"}
     line = {
         "metric": "sphere Poisson DOF/s (FP64)", "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -311,51 +311,57 @@ __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, c
     }
 }
 
-template <bool DIF, int SIGN, bool SWZ>
+// MAXR: largest radix the caller's plans use (kernels compiled for a small
+// register budget only instantiate the small radices).
+template <bool DIF, int SIGN, bool SWZ, int MAXR = 25>
 __device__ __forceinline__ void fft_stage_dispatch(double2* a, const FftDesc& d, int s, const Tw& T, int tid,
                                                    int nthr) {
-    switch (d.R[s]) {
-        case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 8: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 10: fft_stage<10, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 16: fft_stage<16, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        case 20: fft_stage<20, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-        default: fft_stage<25, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+    if constexpr (MAXR > 8) {
+        switch (d.R[s]) {
+            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 8: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 10: fft_stage<10, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 16: fft_stage<16, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 20: fft_stage<20, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            default: fft_stage<25, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        }
+    } else {  // plans built with radices <= 8 (the plan checks this)
+        switch (d.R[s]) {
+            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            default: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+        }
     }
 }
 
-// Whole transforms (callers __syncthreads() before; each ends with a barrier).
-// DIF stages run s = 0..nst-1 and take natural order to digit-reversed order;
-// DIT stages run s = nst-1..0 and take digit-reversed order to natural order.
-//   fft_forward      DIF, exp(-):  natural -> reversed   (lambda forward)
-//   fft_inverse      DIT, exp(+):  reversed -> natural   (lambda inverse)
-//   fft_forward_dit  DIT, exp(-):  reversed -> natural   (theta forward)
-//   fft_inverse_dif  DIF, exp(+):  natural -> reversed   (theta inverse)
-template <bool DIF, int SIGN, bool SWZ>
+template <bool DIF, int SIGN, bool SWZ, int MAXR = 25>
 __device__ __forceinline__ void fft_run(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
     if constexpr (DIF) {
         for (int s = 0; s < d.nst; ++s) {
-            fft_stage_dispatch<true, SIGN, SWZ>(a, d, s, T, tid, nthr);
+            fft_stage_dispatch<true, SIGN, SWZ, MAXR>(a, d, s, T, tid, nthr);
             __syncthreads();
         }
     } else {
         for (int s = d.nst - 1; s >= 0; --s) {
-            fft_stage_dispatch<false, SIGN, SWZ>(a, d, s, T, tid, nthr);
+            fft_stage_dispatch<false, SIGN, SWZ, MAXR>(a, d, s, T, tid, nthr);
             __syncthreads();
         }
     }
 }
-template <bool SWZ = false>
+template <bool SWZ = false, int MAXR = 25>
 __device__ __forceinline__ void fft_forward(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<true, -1, SWZ>(a, d, T, tid, nthr);
+    fft_run<true, -1, SWZ, MAXR>(a, d, T, tid, nthr);
 }
-template <bool SWZ = false>
+template <bool SWZ = false, int MAXR = 25>
 __device__ __forceinline__ void fft_inverse(double2* a, const FftDesc& d, const Tw& T, int tid, int nthr) {
-    fft_run<false, +1, SWZ>(a, d, T, tid, nthr);
+    fft_run<false, +1, SWZ, MAXR>(a, d, T, tid, nthr);
 }
 
 // Stage the 2L-th-root twiddle tables of `d` into shared memory.

@@ -474,7 +474,7 @@ __device__ __forceinline__ unsigned launder(unsigned x) {
 #ifndef SK_CHAIN_ATTR
 #define SK_CHAIN_ATTR __noinline__
 #endif
-template <int S>
+template <int S, bool HI>
 __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict__ rev, const double* ip, Aff3* wsc,
                                                  const Chain& ch, int L, double2 inner, unsigned* fmax_hi,
                                                  double2* wsum, bool want_wsum, double2* x_first) {
@@ -618,10 +618,11 @@ __device__ __forceinline__ int chain_segment(int n, int nthr) {
     return 0;
 }
 
+template <bool HI>
 __device__ __forceinline__ bool solve_chain_fast_dispatch(double2* a, const int* rev, const double* ip, Aff3* wsc,
                                                           const Chain& ch, int L, double2 inner, unsigned* fmax_hi,
                                                           double2* wsum, bool want_wsum, double2* x_first) {
-#define SK_CH(S) solve_chain_fast<S>(a, rev, ip, wsc, ch, L, inner, fmax_hi, wsum, want_wsum, x_first)
+#define SK_CH(S) solve_chain_fast<S, HI>(a, rev, ip, wsc, ch, L, inner, fmax_hi, wsum, want_wsum, x_first)
     switch (chain_segment(ch.n, blockDim.x)) {
         case 2: SK_CH(2); return true;
         case 4: SK_CH(4); return true;
@@ -766,8 +767,12 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
 // CH selects the chain solver at compile time (one per kernel so that the
 // register allocation of each is independent): 0 shared-memory walk,
 // 1 fixed short segments (solve_chain_fast), 2 SMAX = 12 register walk.
-template <bool SWZ, int CH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(ThetaParams P) {
+// HI: high-occupancy variant for short columns (<= 256 threads per CTA, radices
+// <= 8): 64 registers per thread, so twice the CTAs per SM hide the latency of
+// a transform that gives each thread only one or two butterflies per stage.
+template <bool SWZ, int CH, bool HI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) theta_kernel(ThetaParams P) {
+    constexpr int kFold = HI ? kFoldMaxHi : kFoldMax;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int L = P.fd.L;  // M/2
@@ -844,9 +849,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     // so no slot is overwritten before it is read); otherwise in place.
     const double invM = 1.0 / P.g.M;
     if constexpr (SWZ) {
-        double2 v0[kFoldMax], v1[kFoldMax];
+        double2 v0[kFold], v1[kFold];
 #pragma unroll
-        for (int u = 0; u < kFoldMax; ++u) {
+        for (int u = 0; u < kFold; ++u) {
             const int r = tid + u * nthr;
             if (r <= L / 2) {
                 const int rm = L - r;
@@ -863,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < kFoldMax; ++u) {
+        for (int u = 0; u < kFold; ++u) {
             const int r = tid + u * nthr;
             if (r <= L / 2) {
                 const int rm = L - r;
@@ -890,7 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     }
     __syncthreads();
     SK_PROBE(2);
-    fft_forward<SWZ>(a, P.fd, T, tid, nthr);
+    fft_forward<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);
     SK_PROBE(3);
 
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)
@@ -948,7 +953,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
             if (reg12) solve_chain_reg<kSegMax>(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
             else solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
         } else if constexpr (CH == 1) {
-            if (!solve_chain_fast_dispatch(a, rev, ipc, wsc3, ch, L, inner, &fmax_hi, &wsum, want_wsum, xf))
+            if (!solve_chain_fast_dispatch<HI>(a, rev, ipc, wsc3, ch, L, inner, &fmax_hi, &wsum, want_wsum, xf))
                 solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
         } else {
             solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
@@ -1005,7 +1010,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512) theta_kernel(Th
     __syncthreads();
 
     SK_PROBE(7);
-    fft_inverse<SWZ>(a, P.fd, T, tid, nthr);
+    fft_inverse<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);
     SK_PROBE(8);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
@@ -1123,20 +1128,22 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
     return P.swizzle ? launch_lambda_inv_t<true>(P, map, nthr, smem, st) : launch_lambda_inv_t<false>(P, map, nthr, smem, st);
 }
 
-template <bool SWZ, int CH>
+template <bool SWZ, int CH, bool HI = false>
 static cudaError_t launch_theta_t(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(theta_kernel<SWZ, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(theta_kernel<SWZ, CH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr = true;
     }
-    theta_kernel<SWZ, CH><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
     return cudaGetLastError();
 }
 
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
     const int ch = P.regsolve;  // chain solver chosen by the plan
+    if (P.hiocc && ch == 1 && nthr <= 256)  // short columns (plan: radices <= 8, fixed-segment chains)
+        return P.swizzle ? launch_theta_t<true, 1, true>(P, nthr, smem, st) : launch_theta_t<false, 1, true>(P, nthr, smem, st);
     if (P.swizzle) {
         if (ch == 2) return launch_theta_t<true, 2>(P, nthr, smem, st);
         if (ch == 1) return launch_theta_t<true, 1>(P, nthr, smem, st);

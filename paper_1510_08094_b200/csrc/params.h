@@ -43,6 +43,7 @@ struct ThetaParams {
     int piv_stride;        // doubles per (mode, parity) pivot row
     PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
     int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
+    int hiocc;             // high-occupancy kernel variant (short columns: 64 registers, radices <= 8)
 };
 
 struct AssembleParams {

@@ -58,13 +58,13 @@ void search_radices(int m, int nthr, int L, int maxr, std::vector<int>& cur, dou
     }
 }
 
-bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = false) {
+bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = false, int maxr_plan = 25) {
     R.clear();
     if (L < 1) return false;
     if (L == 1) return true;
     std::vector<int> cur;
     double best = 1e300;
-    int maxr = 25;  // largest register radix (SK_MAXRADIX: A/B switch)
+    int maxr = maxr_plan;  // largest register radix (SK_MAXRADIX: A/B switch)
     if (const char* e = std::getenv("SK_MAXRADIX")) maxr = std::atoi(e);
     if (odd_first_span) {
         // First radix takes every factor of two, so consecutive natural indices
@@ -72,7 +72,7 @@ bool factor_radices(int L, int nthr, std::vector<int>& R, bool odd_first_span = 
         // warp walking consecutive chain elements spreads over all banks.
         int p2 = 1;
         while (L % (2 * p2) == 0) p2 *= 2;
-        if (p2 > 1 && p2 <= 16 && L / p2 > 1) {
+        if (p2 > 1 && p2 <= 16 && p2 <= maxr && L / p2 > 1) {
             const long long nb = L / p2;
             cur.push_back(p2);
             search_radices(L / p2, nthr, L, maxr, cur, static_cast<double>((nb + nthr - 1) / nthr) * (p2 + 6) + 30,
@@ -103,9 +103,9 @@ void root(long long m, long long n, double& c, double& s) {
     s = static_cast<double>(-sinl(a));
 }
 
-sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, bool swizzle = false) {
+sk_status build_fft(int L, int nthr, DevFft& out, bool odd_first_span = false, bool swizzle = false, int maxr = 25) {
     std::vector<int> R;
-    if (!factor_radices(L, nthr, R, odd_first_span)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
+    if (!factor_radices(L, nthr, R, odd_first_span, maxr)) return fail(SK_ERR_UNSUPPORTED, "FFT length " + std::to_string(L) + " has prime factors > 7");
     sk::FftDesc& d = out.d;
     d.L = L;
     d.nst = static_cast<int>(R.size());
@@ -298,6 +298,7 @@ struct sk_plan_s {
     double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
     int piv_stride = 0;        // doubles per pivot-table row
+    bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
@@ -464,10 +465,17 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     p->thr_theta = round_threads(Lt / 8, 64, 512);
     const bool odd_t = !std::getenv("SK_ODDSPAN_THETA") || std::atoi(std::getenv("SK_ODDSPAN_THETA")) != 0;
     const bool odd_l = !std::getenv("SK_ODDSPAN_LAMBDA") || std::atoi(std::getenv("SK_ODDSPAN_LAMBDA")) != 0;
-    if (p->grid_ok && (s = build_fft(Lt, p->thr_theta, p->ft, odd_t, true)) != SK_OK) {
+    // short columns (<= 256 threads per CTA) run the high-occupancy theta
+    // variant: 64 registers per thread, register radices <= 8, fold and
+    // chains within its per-thread limits (SK_NO_HIOCC: A/B switch)
+    p->theta_hiocc = p->thr_theta <= 256 && (Lt / 2 + 1) <= 6 * p->thr_theta /* kFoldMaxHi */ &&
+                     (Lt / 2 + 1) <= 6 * p->thr_theta && !std::getenv("SK_NO_HIOCC");
+    if (p->grid_ok && (s = build_fft(Lt, p->thr_theta, p->ft, odd_t, true, p->theta_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
+    for (int st = 0; p->theta_hiocc && st < p->ft.d.nst; ++st)
+        if (p->ft.d.R[st] > 8) p->theta_hiocc = false;  // the variant only instantiates radices <= 8
     if (p->grid_ok) {
         p->smem_theta = sk::theta_smem_bytes(Lt, p->ft.d.nhi, p->ft.d.nlo);
         // stage the chains' digit-reversal entries in shared memory when they fit
@@ -759,6 +767,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
         tp.regsolve = p->chain_mode;
+        tp.hiocc = p->theta_hiocc ? 1 : 0;
         tp.rev_win = p->theta_q ? 0 : p->rev_win;
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes

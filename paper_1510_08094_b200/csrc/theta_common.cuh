@@ -40,6 +40,7 @@ __device__ __forceinline__ int t_of(int tau, int par, int L) {
 // i-1 (towards j = 0) and i+1 (towards the truncation boundary).
 constexpr int kSegMax = 12;  // register-resident chain segment length per thread
 constexpr int kFoldMax = 12;  // column pairs per thread in the fold
+constexpr int kFoldMaxHi = 6;  // same, high-occupancy theta variant
 
 struct Chain {
     int n;       // length

@@ -463,6 +463,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // theta stage: one CTA pair per mode when a parity half fits shared
     // memory, else a cluster of 2Q CTAs (Q = 4) holding quarters
     p->thr_theta = round_threads(Lt / 8, 64, 512);
+    if (const char* e = std::getenv("SK_THETA_THREADS")) p->thr_theta = round_threads(std::atoi(e), 64, 512);  // A/B
     const bool odd_t = !std::getenv("SK_ODDSPAN_THETA") || std::atoi(std::getenv("SK_ODDSPAN_THETA")) != 0;
     const bool odd_l = !std::getenv("SK_ODDSPAN_LAMBDA") || std::atoi(std::getenv("SK_ODDSPAN_LAMBDA")) != 0;
     // short columns (<= 256 threads per CTA) run the high-occupancy theta

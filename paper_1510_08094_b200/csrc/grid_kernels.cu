@@ -47,15 +47,18 @@ __device__ unsigned long long g_phase[4096][24];
 // Box of the spectrum tensor map: 256 lambda modes x one physical row
 // (2 doubles), i.e. the strided [k][p] column slice of one row.
 constexpr int kBoxModes = 256;
-constexpr int kLamPairs = 12;  // mode pairs per thread held in registers
+constexpr int kLamPairs = 12;   // mode pairs per thread held in registers
+constexpr int kLamPairsHi = 6;  // same, high-occupancy lambda variant
 
 // One CTA per physical row: TMA bulk load of the real row (N/2 complex
 // pairs), forward DIF FFT, split into the N/2+1 modes of the real transform
 // with analyze_1d's (-1)^k / N (fourier.cpp:44-51), stored mode-major.
 // SWZ (power-of-two rows, C2/C4): XOR-swizzled slots, filled by per-thread
 // loads instead of the bulk copy (the bulk copy lands elements in order).
-template <bool SWZ>
-__global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+// HI: high-occupancy variant for short rows (<= 128 threads per CTA, radices
+// <= 8): 64 registers per thread, twice the CTAs per SM.
+template <bool SWZ, bool HI>
+__global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
     const int Lpad = (L / kBoxModes + 1) * kBoxModes;  // >= L+1, whole boxes
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
     for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
     __syncthreads();
     if constexpr (!SWZ) mbar_wait(bar, 0);
-    fft_forward<SWZ>(a, P.fd, T, tid, nthr);
+    fft_forward<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);
     const double invN = 1.0 / P.g.N;
     double2* out = P.spec + rhs * P.out_rhs_stride;
     (void)tmap;  // scattered fire-and-forget stores measured faster than staged TMA tensor stores here
@@ -115,8 +118,9 @@ __global__ void __launch_bounds__(256, 2) lambda_fwd_kernel(LambdaParams P, cons
 // spectrum; sample_grid's (-1)^k (fourier.cpp:61-62) and the packing into
 // N/2 complex go through registers into digit-reversed order; inverse DIT
 // FFT; the real row is stored (unnormalised, as FFTW_BACKWARD).
-template <bool SWZ>
-__global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+template <bool SWZ, bool HI>
+__global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int kPairs = HI ? kLamPairsHi : kLamPairs;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = P.fd.L;
     const int Lpad = (L / kBoxModes + 1) * kBoxModes;
@@ -142,9 +146,9 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
     const Tw T{s_hi, s_lo, P.fd.shift, (1 << P.fd.shift) - 1};
     __syncthreads();
     mbar_wait(bar, 0);
-    double2 zk[kLamPairs], zm[kLamPairs];
+    double2 zk[kPairs], zm[kPairs];
 #pragma unroll
-    for (int u = 0; u < kLamPairs; ++u) {
+    for (int u = 0; u < kPairs; ++u) {
         const int k = tid + u * nthr;
         if (k <= L / 2) {
             const int km = L - k;
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < kLamPairs; ++u) {
+    for (int u = 0; u < kPairs; ++u) {
         const int k = tid + u * nthr;
         if (k <= L / 2) {
             const int km = L - k;
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(256, 2) lambda_inv_kernel(LambdaParams P, cons
         }
     }
     __syncthreads();
-    fft_inverse<SWZ>(a, P.fd, T, tid, nthr);
+    fft_inverse<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);
     double2* dst = reinterpret_cast<double2*>(P.u + rhs * P.out_rhs_stride + static_cast<long long>(row) * P.g.N);
     for (int j = tid; j < L; j += nthr) dst[j] = a[swz<SWZ>(j)];
 }
@@ -1098,34 +1102,42 @@ __global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
 }
 
 // --------------------------------------------------------- host launchers
-template <bool SWZ>
+template <bool SWZ, bool HI>
 static cudaError_t launch_lambda_fwd_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
                                        cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(lambda_fwd_kernel<SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(lambda_fwd_kernel<SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_fwd_kernel<SWZ><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
+    lambda_fwd_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
-    return P.swizzle ? launch_lambda_fwd_t<true>(P, map, nthr, smem, st) : launch_lambda_fwd_t<false>(P, map, nthr, smem, st);
+    if (P.hiocc)
+        return P.swizzle ? launch_lambda_fwd_t<true, true>(P, map, nthr, smem, st)
+                         : launch_lambda_fwd_t<false, true>(P, map, nthr, smem, st);
+    return P.swizzle ? launch_lambda_fwd_t<true, false>(P, map, nthr, smem, st)
+                     : launch_lambda_fwd_t<false, false>(P, map, nthr, smem, st);
 }
 
-template <bool SWZ>
+template <bool SWZ, bool HI>
 static cudaError_t launch_lambda_inv_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
                                        cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(lambda_inv_kernel<SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(lambda_inv_kernel<SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    lambda_inv_kernel<SWZ><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
+    lambda_inv_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
-    return P.swizzle ? launch_lambda_inv_t<true>(P, map, nthr, smem, st) : launch_lambda_inv_t<false>(P, map, nthr, smem, st);
+    if (P.hiocc)
+        return P.swizzle ? launch_lambda_inv_t<true, true>(P, map, nthr, smem, st)
+                         : launch_lambda_inv_t<false, true>(P, map, nthr, smem, st);
+    return P.swizzle ? launch_lambda_inv_t<true, false>(P, map, nthr, smem, st)
+                     : launch_lambda_inv_t<false, false>(P, map, nthr, smem, st);
 }
 
 template <bool SWZ, int CH, bool HI = false>

@@ -23,6 +23,7 @@ struct LambdaParams {
     double* u;          // inv: real rows
     PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
     int swizzle;        // XOR-swizzled shared-memory slots (plans whose first FFT span is even)
+    int hiocc;          // high-occupancy kernel variant (short rows: 64 registers, radices <= 8)
 };
 
 struct ThetaParams {

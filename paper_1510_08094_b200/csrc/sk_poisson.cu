@@ -299,6 +299,7 @@ struct sk_plan_s {
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
     int piv_stride = 0;        // doubles per pivot-table row
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
+    bool lambda_hiocc = false; // high-occupancy lambda kernel variant (short rows)
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
@@ -507,10 +508,15 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // lambda stages: one CTA per row, or a CTA pair splitting the row by parity
     // (odd first span: the digit-reversed split/pack walks spread over all banks)
     p->thr_lambda = round_threads(Ll / 8, 64, 256);
-    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l)) != SK_OK) {
+    // short rows (<= 128 threads per CTA) run the high-occupancy lambda variant
+    // (64 registers, radices <= 8, <= 6 mode pairs per thread; SK_NO_HIOCC)
+    p->lambda_hiocc = p->thr_lambda <= 128 && (Ll / 2 + 1) <= 6 * p->thr_lambda && !std::getenv("SK_NO_HIOCC");
+    if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
     }
+    for (int st = 0; p->lambda_hiocc && st < p->fl.d.nst; ++st)
+        if (p->fl.d.R[st] > 8) p->lambda_hiocc = false;
     if (p->grid_ok) {
         p->smem_lambda = sk::lambda_smem_bytes(Ll, p->fl.d.nhi, p->fl.d.nlo);
         const bool fits = p->smem_lambda <= cap && (Ll / 2 + 1) <= 12 * p->thr_lambda;
@@ -733,6 +739,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
     lp.g = p->g;
     lp.fd = p->fl.d;
     lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
+    lp.hiocc = p->lambda_hiocc && !p->lambda_split ? 1 : 0;
     lp.rows_local = rows_local;
     lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
     if (stages & 1) {
@@ -927,6 +934,7 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     lp.g = p->g;
     lp.fd = p->fl.d;
     lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
+    lp.hiocc = p->lambda_hiocc && !p->lambda_split ? 1 : 0;
     lp.rows_local = p->g.rows;
     lp.nrhs = 1;
     lp.in_rhs_stride = 0;

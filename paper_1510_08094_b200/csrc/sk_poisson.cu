@@ -662,6 +662,10 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     info[10] = static_cast<long long>(p->smem_theta);
     info[11] = static_cast<long long>(p->smem_lambda);
     info[12] = p->chain_mode;
+    const bool swz_t = p->ft.d.nst > 0 && p->ft.d.span[0] % 2 == 0;
+    const bool swz_l = p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0;
+    info[13] = (p->theta_hiocc && !p->theta_q && p->chain_mode == 1 && p->thr_theta <= 256 ? 1 : 0) |
+               (p->lambda_hiocc && !p->lambda_split ? 2 : 0) | (swz_t ? 4 : 0) | (swz_l ? 8 : 0);
     return SK_OK;
 }
 

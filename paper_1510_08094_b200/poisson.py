@@ -117,7 +117,7 @@ class Plan:
         a = (ctypes.c_longlong * 16)()
         _lib.check(self.lib.sk_plan_info(self._h, a))
         keys = ["M", "N", "nrhs", "device", "grid_ok", "rows", "theta_split", "theta_threads", "lambda_threads",
-                "last_launches", "theta_smem", "lambda_smem", "chain_solver"]
+                "last_launches", "theta_smem", "lambda_smem", "chain_solver", "variants"]
         return {k: int(a[i]) for i, k in enumerate(keys)}
 
     @property

@@ -255,6 +255,16 @@ def test_grid_split_kernels_rough_data(pkg, oracle, m, n):
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n,theta_hi,lambda_hi", [(2048, 1024, True, True), (4096, 2048, True, True),
+                                                     (20000, 10000, False, False), (512, 256, True, True)])
+def test_plan_kernel_variants(pkg, m, n, theta_hi, lambda_hi):
+    """Short columns / rows select the high-occupancy kernel variants (C4,
+    C2, C1); the paper-scale plan keeps the 128-register kernels."""
+    with pkg.Plan(m, n) as plan:
+        v = plan.info()["variants"]
+    assert bool(v & 1) == theta_hi and bool(v & 2) == lambda_hi, v
+
+
 @pytest.mark.parametrize("m,n", [(256, 1024), (128, 2048), (96, 512), (64, 4096)])
 def test_grid_pow2_rows_rough_data(pkg, oracle, m, n):
     """Power-of-two lambda rows (N/2 = 256 .. 2048) run the lambda kernels on

@@ -68,6 +68,7 @@ struct XformParams {
     const double2* src;
     double2* dst;
     int swizzle;           // XOR-swizzled shared-memory slots (first FFT span even)
+    int hiocc;             // high-occupancy variant (<= 256 threads: 64 registers, radices <= 8)
 };
 
 struct ShgenParams {

@@ -997,7 +997,9 @@ sk_status xform_fft(sk_plan_t p, int n, const DevFft** out) {
     auto it = p->xf.find(n);
     if (it == p->xf.end()) {
         DevFft f;
-        sk_status s = build_fft(n, xform_threads(n), f);
+        // <= 256 threads: high-occupancy kernel variant, register radices <= 8
+        const bool hi = xform_threads(n) <= 256 && !std::getenv("SK_NO_HIOCC");
+        sk_status s = build_fft(n, xform_threads(n), f, false, false, hi ? 8 : 25);
         if (s != SK_OK) return s;
         if (sk::xform_smem_bytes(n, f.d.nhi, f.d.nlo) > 227 * 1024) {
             free_fft(f);
@@ -1016,7 +1018,10 @@ sk_status xform_pass(sk_plan_t p, bool analyze, int nrows, int n, int n_in, long
     const DevFft* f = nullptr;
     sk_status s = xform_fft(p, n, &f);
     if (s != SK_OK) return s;
-    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0};
+    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0, 0};
+    xp.hiocc = xform_threads(n) <= 256 ? 1 : 0;
+    for (int st = 0; st < f->d.nst; ++st)
+        if (f->d.R[st] > 8) xp.hiocc = 0;  // the variant only instantiates radices <= 8
     CU(sk::launch_xform(xp, analyze, nrows, xform_threads(n), sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo), p->stream));
     return SK_OK;
 }

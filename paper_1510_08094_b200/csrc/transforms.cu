@@ -28,8 +28,9 @@ namespace sk {
 //   the modes both lengths hold, then the unnormalised backward transform.
 // SWZ: XOR-swizzled slots (plans whose first span is even, e.g. power-of-two
 // lengths, where the butterflies of a stage otherwise share one bank).
-template <bool ANALYZE, bool SWZ>
-__global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
+// HI: high-occupancy variant for short transforms (<= 256 threads, radices <= 8).
+template <bool ANALYZE, bool SWZ, bool HI>
+__global__ void __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) xform_kernel(XformParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int n = P.fd.L;  // transform length (n for ANALYZE, n_out for SYNTH)
     double2* a = reinterpret_cast<double2*>(smem_raw);
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
     if constexpr (ANALYZE) {
         for (int j = tid; j < n; j += nthr) a[swz<SWZ>(j)] = src[j];
         __syncthreads();
-        fft_forward<SWZ>(a, P.fd, T, tid, nthr);  // X_t at a[swz(rev[t])]
+        fft_forward<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);  // X_t at a[swz(rev[t])]
         const double inv = 1.0 / n;
         for (int kp = tid; kp < n; kp += nthr) {
             const int k = kp - n / 2;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(512) xform_kernel(XformParams P) {
             a[swz<SWZ>(s_rev[t])] = (k % 2 == 0) ? c : make_double2(-c.x, -c.y);  // DIT input: digit-reversed
         }
         __syncthreads();
-        fft_inverse<SWZ>(a, P.fd, T, tid, nthr);  // natural order
+        fft_inverse<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);  // natural order
         for (int j = tid; j < n; j += nthr) P.dst[static_cast<long long>(j) * P.ld_out + r] = a[swz<SWZ>(j)];
     }
 }
@@ -84,24 +85,30 @@ size_t xform_smem_bytes(int n, int nhi, int nlo) {
     return static_cast<size_t>((n + 7) & ~7) * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>(n) * 4;
 }
 
-cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
+template <bool ANALYZE, bool SWZ, bool HI>
+static cudaError_t launch_xform_t(const XformParams& P, int nrows, int nthr, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(xform_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(xform_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(xform_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(xform_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(xform_kernel<ANALYZE, SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    if (nrows <= 0) return cudaSuccess;
-    if (analyze) {
-        if (P.swizzle) xform_kernel<true, true><<<nrows, nthr, smem, st>>>(P);
-        else xform_kernel<true, false><<<nrows, nthr, smem, st>>>(P);
-    } else {
-        if (P.swizzle) xform_kernel<false, true><<<nrows, nthr, smem, st>>>(P);
-        else xform_kernel<false, false><<<nrows, nthr, smem, st>>>(P);
-    }
+    xform_kernel<ANALYZE, SWZ, HI><<<nrows, nthr, smem, st>>>(P);
     return cudaGetLastError();
+}
+
+cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
+    if (nrows <= 0) return cudaSuccess;
+    const bool hi = P.hiocc && nthr <= 256;
+    if (analyze) {
+        if (hi) return P.swizzle ? launch_xform_t<true, true, true>(P, nrows, nthr, smem, st)
+                                 : launch_xform_t<true, false, true>(P, nrows, nthr, smem, st);
+        return P.swizzle ? launch_xform_t<true, true, false>(P, nrows, nthr, smem, st)
+                         : launch_xform_t<true, false, false>(P, nrows, nthr, smem, st);
+    }
+    if (hi) return P.swizzle ? launch_xform_t<false, true, true>(P, nrows, nthr, smem, st)
+                             : launch_xform_t<false, false, true>(P, nrows, nthr, smem, st);
+    return P.swizzle ? launch_xform_t<false, true, false>(P, nrows, nthr, smem, st)
+                     : launch_xform_t<false, false, false>(P, nrows, nthr, smem, st);
 }
 
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st) {

@@ -31,6 +31,7 @@ namespace cg = cooperative_groups;
 namespace sk {
 
 constexpr int kStage = 16;  // values per thread staged in registers across cluster exchanges
+constexpr int kFoldStages = 3;  // TMA stages of fold inputs in flight (in the pivot window)
 
 #ifdef SK_PHASES
 extern __device__ unsigned long long g_phase[4096][24];
@@ -168,7 +169,7 @@ __device__ void solve_chain_part(double2* a, const double* ipw, V4* wsc, V4* tot
 }
 
 template <int Q>
-__global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL) {
+__global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL, const __grid_constant__ CUtensorMap cmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const ThetaParams& P = PL.t;
     const FftDesc& fq = PL.fq;
@@ -229,14 +230,17 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
     uint32_t pbytes = 0;
     const double* ipv = pivot_window(ipw, P.pivots, prow, tau_a, tau_b, pbytes);
     if (tid == 0) {
-        mbar_init(bar, 1);
+        for (int b = 0; b < 4; ++b) mbar_init(&bar[b], 1);  // [0] pivots, [1..3] fold staging
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0 && i_hi > i_lo) {
-        mbar_expect_tx(bar, pbytes);
-        bulk_g2s_chunked(ipw, P.pivots + ((prow + tau_a) & ~static_cast<size_t>(1)), pbytes, bar);
-    }
+    auto issue_pivots = [&]() {
+        if (tid == 0 && i_hi > i_lo) {
+            mbar_expect_tx(bar, pbytes);
+            bulk_g2s_chunked(ipw, P.pivots + ((prow + tau_a) & ~static_cast<size_t>(1)), pbytes, bar);
+        }
+    };
+    if (!PL.use_cmap) issue_pivots();  // else after the fold, which stages its inputs in the pivot window
     const Tw TM = load_tw(P.fd, tM_hi, tM_lo, tid, nthr);
     const Tw TQ = load_tw(fq, tq_hi, tq_lo, tid, nthr);
     __syncthreads();
@@ -244,29 +248,82 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
 
     // ---- 1. fold + decimation: inputs x_j, j = Q r + q (first radix-Q split)
     const double invM = 1.0 / P.g.M;
-    // batches of kFoldU inputs per thread: all global loads of a batch are
-    // in flight before any shared-memory store
-    constexpr int kFoldU = 8;
-    for (int r0 = tid; r0 < Lq; r0 += kFoldU * nthr) {
-        double2 aj[kFoldU], am[kFoldU];
-#pragma unroll
-        for (int u = 0; u < kFoldU; ++u) {
-            const int r = r0 + u * nthr;
-            if (r < Lq) {
-                const int j = Q * r + q;
-                aj[u] = *gcol(j);
-                am[u] = *gcol(L - j);
+    if (PL.use_cmap) {
+        // Inputs a_j (j = Q r + q) and a_(L-j) by TMA boxes of the column
+        // tensor map {re/im, j mod Q, j / Q, column} into the pivot window:
+        // kFoldStages chunks of kFoldChunk r in flight; a_(L-j) runs backwards
+        // through its box (r' = L/Q - 1 - r for q > 0, L/Q - r for q = 0; the
+        // one out-of-range element, a_L, comes from global memory).
+        const int CB = PL.fold_chunk;  // 512 or 256 (what the pivot window holds)
+        constexpr int NS = kFoldStages;
+        double2* stg = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(ipw) + 127) & ~static_cast<uintptr_t>(127));
+        const int mcol = blockIdx.x / (2 * Q);  // column of the map: rhs * ncols + kl
+        const int nch = (Lq + CB - 1) / CB;
+        const int qm = (Q - q) % Q;
+        auto issue = [&](int c) {
+            const int sI = c % NS, r0 = c * CB;
+            double2* aj = stg + sI * 2 * CB;
+            double2* am = aj + CB;
+            mbar_expect_tx(&bar[1 + sI], 2 * CB * 16);
+            const int st = q > 0 ? (Lq - r0 - CB) : (Lq - r0 - CB + 1);
+            for (int b = 0; b < CB; b += 256) {
+                tma_load_4d(aj + b, &cmap, 0, q, r0 + b, mcol, &bar[1 + sI]);
+                tma_load_4d(am + b, &cmap, 0, qm, st + b, mcol, &bar[1 + sI]);
+            }
+        };
+        if (tid == 0)
+            for (int c = 0; c < NS && c < nch; ++c) issue(c);
+        const double2 aL = *gcol(L);
+        for (int c = 0; c < nch; ++c) {
+            const int sI = c % NS;
+            const double2* aj = stg + sI * 2 * CB;
+            const double2* am = aj + CB;
+            mbar_wait(&bar[1 + sI], (c / NS) & 1);
+            for (int i = tid; i < CB; i += nthr) {
+                const int r = c * CB + i;
+                if (r < Lq) {
+                    const int j = Q * r + q;
+                    const double2 vj = aj[i];
+                    const double2 vm = (q == 0 && r == 0) ? aL : am[CB - 1 - i];
+                    double2 x;
+                    if (par == 0) x = make_double2((vj.x + sgn * vm.x) * invM, (vj.y + sgn * vm.y) * invM);
+                    else x = cscale(cmul(make_double2(vj.x - sgn * vm.x, vj.y - sgn * vm.y), TM(j)), invM);
+                    a[swz<true>(__ldg(revq + r))] = x;
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && c + NS < nch) {
+                fence_proxy_async();  // this stage's generic reads before the next bulk writes
+                issue(c + NS);
             }
         }
+        if (tid == 0) fence_proxy_async();
+        issue_pivots();
+    } else {
+        // batches of kFoldU inputs per thread: all global loads of a batch are
+        // in flight before any shared-memory store
+        constexpr int kFoldU = 8;
+        for (int r0 = tid; r0 < Lq; r0 += kFoldU * nthr) {
+            double2 aj[kFoldU], am[kFoldU];
 #pragma unroll
-        for (int u = 0; u < kFoldU; ++u) {
-            const int r = r0 + u * nthr;
-            if (r < Lq) {
-                const int j = Q * r + q;
-                double2 x;
-                if (par == 0) x = make_double2((aj[u].x + sgn * am[u].x) * invM, (aj[u].y + sgn * am[u].y) * invM);
-                else x = cscale(cmul(make_double2(aj[u].x - sgn * am[u].x, aj[u].y - sgn * am[u].y), TM(j)), invM);
-                a[swz<true>(__ldg(revq + r))] = x;
+            for (int u = 0; u < kFoldU; ++u) {
+                const int r = r0 + u * nthr;
+                if (r < Lq) {
+                    const int j = Q * r + q;
+                    aj[u] = *gcol(j);
+                    am[u] = *gcol(L - j);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kFoldU; ++u) {
+                const int r = r0 + u * nthr;
+                if (r < Lq) {
+                    const int j = Q * r + q;
+                    double2 x;
+                    if (par == 0) x = make_double2((aj[u].x + sgn * am[u].x) * invM, (aj[u].y + sgn * am[u].y) * invM);
+                    else x = cscale(cmul(make_double2(aj[u].x - sgn * am[u].x, aj[u].y - sgn * am[u].y), TM(j)), invM);
+                    a[swz<true>(__ldg(revq + r))] = x;
+                }
             }
         }
     }
@@ -625,7 +682,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
 }
 
 // --------------------------------------------------------- host launchers
-cudaError_t launch_theta_large(const ThetaLargeParams& P, int Q, int nthr, size_t smem, cudaStream_t st) {
+cudaError_t launch_theta_large(const ThetaLargeParams& P, const CUtensorMap& cmap, int Q, int nthr, size_t smem,
+                               cudaStream_t st) {
     const int nblk = 2 * Q * P.t.ncols * P.t.nrhs;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblk);
@@ -642,10 +700,10 @@ cudaError_t launch_theta_large(const ThetaLargeParams& P, int Q, int nthr, size_
     if (Q == 4) {
         cudaFuncSetAttribute(theta_large_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(theta_large_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        return cudaLaunchKernelEx(&cfg, theta_large_kernel<4>, P);
+        return cudaLaunchKernelEx(&cfg, theta_large_kernel<4>, P, cmap);
     }
     cudaFuncSetAttribute(theta_large_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    return cudaLaunchKernelEx(&cfg, theta_large_kernel<2>, P);
+    return cudaLaunchKernelEx(&cfg, theta_large_kernel<2>, P, cmap);
 }
 
 cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st) {

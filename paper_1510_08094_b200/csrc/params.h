@@ -101,6 +101,8 @@ struct ResidualParams {
 struct ThetaLargeParams {
     ThetaParams t;
     FftDesc fq;
+    int use_cmap;    // fold inputs through the column tensor map (single rank: contiguous columns)
+    int fold_chunk;  // r per TMA stage of the fold (256 or 512, sized to the pivot window)
 };
 struct LambdaSplitParams {
     LambdaParams l;
@@ -108,12 +110,13 @@ struct LambdaSplitParams {
 };
 inline size_t theta_large_smem_bytes(int Lq, int nhiM, int nloM, int nhiq, int nloq) {
     return static_cast<size_t>((Lq + 7) & ~7) * 16 + static_cast<size_t>(nhiM + nloM + nhiq + nloq) * 16 +
-           static_cast<size_t>((Lq + 4 + 1) & ~1) * 8 + 32 * 32 + 2 * 32 + 16 * 16 + 64 * 8 + 16;
+           static_cast<size_t>((Lq + 4 + 1) & ~1) * 8 + 32 * 32 + 2 * 32 + 16 * 16 + 64 * 8 + 4 * 8;
 }
 inline size_t lambda_split_smem_bytes(int Lh, int nhiN, int nloN, int nhih, int nloh) {
     return static_cast<size_t>((Lh + 7) & ~7) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16;
 }
-cudaError_t launch_theta_large(const ThetaLargeParams& P, int Q, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_theta_large(const ThetaLargeParams& P, const CUtensorMap& cmap, int Q, int nthr, size_t smem,
+                               cudaStream_t st);
 cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
 

@@ -187,6 +187,31 @@ sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nr
     return SK_OK;
 }
 
+// Tensor map over the theta-stage columns (complex, contiguous, leading
+// dimension `rows`) as {re/im, j mod Q, j / Q, column} for j < Q*Lq: one box
+// is 256 consecutive j / Q of one residue class j mod Q.
+sk_status make_col_map(CUtensorMap* map, void* base, int rows, int Q, int Lq, int ncols) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled is not available");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[4] = {2, static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(Lq),
+                                static_cast<cuuint64_t>(ncols)};
+    const cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(Q) * 16, static_cast<cuuint64_t>(rows) * 16};
+    const cuuint32_t box[4] = {2, 1, 256, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled (columns) failed (" + std::to_string(r) + ")");
+    return SK_OK;
+}
+
 int round_threads(long long want, int lo, int hi) {
     long long t = ((want + 31) / 32) * 32;
     if (t < lo) t = lo;
@@ -787,8 +812,22 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         if (peers) tp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
         if (p->theta_q) {
-            sk::ThetaLargeParams tl{tp, p->ftq.d};
-            CU(sk::launch_theta_large(tl, p->theta_q, p->thr_theta, p->smem_theta, p->stream));
+            sk::ThetaLargeParams tl{tp, p->ftq.d, 0, 0};
+            CUtensorMap cmap{};
+            {
+                // fold inputs by TMA when the columns are contiguous (one rank)
+                // and the pivot window holds 3 stages of 2 x chunk values
+                const int Q = p->theta_q, Lq = p->g.Lt / Q;
+                const long long cap = static_cast<long long>((Lq + 4 + 1) & ~1) * 8 - 128;
+                const int cb = cap >= 3LL * 2 * 512 * 16 ? 512 : (cap >= 3LL * 2 * 256 * 16 ? 256 : 0);
+                if (sl.P == 1 && !peers && cb && !std::getenv("SK_NO_FOLD_TMA")) {
+                    sk_status ms = make_col_map(&cmap, tp.buf, p->g.rows, Q, Lq, ncols_local * tp.nrhs);
+                    if (ms != SK_OK) return ms;
+                    tl.use_cmap = 1;
+                    tl.fold_chunk = cb;
+                }
+            }
+            CU(sk::launch_theta_large(tl, cmap, p->theta_q, p->thr_theta, p->smem_theta, p->stream));
         } else {
             CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
         }

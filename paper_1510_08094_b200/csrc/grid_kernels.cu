@@ -114,6 +114,80 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
     }
 }
 
+// Row pairs (p, p+1) on a 2-CTA cluster (single RHS, unswizzled rows, no
+// peer stores; C3): each CTA transforms its row as above and leaves the N/2+1
+// modes in natural order in its shared memory; CTA c then stores the modes of
+// its half of k for both rows, adjacent lanes writing the (p, p+1) neighbours
+// of one mode, so a warp's store covers 16 modes x 32 contiguous bytes where
+// the per-row stores covered 32 modes x 16 bytes.  The peer row is read
+// through DSMEM in natural order (contiguous).  Grid = rows rounded up to even;
+// the padding CTA only takes part in the cluster barriers.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_pair_kernel(LambdaParams P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int L = P.fd.L;
+    const int Lpad = (L / kBoxModes + 1) * kBoxModes;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + Lpad;
+    double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int c = static_cast<int>(cluster.block_rank());
+    const int row = blockIdx.x;
+    const bool live = row < P.rows_local;  // CTA-uniform
+    if (live && tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
+        bulk_g2s_chunked(a, reinterpret_cast<const double2*>(P.f + static_cast<long long>(row) * P.g.N),
+                         static_cast<uint32_t>(L) * 16, bar);
+    }
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
+    __syncthreads();
+    if (live) {
+        mbar_wait(bar, 0);
+        fft_forward<false, 25>(a, P.fd, T, tid, nthr);
+        const double invN = 1.0 / P.g.N;
+        double2 vk[kLamPairs], vm[kLamPairs];
+#pragma unroll
+        for (int u = 0; u < kLamPairs; ++u) {
+            const int k = tid + u * nthr;
+            if (k <= L / 2) {
+                const int km = L - k;
+                const double2 z = a[s_rev[k]];
+                const double2 zp = a[s_rev[km == L ? 0 : km]];
+                const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
+                const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
+                vk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
+                vm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kLamPairs; ++u) {
+            const int k = tid + u * nthr;
+            if (k <= L / 2) {
+                a[k] = vk[u];
+                if (L - k != k) a[L - k] = vm[u];
+            }
+        }
+    }
+    cluster.sync();
+    const double2* other = cluster.map_shared_rank(a, c ^ 1);
+    const int r0 = row & ~1;
+    const int nk = L + 1;
+    const int k_lo = c == 0 ? 0 : nk / 2;
+    const int k_hi = c == 0 ? nk / 2 : nk;
+    const int sub_hi = min(2, P.rows_local - r0);  // 1 when the padding CTA is the partner
+    for (int i = tid; i < 2 * (k_hi - k_lo); i += nthr) {
+        const int k = k_lo + (i >> 1), sub = i & 1;
+        if (sub < sub_hi) P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = (sub == c) ? a[k] : other[k];
+    }
+    cluster.sync();
+}
+
 // Inverse: TMA tensor loads gather the row's N/2+1 modes from the mode-major
 // spectrum; sample_grid's (-1)^k (fourier.cpp:61-62) and the packing into
 // N/2 complex go through registers into digit-reversed order; inverse DIT
@@ -1113,7 +1187,20 @@ static cudaError_t launch_lambda_fwd_t(const LambdaParams& P, const CUtensorMap&
     lambda_fwd_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
+bool lambda_pair_ok(const LambdaParams& P, int nthr) {
+    return !P.swizzle && !P.hiocc && P.nrhs == 1 && P.peers.n == 0 && nthr <= 256 &&
+           P.fd.L / 2 + 1 <= kLamPairs * nthr;
+}
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    if (P.pair && lambda_pair_ok(P, nthr)) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(lambda_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        lambda_fwd_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P);
+        return cudaGetLastError();
+    }
     if (P.hiocc)
         return P.swizzle ? launch_lambda_fwd_t<true, true>(P, map, nthr, smem, st)
                          : launch_lambda_fwd_t<false, true>(P, map, nthr, smem, st);

@@ -24,6 +24,7 @@ struct LambdaParams {
     PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
     int swizzle;        // XOR-swizzled shared-memory slots (plans whose first FFT span is even)
     int hiocc;          // high-occupancy kernel variant (short rows: 64 registers, radices <= 8)
+    int pair;           // fwd: row pairs on CTA pairs, 32-byte (p, p+1) stores (lambda_pair_ok decides)
 };
 
 struct ThetaParams {

@@ -325,6 +325,7 @@ struct sk_plan_s {
     int piv_stride = 0;        // doubles per pivot-table row
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
     bool lambda_hiocc = false; // high-occupancy lambda kernel variant (short rows)
+    bool lambda_pair = true;   // forward lambda rows on CTA pairs (32-byte stores); SK_LAMBDA_PAIR=0 for A/B
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
@@ -536,6 +537,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // short rows (<= 128 threads per CTA) run the high-occupancy lambda variant
     // (64 registers, radices <= 8, <= 6 mode pairs per thread; SK_NO_HIOCC)
     p->lambda_hiocc = p->thr_lambda <= 128 && (Ll / 2 + 1) <= 6 * p->thr_lambda && !std::getenv("SK_NO_HIOCC");
+    if (const char* e = std::getenv("SK_LAMBDA_PAIR")) p->lambda_pair = std::atoi(e) != 0;  // A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
@@ -691,6 +693,10 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     const bool swz_l = p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0;
     info[13] = (p->theta_hiocc && !p->theta_q && p->chain_mode == 1 && p->thr_theta <= 256 ? 1 : 0) |
                (p->lambda_hiocc && !p->lambda_split ? 2 : 0) | (swz_t ? 4 : 0) | (swz_l ? 8 : 0);
+    const bool hi_l = p->lambda_hiocc && !p->lambda_split;
+    if (p->grid_ok && p->lambda_pair && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 && p->thr_lambda <= 256 &&
+        p->N / 4 + 1 <= 12 * p->thr_lambda)
+        info[13] |= 16;  // forward lambda rows on CTA pairs (lambda_pair_ok, single GPU)
     return SK_OK;
 }
 
@@ -769,6 +775,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
     lp.fd = p->fl.d;
     lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
     lp.hiocc = p->lambda_hiocc && !p->lambda_split ? 1 : 0;
+    lp.pair = p->lambda_pair ? 1 : 0;
     lp.rows_local = rows_local;
     lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
     if (stages & 1) {

@@ -223,6 +223,31 @@ def test_grid_full_size_analytic_C2(pkg):
     assert err <= 1e-10, err
 
 
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_grid_full_size_analytic(pkg, name):
+    """The same property at the bench workloads: C3 (20000 x 10000, L = 2000,
+    the paper-scale single RHS) and C4 (64 RHS of 2048 x 1024, L = 256, one
+    batched plan): every right-hand side against its analytic solution."""
+    import torch
+    from paper_1510_08094_b200 import inputs
+    cfg = inputs.CONFIGS[name]
+    rows = cfg.M // 2 + 1
+    with pkg.Plan(cfg.M, cfg.N, cfg.nrhs) as plan:
+        f = torch.empty((cfg.nrhs, rows, cfg.N), dtype=torch.float64, device="cuda")
+        for r in range(cfg.nrhs):
+            plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(11 + r, cfg.L, cfg.p)).cuda(), f[r])
+        u = plan.solve_grid(f if cfg.nrhs > 1 else f[0])
+        if cfg.nrhs == 1:
+            u = u.unsqueeze(0)
+        del f
+        ue = torch.empty((rows, cfg.N), dtype=torch.float64, device="cuda")
+        worst = 0.0
+        for r in range(cfg.nrhs):
+            plan.shgen(cfg.L, torch.from_numpy(inputs.sh_coeffs(11 + r, cfg.L, cfg.p, solution=True)).cuda(), ue)
+            worst = max(worst, ((u[r] - ue).abs().max() / ue.abs().max()).item())
+    assert worst <= 1e-10, worst
+
+
 # ------------------------------------------------- cluster-split kernels
 @pytest.mark.parametrize("m,n,L", [(32768, 48, 20), (64, 32768, 20), (32768, 32768 // 64, 24)])
 def test_grid_split_kernels_vs_oracle(pkg, oracle, m, n, L):
@@ -331,3 +356,26 @@ def test_pipelined_host_solves(pkg, oracle):
             plan.solve_grid(fs[1], np.empty_like(bad), sync=False)
             plan.solve_grid(fs[2], np.empty_like(bad), sync=False)
             plan.sync()
+
+
+@pytest.mark.parametrize("m,n", [(64, 3000), (128, 3000), (40, 2400)])
+def test_lambda_row_pairs_bitwise(pkg, oracle, m, n, monkeypatch):
+    """Long non-power-of-two lambda rows run the forward lambda transform on
+    CTA pairs (row pairs, 32-byte stores; the odd row count M/2+1 leaves a padding
+    CTA): bit-identical to the one-row-per-CTA kernel, and against the
+    oracle on rough zero-mean data."""
+    rng = np.random.default_rng(m * n)
+    f = rng.standard_normal((m // 2 + 1, n))
+    A = oracle.analyze_2d(oracle.dfs_double(f, m))
+    mu = (oracle.integration_weights(m) * A[:, n // 2]).sum() / 2.0
+    f = f - mu.real
+    with pkg.Plan(m, n) as plan:
+        assert plan.info()["variants"] & 16, plan.info()
+        u = plan.solve_grid(f)
+    monkeypatch.setenv("SK_LAMBDA_PAIR", "0")
+    with pkg.Plan(m, n) as plan:
+        assert not plan.info()["variants"] & 16
+        u1 = plan.solve_grid(f)
+    assert np.array_equal(u, u1)
+    u_ref = oracle.grid_pipeline_real(f, m, threads=8)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()

@@ -205,7 +205,8 @@ sk_status sk_ipc_close(void* ptr);
  * solver (0 shared-memory walk, 1 fixed segments, 2 12-element register
  * walk), [13] = kernel variants (bit 0 high-occupancy theta kernel, bit 1
  * high-occupancy lambda kernels, bit 2 swizzled theta slots, bit 3 swizzled
- * lambda slots, bit 4 forward lambda rows on CTA pairs). */
+ * lambda slots, bit 4 forward lambda rows on CTA pairs, bit 5 inverse lambda
+ * rows on CTA pairs). */
 sk_status sk_plan_info(sk_plan_t plan, long long info[16]);
 
 /* Time one launch of each stage (device events, ms): t[0] lambda_fwd,

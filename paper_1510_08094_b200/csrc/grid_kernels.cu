@@ -263,6 +263,100 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParam
     for (int j = tid; j < L; j += nthr) dst[j] = a[swz<SWZ>(j)];
 }
 
+// Inverse on row pairs (p, p+1), the mirror image of lambda_fwd_pair_kernel
+// (single RHS, unswizzled rows; C3): a 2-row x 256-mode box of the spectrum
+// map gathers 32-byte (p, p+1) segments, CTA c loading the boxes of its half
+// of the modes for both rows into its own row buffer ([mode][row] order; the
+// box count nb is even, so half the boxes fill exactly the buffer). After a
+// cluster barrier each CTA reads its row's modes from both buffers (the peer
+// through DSMEM) into registers; a second barrier frees the buffers for the
+// digit-reversed C2R pack, then the inverse FFT runs as in lambda_inv_kernel.
+// The padding CTA of an odd row count loads its boxes (row p+1 is zero-filled
+// out of bounds) but transforms and stores nothing.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+    lambda_inv_pair_kernel(LambdaParams P, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int L = P.fd.L;
+    const int nb = L / kBoxModes + 1;  // even (lambda_inv_pair_ok)
+    const int Lpad = nb * kBoxModes;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + Lpad;
+    double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int c = static_cast<int>(cluster.block_rank());
+    const int row = blockIdx.x;
+    const bool live = row < P.rows_local;  // CTA-uniform
+    const int r0 = row & ~1;
+    const int kspl = (nb / 2) * kBoxModes;  // modes [0, kspl) in CTA 0, the rest in CTA 1
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t rb = static_cast<uint32_t>((L + 3) & ~3) * 4;
+        mbar_expect_tx(bar, static_cast<uint32_t>(nb / 2) * kBoxModes * 32 + (P.fd.nhi + P.fd.nlo) * 16 + rb);
+        for (int b = 0; b < nb / 2; ++b)
+            tma_load_3d(a + b * 2 * kBoxModes, &tmap, 2 * r0, c * kspl + b * kBoxModes, 0, bar);
+        bulk_g2s_chunked(s_hi, P.fd.hi, P.fd.nhi * 16, bar);
+        bulk_g2s_chunked(s_lo, P.fd.lo, P.fd.nlo * 16, bar);
+        bulk_g2s_chunked(s_rev, P.fd.rev, rb, bar);
+    }
+    const Tw T{s_hi, s_lo, P.fd.shift, (1 << P.fd.shift) - 1};
+    __syncthreads();
+    mbar_wait(bar, 0);
+    cluster.sync();
+    const double2* other = cluster.map_shared_rank(a, c ^ 1);
+    const int sub = row & 1;
+    auto mode = [&](int k) -> double2 {
+        const int o = k >= kspl ? 1 : 0;
+        return (o == c ? a : other)[(k - o * kspl) * 2 + sub];
+    };
+    double2 zk[kLamPairs], zm[kLamPairs];
+    if (live) {
+#pragma unroll
+        for (int u = 0; u < kLamPairs; ++u) {
+            const int k = tid + u * nthr;
+            if (k <= L / 2) {
+                const int km = L - k;
+                double2 v = mode(k);
+                double2 w = mode(km);
+                if (k & 1) v = make_double2(-v.x, -v.y);
+                if (km & 1) w = make_double2(-w.x, -w.y);
+                if (k == 0) {
+                    v.y = 0.0;
+                    w.y = 0.0;
+                }
+                {
+                    const double2 E = make_double2(v.x + w.x, v.y - w.y);
+                    const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
+                    zk[u] = make_double2(E.x - O.y, E.y + O.x);
+                }
+                {
+                    const double2 E = make_double2(w.x + v.x, w.y - v.y);
+                    const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
+                    zm[u] = make_double2(E.x - O.y, E.y + O.x);
+                }
+            }
+        }
+    }
+    cluster.sync();  // the peer has finished reading this CTA's buffer
+    if (!live) return;
+#pragma unroll
+    for (int u = 0; u < kLamPairs; ++u) {
+        const int k = tid + u * nthr;
+        if (k <= L / 2) {
+            const int km = L - k;
+            a[s_rev[k]] = zk[u];
+            if (k != 0 && km != k) a[s_rev[km]] = zm[u];
+        }
+    }
+    __syncthreads();
+    fft_inverse<false, 25>(a, P.fd, T, tid, nthr);
+    double2* dst = reinterpret_cast<double2*>(P.u + static_cast<long long>(row) * P.g.N);
+    for (int j = tid; j < L; j += nthr) dst[j] = a[j];
+}
+
 // -------------------------------------------------------------- theta stage
 // Pivot table: for every lambda mode k >= 0 and parity class, the reciprocal
 // Thomas pivots 1/d'_i of both chains, indexed by the natural FFT index tau
@@ -1192,7 +1286,7 @@ bool lambda_pair_ok(const LambdaParams& P, int nthr) {
            P.fd.L / 2 + 1 <= kLamPairs * nthr;
 }
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
-    if (P.pair && lambda_pair_ok(P, nthr)) {
+    if ((P.pair & 1) && lambda_pair_ok(P, nthr)) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(lambda_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1219,7 +1313,19 @@ static cudaError_t launch_lambda_inv_t(const LambdaParams& P, const CUtensorMap&
     lambda_inv_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
+bool lambda_inv_pair_ok(const LambdaParams& P, int nthr) {
+    return lambda_pair_ok(P, nthr) && (P.fd.L / kBoxModes + 1) % 2 == 0;
+}
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    if ((P.pair & 2) && lambda_inv_pair_ok(P, nthr)) {  // map has 2-row boxes (make_spec_map box_rows = 2)
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(lambda_inv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        lambda_inv_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P, map);
+        return cudaGetLastError();
+    }
     if (P.hiocc)
         return P.swizzle ? launch_lambda_inv_t<true, true>(P, map, nthr, smem, st)
                          : launch_lambda_inv_t<false, true>(P, map, nthr, smem, st);

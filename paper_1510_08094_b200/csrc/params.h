@@ -24,7 +24,7 @@ struct LambdaParams {
     PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
     int swizzle;        // XOR-swizzled shared-memory slots (plans whose first FFT span is even)
     int hiocc;          // high-occupancy kernel variant (short rows: 64 registers, radices <= 8)
-    int pair;           // fwd: row pairs on CTA pairs, 32-byte (p, p+1) stores (lambda_pair_ok decides)
+    int pair;           // bit 0 fwd, bit 1 inv: row pairs on CTA pairs, 32-byte (p, p+1) segments (lambda_pair_ok decides)
 };
 
 struct ThetaParams {
@@ -139,6 +139,7 @@ __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo, bool
 }
 
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
+bool lambda_inv_pair_ok(const LambdaParams& P, int nthr);  // inverse on CTA pairs (needs 2-row boxes)
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
 // Lambda-stage shared memory (bytes) for transform length L and twiddle table sizes.
 inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {

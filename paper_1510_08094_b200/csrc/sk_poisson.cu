@@ -164,8 +164,8 @@ void free_fft(DevFft& f) {
 
 // Tensor map over a mode-major spectrum [rhs][k][p] (complex, rows p
 // contiguous) as a 3-D float64 tensor {2*rows, cols, nrhs}; one box is one
-// row's slice of 256 consecutive modes.
-sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs) {
+// row's slice of 256 consecutive modes (box_rows = 2: rows p, p+1 together).
+sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs, int box_rows = 1) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -178,7 +178,7 @@ sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nr
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * rows), static_cast<cuuint64_t>(cols),
                                 static_cast<cuuint64_t>(nrhs)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rows) * 16, static_cast<cuuint64_t>(rows) * cols * 16};
-    const cuuint32_t box[3] = {2, 256, 1};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * box_rows), 256, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -326,6 +326,9 @@ struct sk_plan_s {
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
     bool lambda_hiocc = false; // high-occupancy lambda kernel variant (short rows)
     bool lambda_pair = true;   // forward lambda rows on CTA pairs (32-byte stores); SK_LAMBDA_PAIR=0 for A/B
+    // inverse lambda rows on CTA pairs (32-byte gathers): opt-in, SK_LAMBDA_PAIR_INV=1. Measured slower at C3
+    // (0.80 vs 0.57 ms: the peer's modes are 16-byte DSMEM reads at a 32-byte stride)
+    bool lambda_pair_inv = false;
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
@@ -538,6 +541,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // (64 registers, radices <= 8, <= 6 mode pairs per thread; SK_NO_HIOCC)
     p->lambda_hiocc = p->thr_lambda <= 128 && (Ll / 2 + 1) <= 6 * p->thr_lambda && !std::getenv("SK_NO_HIOCC");
     if (const char* e = std::getenv("SK_LAMBDA_PAIR")) p->lambda_pair = std::atoi(e) != 0;  // A/B
+    if (const char* e = std::getenv("SK_LAMBDA_PAIR_INV")) p->lambda_pair_inv = std::atoi(e) != 0;  // opt-in A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
@@ -697,6 +701,9 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     if (p->grid_ok && p->lambda_pair && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 && p->thr_lambda <= 256 &&
         p->N / 4 + 1 <= 12 * p->thr_lambda)
         info[13] |= 16;  // forward lambda rows on CTA pairs (lambda_pair_ok, single GPU)
+    if (p->grid_ok && p->lambda_pair_inv && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
+        p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda && (p->N / 2 / 256 + 1) % 2 == 0)
+        info[13] |= 32;  // inverse lambda rows on CTA pairs (lambda_inv_pair_ok)
     return SK_OK;
 }
 
@@ -854,7 +861,9 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
             CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
         } else {
             CUtensorMap map;
-            sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
+            if (p->lambda_pair_inv) lp.pair |= 2;
+            const int box_rows = (lp.pair & 2) && sk::lambda_inv_pair_ok(lp, p->thr_lambda) ? 2 : 1;
+            sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs, box_rows);
             if (ms != SK_OK) return ms;
             CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
         }

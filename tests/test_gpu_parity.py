@@ -379,3 +379,27 @@ def test_lambda_row_pairs_bitwise(pkg, oracle, m, n, monkeypatch):
     assert np.array_equal(u, u1)
     u_ref = oracle.grid_pipeline_real(f, m, threads=8)
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+@pytest.mark.parametrize("m,n,paired", [(64, 3000, True), (54, 3000, True), (40, 2400, False)])
+def test_lambda_inv_row_pairs_bitwise(pkg, oracle, m, n, paired, monkeypatch):
+    """The opt-in inverse lambda transform on CTA pairs (SK_LAMBDA_PAIR_INV=1:
+    2-row TMA boxes, the peer's modes through DSMEM; used when the row's box
+    count is even: L = 1500 -> 6 boxes, L = 1200 -> 5 boxes falls back):
+    bit-identical to the one-row-per-CTA kernel for odd (33) and even (28)
+    row counts, and against the oracle."""
+    rng = np.random.default_rng(m * n + 1)
+    f = rng.standard_normal((m // 2 + 1, n))
+    A = oracle.analyze_2d(oracle.dfs_double(f, m))
+    mu = (oracle.integration_weights(m) * A[:, n // 2]).sum() / 2.0
+    f = f - mu.real
+    with pkg.Plan(m, n) as plan:
+        assert not plan.info()["variants"] & 32
+        u1 = plan.solve_grid(f)
+    monkeypatch.setenv("SK_LAMBDA_PAIR_INV", "1")
+    with pkg.Plan(m, n) as plan:
+        assert bool(plan.info()["variants"] & 32) == paired, plan.info()
+        u = plan.solve_grid(f)
+    assert np.array_equal(u, u1)
+    u_ref = oracle.grid_pipeline_real(f, m, threads=8)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()

@@ -16,6 +16,7 @@
 // (real data: the k < 0 half is its Hermitian mirror), p = 0..M/2 (physical
 // rows only: the doubled rows j < M/2 are (-1)^k times row M/2-j in lambda-
 // spectral space, so the doubled grid is never stored).
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -114,6 +115,21 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
     }
 }
 
+// Last cluster barrier of a kernel whose CTAs read peer shared memory just
+// before it: it only has to keep each CTA's shared memory alive until the
+// peer has finished reading. Every such read feeds a global store issued
+// before the reader arrives, so a relaxed arrive suffices; cluster.sync()'s
+// release would also wait for all of the CTA's global stores to complete
+// (ncu: 10 % membar stalls in lambda_fwd_pair_kernel). relaxed = 0 for A/B.
+__device__ __forceinline__ void cluster_exit_barrier(int relaxed) {
+    if (relaxed) {
+        asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+        asm volatile("barrier.cluster.wait;" ::: "memory");
+    } else {
+        cg::this_cluster().sync();
+    }
+}
+
 // Row pairs (p, p+1) on a 2-CTA cluster (single RHS, unswizzled rows, no
 // peer stores; C3): each CTA transforms its row as above and leaves the N/2+1
 // modes in natural order in its shared memory; CTA c then stores the modes of
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
 // the per-row stores covered 32 modes x 16 bytes.  The peer row is read
 // through DSMEM in natural order (contiguous).  Grid = rows rounded up to even;
 // the padding CTA only takes part in the cluster barriers.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_pair_kernel(LambdaParams P) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_pair_kernel(LambdaParams P, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int L = P.fd.L;
@@ -185,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
         const int k = k_lo + (i >> 1), sub = i & 1;
         if (sub < sub_hi) P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = (sub == c) ? a[k] : other[k];
     }
-    cluster.sync();
+    cluster_exit_barrier(relaxed_exit);
 }
 
 // Inverse: TMA tensor loads gather the row's N/2+1 modes from the mode-major
@@ -943,7 +959,7 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
 // <= 8): 64 registers per thread, so twice the CTAs per SM hide the latency of
 // a transform that gives each thread only one or two butterflies per stage.
 template <bool SWZ, int CH, bool HI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) theta_kernel(ThetaParams P) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) theta_kernel(ThetaParams P, int relaxed_exit) {
     constexpr int kFold = HI ? kFoldMaxHi : kFoldMax;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -1199,7 +1215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
         else colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }
     SK_PROBE(9);
-    cluster.sync();
+    cluster_exit_barrier(relaxed_exit);
     SK_PROBE(10);
 }
 
@@ -1270,6 +1286,11 @@ __global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
 }
 
 // --------------------------------------------------------- host launchers
+// SK_PAIR_SYNC_EXIT=1: full cluster.sync() as the exit barrier (A/B)
+static int exit_relaxed() {
+    static const int r = std::getenv("SK_PAIR_SYNC_EXIT") ? 0 : 1;
+    return r;
+}
 template <bool SWZ, bool HI>
 static cudaError_t launch_lambda_fwd_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
                                        cudaStream_t st) {
@@ -1292,7 +1313,7 @@ cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int
             cudaFuncSetAttribute(lambda_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attr = true;
         }
-        lambda_fwd_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P);
+        lambda_fwd_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P, exit_relaxed());
         return cudaGetLastError();
     }
     if (P.hiocc)
@@ -1341,7 +1362,7 @@ static cudaError_t launch_theta_t(const ThetaParams& P, int nthr, size_t smem, c
         cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr = true;
     }
-    theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P);
+    theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P, exit_relaxed());
     return cudaGetLastError();
 }
 

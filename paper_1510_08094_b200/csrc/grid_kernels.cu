@@ -115,21 +115,6 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
     }
 }
 
-// Last cluster barrier of a kernel whose CTAs read peer shared memory just
-// before it: it only has to keep each CTA's shared memory alive until the
-// peer has finished reading. Every such read feeds a global store issued
-// before the reader arrives, so a relaxed arrive suffices; cluster.sync()'s
-// release would also wait for all of the CTA's global stores to complete
-// (ncu: 10 % membar stalls in lambda_fwd_pair_kernel). relaxed = 0 for A/B.
-__device__ __forceinline__ void cluster_exit_barrier(int relaxed) {
-    if (relaxed) {
-        asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
-        asm volatile("barrier.cluster.wait;" ::: "memory");
-    } else {
-        cg::this_cluster().sync();
-    }
-}
-
 // Row pairs (p, p+1) on a 2-CTA cluster (single RHS, unswizzled rows, no
 // peer stores; C3): each CTA transforms its row as above and leaves the N/2+1
 // modes in natural order in its shared memory; CTA c then stores the modes of
@@ -1287,7 +1272,7 @@ __global__ void __launch_bounds__(256) shgen_kernel(ShgenParams P) {
 
 // --------------------------------------------------------- host launchers
 // SK_PAIR_SYNC_EXIT=1: full cluster.sync() as the exit barrier (A/B)
-static int exit_relaxed() {
+int exit_relaxed() {
     static const int r = std::getenv("SK_PAIR_SYNC_EXIT") ? 0 : 1;
     return r;
 }

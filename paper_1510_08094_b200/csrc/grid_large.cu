@@ -169,7 +169,7 @@ __device__ void solve_chain_part(double2* a, const double* ipw, V4* wsc, V4* tot
 }
 
 template <int Q>
-__global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL, const __grid_constant__ CUtensorMap cmap) {
+__global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL, const __grid_constant__ CUtensorMap cmap, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const ThetaParams& P = PL.t;
     const FftDesc& fq = PL.fq;
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
         }
     }
     SK_PROBE_L(12);
-    cluster.sync();
+    cluster_exit_barrier(relaxed_exit);
     SK_PROBE_L(13);
 }
 
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
 // r < L/2, from the row (L complex pairs), transforms it (length L/2) to
 // Z_(2 m + c), and emits the real-split modes X_k, k = c (mod 2), plus the
 // Nyquist mode (c = 0).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_split_kernel(LambdaSplitParams PS) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_split_kernel(LambdaSplitParams PS, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const LambdaParams& P = PS.l;
     const FftDesc& fh = PS.fh;  // length L/2
@@ -614,13 +614,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
         }
     }
     SK_PROBE_L(18);
-    cluster.sync();
+    cluster_exit_barrier(relaxed_exit);
 }
 
 // Inverse: CTA c gathers the modes k = c (mod 2) (and their partners L - k),
 // forms Z_k, runs the length-L/2 inverse transform of its class and the pair
 // recombines z_j = W0_j + w_L^j W1_j through DSMEM (CTA c writes half the row).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_split_kernel(LambdaSplitParams PS) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_split_kernel(LambdaSplitParams PS, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const LambdaParams& P = PS.l;
     const FftDesc& fh = PS.fh;
@@ -678,7 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
         dst[j] = cadd(w0[swz<true>(jj)], cmulc(w1[swz<true>(jj)], TN(2 * j)));
     }
     SK_PROBE_L(23);
-    cluster.sync();
+    cluster_exit_barrier(relaxed_exit);
 }
 
 // --------------------------------------------------------- host launchers
@@ -700,21 +700,21 @@ cudaError_t launch_theta_large(const ThetaLargeParams& P, const CUtensorMap& cma
     if (Q == 4) {
         cudaFuncSetAttribute(theta_large_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(theta_large_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        return cudaLaunchKernelEx(&cfg, theta_large_kernel<4>, P, cmap);
+        return cudaLaunchKernelEx(&cfg, theta_large_kernel<4>, P, cmap, exit_relaxed());
     }
     cudaFuncSetAttribute(theta_large_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    return cudaLaunchKernelEx(&cfg, theta_large_kernel<2>, P, cmap);
+    return cudaLaunchKernelEx(&cfg, theta_large_kernel<2>, P, cmap, exit_relaxed());
 }
 
 cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(lambda_fwd_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    lambda_fwd_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P);
+    lambda_fwd_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P, exit_relaxed());
     return cudaGetLastError();
 }
 
 cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(lambda_inv_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    lambda_inv_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P);
+    lambda_inv_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P, exit_relaxed());
     return cudaGetLastError();
 }
 

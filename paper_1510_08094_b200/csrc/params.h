@@ -139,6 +139,7 @@ __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo, bool
 }
 
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
+int exit_relaxed();  // 1 unless SK_PAIR_SYNC_EXIT is set: relaxed cluster exit barriers
 bool lambda_inv_pair_ok(const LambdaParams& P, int nthr);  // inverse on CTA pairs (needs 2-row boxes)
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
 // Lambda-stage shared memory (bytes) for transform length L and twiddle table sizes.

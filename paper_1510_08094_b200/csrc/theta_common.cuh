@@ -3,11 +3,29 @@
 // (lap - k^2) and the pivot windows.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "sk_internal.h"
 
 namespace sk {
+
+// Last cluster barrier of a kernel whose CTAs read peer shared memory just
+// before it: it only has to keep each CTA's shared memory alive until the
+// peer has finished reading. Every such read feeds a global store issued
+// before the reader arrives, so a relaxed arrive suffices; cluster.sync()'s
+// release would also wait for all of the CTA's global stores to complete
+// (ncu: 10 % membar stalls in lambda_fwd_pair_kernel). relaxed = 0 for A/B
+// (host side: exit_relaxed(), SK_PAIR_SYNC_EXIT=1).
+__device__ __forceinline__ void cluster_exit_barrier(int relaxed) {
+    if (relaxed) {
+        asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+        asm volatile("barrier.cluster.wait;" ::: "memory");
+    } else {
+        cooperative_groups::this_cluster().sync();
+    }
+}
+
 
 // ------------------------------------------------------------------ layout
 // Element (kl, p) of a lambda-mode column on the theta rank: pieces from each

@@ -116,6 +116,20 @@ sk_status sk_residual(sk_plan_t plan, const double* F, const double* X, double o
  * (the k < 0 half is its complex conjugate, reflected: real data). */
 sk_status sk_solve_grid(sk_plan_t plan, const double* f, double* u, double* X_half, unsigned flags);
 
+/* Reference-semantics grid solve: exactly the composition the reference runs
+ * — sample_dfs (sphere_domain.cpp:46-52) -> analyze_2d (fourier.cpp:170-188)
+ * -> Msin^2 per column (poisson.cpp:61) -> solve (poisson.cpp:121-161) ->
+ * sample_grid (fourier.cpp:190-209) — on the device.  All N lambda modes are
+ * solved (k < 0 too), so U is the reference's complex M x N doubled grid
+ * (BMCGrid layout, row j <-> theta_j = -pi + 2 pi j/M) for ANY input, also
+ * where under-resolved data make it differ from the real, Hermitian grid
+ * solve above (the reference's truncated theta operators are not mirror-
+ * symmetric at j = -M/2).  f: nrhs x (M/2+1) x N real; U: nrhs x M x N
+ * complex; X (may be NULL): nrhs x M x N complex solution coefficients.
+ * M and N must factor into 2,3,5,7 and fit one CTA (<= ~12000).  Same
+ * precondition / error behaviour as sk_solve_coeffs. */
+sk_status sk_solve_grid_exact(sk_plan_t plan, const double* f, double* U, double* X, unsigned flags);
+
 /* Surface mean 2 pi w^T f~_0 of the last grid solve's right-hand side and
  * max|F| of its coefficients (for callers that want the precondition data). */
 sk_status sk_last_mean(sk_plan_t plan, double out[3]);

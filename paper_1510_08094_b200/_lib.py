@@ -32,6 +32,7 @@ EXPORTS = [
     "sk_plan_info", "sk_stage_times", "sk_enable_stage_timing", "sk_last_error", "sk_version",
     "sk_stage_lambda_fwd_peer", "sk_stage_theta_peer", "sk_device_alloc", "sk_device_free", "sk_ipc_handle",
     "sk_ipc_open", "sk_ipc_close", "sk_assemble", "sk_analyze_2d", "sk_sample_grid", "sk_sample_dfs",
+    "sk_solve_grid_exact",
 ]
 
 
@@ -111,6 +112,7 @@ def load() -> ctypes.CDLL:
         "sk_analyze_2d": (I, [P, I, I, P, P, U]),
         "sk_sample_grid": (I, [P, I, I, P, I, I, P, U]),
         "sk_sample_dfs": (I, [P, I, I, P, P, U]),
+        "sk_solve_grid_exact": (I, [P, P, P, P, U]),
         "sk_last_error": (ctypes.c_char_p, []),
         "sk_version": (ctypes.c_char_p, []),
     }

@@ -240,6 +240,40 @@ __global__ void __launch_bounds__(128) residual_kernel(ResidualParams P) {
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(P.out, m);
 }
 
+// F = Msin^2 A column by column (the reference's composition applies
+// band_mul(msin, msin).apply to every column, poisson.cpp:61 / ref harness):
+// row i of Msin^2 is (-1/4, 0, 1/2, 0, -1/4) at offsets -2..2 with 1/4 on the
+// first and last diagonal entries, all imaginary parts +0; the products and
+// the ascending accumulation (including the exact-zero +-1 terms) are those of
+// BandMatrix::apply (banded.cpp:8-19), so F is bit-identical.  One thread per
+// entry, consecutive threads on consecutive columns (coalesced rows).
+__global__ void __launch_bounds__(256) msin2_kernel(int M, int N, const double2* __restrict__ A, double2* __restrict__ F) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(M) * N) return;
+    const int i = static_cast<int>(idx / N);
+    const int kc = static_cast<int>(idx - static_cast<long long>(i) * N);
+    double2 acc = make_double2(0.0, 0.0);
+    const int jlo = i - 2 < 0 ? 0 : i - 2, jhi = i + 2 > M - 1 ? M - 1 : i + 2;
+    for (int c = jlo; c <= jhi; ++c) {
+        const int off = c - i;
+        double s;
+        if (off == 0) s = (i == 0 || i == M - 1) ? 0.25 : 0.5;
+        else if (off == 2 || off == -2) s = -0.25;
+        else s = 0.0;
+        const double2 x = A[static_cast<long long>(c) * N + kc];
+        // (s + 0i) * x, as std::complex multiplication
+        const double2 pr = make_double2(s * x.x - 0.0 * x.y, s * x.y + 0.0 * x.x);
+        acc = make_double2(acc.x + pr.x, acc.y + pr.y);
+    }
+    F[idx] = acc;
+}
+
+cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st) {
+    const long long n = static_cast<long long>(M) * N;
+    msin2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(M, N, A, F);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st) {
     if (P.z) {
         mean_kernel<<<P.nrhs, 256, 0, st>>>(P);

@@ -155,6 +155,7 @@ cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st);
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
+cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 
 }  // namespace sk

@@ -348,8 +348,9 @@ struct sk_plan_s {
     std::vector<double> host_stats;
     // standalone transforms / assemble: FFT plans per length, growable scratch
     std::map<int, DevFft> xf;
-    void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
-    size_t scratch_bytes[4] = {0, 0, 0, 0};
+    static constexpr int kScratch = 8;  // 0-3 assemble / transforms, 4-7 reference-semantics grid solve
+    void* scratch[kScratch] = {};
+    size_t scratch_bytes[kScratch] = {};
 };
 
 namespace {
@@ -1190,6 +1191,59 @@ sk_status sk_sample_dfs(sk_plan_t p, int m, int n, const double* phys, double* g
     if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(grid, out, sizeof(double2) * ng, cudaMemcpyDeviceToHost, p->stream));
     if (!(flags & SK_ASYNC) || !(flags & SK_DEVICE)) CU(cudaStreamSynchronize(p->stream));
     return SK_OK;
+}
+
+
+// Reference-semantics grid solve: the composition the reference runs (and
+// its tests use) — sample_dfs (sphere_domain.cpp:46-52) ->
+// analyze_2d (fourier.cpp:170-188) -> Msin^2 per column (poisson.cpp:61) ->
+// solve (poisson.cpp:121-161) -> sample_grid (fourier.cpp:190-209) — with
+// every stage on the device: K12 dfs_double, two K11 analyze passes, msin2,
+// K5 coeff_solve (bit-exact Thomas, mean precondition), two K11 synthesis
+// passes.  All N lambda modes are solved, k < 0 included, so the result is
+// the reference's complex doubled grid even where the reference's truncated
+// operators make it differ from the Hermitian (real-output) grid path.
+sk_status sk_solve_grid_exact(sk_plan_t p, const double* f, double* U, double* X, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!f || !U) return fail(SK_ERR_ARGUMENT, "null f or U");
+    const int M = p->M, N = p->N;
+    const size_t np = static_cast<size_t>(M / 2 + 1) * N, mn = static_cast<size_t>(M) * N;
+    const bool dev = (flags & SK_DEVICE) != 0;
+    void *g = nullptr, *t = nullptr, *h = nullptr, *in = nullptr;
+    if ((s = scratch(p, 4, sizeof(double2) * mn, &g)) != SK_OK) return s;
+    if ((s = scratch(p, 5, sizeof(double2) * mn, &t)) != SK_OK) return s;
+    if ((s = scratch(p, 6, sizeof(double2) * mn, &h)) != SK_OK) return s;
+    if (!dev && (s = scratch(p, 7, sizeof(double) * np, &in)) != SK_OK) return s;
+    if ((s = ensure(reinterpret_cast<void**>(&p->D), sizeof(double) * mn * p->nrhs)) != SK_OK) return s;
+    double2* G = static_cast<double2*>(g);  // doubled grid, then 2D coefficients, then X
+    double2* T = static_cast<double2*>(t);  // transposed intermediates, then F
+    double2* H = static_cast<double2*>(h);  // u (host calls), X staging
+    CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4 * p->nrhs, p->stream));
+    p->last_launches = 0;
+    for (int r = 0; r < p->nrhs; ++r) {
+        const double* fr = f + r * np;
+        const double* df = fr;
+        if (!dev) {
+            CU(cudaMemcpyAsync(in, fr, sizeof(double) * np, cudaMemcpyHostToDevice, p->stream));
+            df = static_cast<const double*>(in);
+        }
+        CU(sk::launch_dfs_double(M, N, df, G, p->stream));                            // sample_dfs
+        if ((s = xform_pass(p, true, M, N, N, N, G, M, T)) != SK_OK) return s;          // analyze: lambda rows
+        if ((s = xform_pass(p, true, N, M, M, M, T, N, G)) != SK_OK) return s;          // analyze: theta columns
+        CU(sk::launch_msin2(M, N, G, T, p->stream));                                    // F = Msin^2 A
+        double2* dX = (dev && X) ? reinterpret_cast<double2*>(X) + r * mn : G;
+        sk::CoeffParams cp{M, N, 1, T, dX, p->D, p->stats + 4 * r, p->z};
+        CU(sk::launch_coeff_solve(cp, p->stream));                                      // solve
+        if (!dev && X) CU(cudaMemcpyAsync(X + 2 * r * mn, dX, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
+        double2* dU = dev ? reinterpret_cast<double2*>(U) + r * mn : H;
+        if ((s = xform_pass(p, false, M, N, N, N, dX, M, T)) != SK_OK) return s;        // sample_grid: lambda
+        if ((s = xform_pass(p, false, N, M, M, M, T, N, dU)) != SK_OK) return s;        // sample_grid: theta
+        if (!dev) CU(cudaMemcpyAsync(U + 2 * r * mn, dU, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
+        p->last_launches += 9;
+    }
+    if ((flags & SK_ASYNC) && dev) return SK_OK;
+    return check_precondition(p, p->nrhs);
 }
 
 static sk_status make_slabs(sk_plan_t p, int P, const int* rb, const int* cb, int rank, sk::Slabs& sl) {

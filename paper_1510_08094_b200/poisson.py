@@ -15,8 +15,9 @@ LowRankSphereFun / AssembleReport                 LowRankSphereFun / AssembleRep
 analyze_2d(BMCGrid)          fourier.hpp:107      analyze_2d(grid)     -> sk_analyze_2d
 sample_grid(X, m, n)         fourier.hpp:108      sample_grid(X, m, n) -> sk_sample_grid
 sample_dfs(f, m, n)          sphere_domain.hpp:61 sample_dfs(phys, m)  -> sk_sample_dfs (of samples)
-sample_dfs -> analyze_2d -> Msin^2 -> solve ->    solve_grid(f_phys)   -> sk_solve_grid
-  sample_grid (the grid-level composition)
+sample_dfs -> analyze_2d -> Msin^2 -> solve ->    solve_grid(f_phys)   -> sk_solve_grid (real, Hermitian)
+  sample_grid (the grid-level composition)        solve_grid_exact(f_phys) -> sk_solve_grid_exact
+                                                    (the reference's complex doubled grid, every input)
 
 Matrices are numpy complex128 arrays in the reference layout (row i = theta
 mode i - m/2, column kc = lambda mode kc - n/2).  Errors raise the
@@ -39,7 +40,7 @@ __all__ = [
     "Plan", "PoissonProblem", "PoissonSolution", "ResidualReport", "BenchRow", "solve", "residual", "solve_grid",
     "bench_poisson", "integration_weights", "size_error", "precondition_error", "structure_error", "DeviceError",
     "UnsupportedError", "LowRankSphereFun", "AssembleReport", "assemble_poisson", "analyze_2d", "sample_grid",
-    "sample_dfs",
+    "sample_dfs", "solve_grid_exact",
 ]
 
 
@@ -194,6 +195,28 @@ class Plan:
                 Xh = Xh[0]
             return u, Xh
         return u
+
+    def solve_grid_exact(self, f, coeffs: bool = False):
+        """The reference's own grid composition on the device (sk_solve_grid_exact):
+        sample_dfs -> analyze_2d -> Msin^2 -> solve -> sample_grid with all N
+        lambda modes solved.  f: (nrhs, M/2+1, N) or (M/2+1, N) float64.
+        Returns the complex doubled grid U ((nrhs,) M x N, BMCGrid layout) and,
+        with ``coeffs``, the full M x N solution coefficients X."""
+        dev = _is_device(f)
+        self._check_shape(f, (self.M // 2 + 1, self.N))
+        shp = (self.nrhs, self.M, self.N) if (len(f.shape) > 2 or self.nrhs > 1) else (self.M, self.N)
+        if dev:
+            import torch
+            U = torch.empty(shp, dtype=torch.complex128, device=f.device)
+            X = torch.empty(shp, dtype=torch.complex128, device=f.device) if coeffs else None
+        else:
+            f = np.ascontiguousarray(f, dtype=np.float64)
+            U = np.empty(shp, np.complex128)
+            X = np.empty(shp, np.complex128) if coeffs else None
+        self._follow_torch(f)
+        _lib.check(self.lib.sk_solve_grid_exact(self._h, _ptr(f), _ptr(U), _ptr(X),
+                                                _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return (U, X) if coeffs else U
 
     def last_mean(self):
         out = (ctypes.c_double * 3)()
@@ -389,6 +412,16 @@ def solve_grid(f_phys: np.ndarray, m: Optional[int] = None, coeffs: bool = False
     m = 2 * (rows - 1) if m is None else m
     _check_sizes(m, n)
     return _plan(m, n).solve_grid(f_phys, coeffs=coeffs)
+
+
+def solve_grid_exact(f_phys: np.ndarray, m: Optional[int] = None, coeffs: bool = False):
+    """The reference's grid composition (sample_dfs -> analyze_2d -> Msin^2 ->
+    solve -> sample_grid) on the GPU: the complex m x n doubled grid u, every
+    lambda mode solved, for any input (see Plan.solve_grid_exact)."""
+    rows, n = f_phys.shape[-2:]
+    m = 2 * (rows - 1) if m is None else m
+    _check_sizes(m, n)
+    return _plan(m, n).solve_grid_exact(f_phys, coeffs=coeffs)
 
 
 def integration_weights(m: int) -> np.ndarray:

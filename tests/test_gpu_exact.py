@@ -1,0 +1,105 @@
+"""GPU parity of the reference-semantics grid solve (sk_solve_grid_exact)
+against the reference's own composition (oracle/_ref: sample_dfs ->
+analyze_2d -> Msin^2 -> solve -> sample_grid).
+
+Tolerance: max |x_gpu - x_ref| / max |x_ref| <= 1e-10 for U (the complex
+doubled grid) and X (the coefficients) -- north_star's parity bound -- on
+band-limited and on white-noise (under-resolved) inputs alike."""
+import numpy as np
+import pytest
+
+from conftest import golden, ref_grid, zero_mean_noise
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests need a B200 (there is no CPU fallback)")
+    import paper_1510_08094_b200 as p
+    return p
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("m,n", [(64, 48), (256, 128), (512, 256), (150, 150), (96, 160), (18, 24)])
+def test_exact_white_noise_vs_reference(pkg, oracle, reference, m, n):
+    f = zero_mean_noise(oracle, m, n, 11 * m + n)
+    X_ref, U_ref, u_herm = ref_grid(reference, f, m)
+    with pkg.Plan(m, n) as plan:
+        U, X = plan.solve_grid_exact(f, coeffs=True)
+        u_real = plan.solve_grid(f)
+    assert U.shape == (m, n) and X.shape == (m, n)
+    assert _rel(U, U_ref) <= TOL
+    assert _rel(X, X_ref) <= TOL
+    # every k != 0 column of X is the reference's bit-exact Thomas solve of the
+    # device's F; F itself differs from the reference's by FFT rounding only
+    # The real grid path is the Hermitian completion of the same X (declared
+    # in DESIGN.md §4): it matches u_herm, and differs from Re(U_ref) by the
+    # reference's own truncation asymmetry, which white noise exposes.
+    from oracle.oracle import phys_from_doubled
+    assert _rel(u_real, u_herm) <= TOL
+    dev = _rel(u_real, phys_from_doubled(U_ref, m).real)
+    assert dev < 0.1  # O(1e-3) measured; recorded in DESIGN.md
+
+
+@pytest.mark.parametrize("name", ["grid_sh_32x64_L6", "grid_sh_64x64_L12", "grid_sh_128x96_L30",
+                                  "grid_sh_150x150_L20"])
+def test_exact_golden(pkg, name):
+    """The reference's golden outputs (tests/golden, made by the reference
+    itself): complex U and X to 1e-10, u against the analytic solution."""
+    d = golden(name)
+    m, n = d["X"].shape
+    with pkg.Plan(m, n) as plan:
+        U, X = plan.solve_grid_exact(d["phys"], coeffs=True)
+    assert _rel(U, d["U"]) <= TOL
+    assert _rel(X, d["X"]) <= TOL
+
+
+def test_exact_bench_problem_bits(pkg, oracle, reference):
+    """The coefficient-space stage of the exact path is the bit-exact K5 solve:
+    feeding the reference's own F (from its analyze_2d + Msin^2) through
+    sk_solve_coeffs reproduces its X bit for bit for k != 0, so every
+    deviation of the exact grid path is FFT rounding."""
+    m, n = 96, 64
+    f = zero_mean_noise(oracle, m, n, 5)
+    A = reference.analyze_2d(reference.sample_dfs_phys(f, m))
+    F = reference.msin2_columns(A)
+    X_ref = reference.solve(F)
+    with pkg.Plan(m, n) as plan:
+        X = plan.solve_coeffs(F)
+    cols = np.arange(n) != n // 2
+    np.testing.assert_array_equal(X[:, cols], X_ref[:, cols])
+
+
+def test_exact_device_tensors_and_batches(pkg, oracle, reference):
+    import torch
+    m, n, R = 128, 96, 3
+    fs = np.stack([zero_mean_noise(oracle, m, n, 40 + r) for r in range(R)])
+    with pkg.Plan(m, n, nrhs=R) as plan:
+        Ub = plan.solve_grid_exact(fs)
+        Ud = plan.solve_grid_exact(torch.from_numpy(fs).cuda())
+        torch.cuda.synchronize()
+    assert Ub.shape == (R, m, n)
+    np.testing.assert_array_equal(Ud.cpu().numpy(), Ub)
+    for r in range(R):
+        _, U_ref, _ = ref_grid(reference, fs[r], m)
+        assert _rel(Ub[r], U_ref) <= TOL
+
+
+def test_exact_precondition_and_sizes(pkg):
+    m, n = 32, 16
+    with pkg.Plan(m, n) as plan:
+        with pytest.raises(pkg.precondition_error):
+            plan.solve_grid_exact(np.ones((m // 2 + 1, n)))
+        with pytest.raises(pkg.size_error):
+            plan.solve_grid_exact(np.ones((m // 2, n)))
+    with pkg.Plan(8, 602) as plan:  # 602 = 2 * 7 * 43
+        with pytest.raises(pkg.UnsupportedError):
+            plan.solve_grid_exact(np.zeros((5, 602)))

@@ -249,6 +249,17 @@ class Reference(_Lib):
                    _I(threads))
         return X, U
 
+    def grid_pipeline_timed(self, phys, m, threads=1):
+        """grid_pipeline with its phases timed: (X, U, t[sample_dfs, analyze_2d,
+        Msin^2, solve, sample_grid] seconds)."""
+        n = phys.shape[1]
+        X = np.zeros((m, n), np.complex128)
+        U = np.zeros((m, n), np.complex128)
+        t = np.zeros(5)
+        self._call("grid_pipeline_timed", _I(m), _I(n), _ptr(np.ascontiguousarray(phys, np.float64)), _ptr(X),
+                   _ptr(U), _I(threads), _ptr(t))
+        return X, U, t
+
     def assemble_fn(self, fn_id, params, m, n):
         par = np.ascontiguousarray(params, np.float64) if params is not None and len(params) else None
         F = np.zeros((m, n), np.complex128)
@@ -294,6 +305,14 @@ class Reference(_Lib):
         reps = (ctypes.c_int * k)()
         self._call("bench_poisson", _I(k), s, _I(threads), secs, reps)
         return list(secs), list(reps)
+
+    def time_stock_sample(self, m, n, kc0, ncols, j0, nrows, threads):
+        """The reference's stock grid composition on a block of ncols columns
+        and nrows rows of full-size matrices (ref_time_stock_sample): per-unit
+        seconds t[0..4], the sample's wall time t[5], sample_dfs per row t[6]."""
+        t = np.zeros(7)
+        self._call("time_stock_sample", _I(m), _I(n), _I(kc0), _I(ncols), _I(j0), _I(nrows), _I(threads), _ptr(t))
+        return t
 
     def time_sample(self, m, n, ncols, nrows, threads):
         t = np.zeros(5)

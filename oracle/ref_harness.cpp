@@ -287,13 +287,18 @@ int ref_sample_dfs_phys(int m, int n, const double* phys, double* grid) {
 // The grid-level composition: sample_dfs -> analyze_2d ->
 // Msin^2 per column -> solve -> sample_grid.  Outputs the coefficient matrix
 // X (m x n complex) and the doubled solution grid u (m x n complex).
-int ref_grid_pipeline(int m, int n, const double* phys, double* X, double* u, int threads) {
+int ref_grid_pipeline_timed(int m, int n, const double* phys, double* X, double* u, int threads, double* t) {
     return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+        const auto t0 = clk::now();
         std::vector<double> grid(2 * static_cast<size_t>(m) * n);
         if (ref_sample_dfs_phys(m, n, phys, grid.data()) != OK) throw std::runtime_error(g_err);
         BMCGrid g(m, n);
         std::memcpy(g.v.data(), grid.data(), sizeof(complex) * static_cast<size_t>(m) * n);
+        const auto t1 = clk::now();
         const Matrix a = analyze_2d(g);
+        const auto t2 = clk::now();
         const ThetaOperators ops = build_operators(m);
         const BandMatrix msin2 = band_mul(ops.msin, ops.msin);
         PoissonProblem pb;
@@ -306,13 +311,27 @@ int ref_grid_pipeline(int m, int n, const double* phys, double* X, double* u, in
             const std::vector<complex> y = msin2.apply(col);
             for (int i = 0; i < m; ++i) pb.f.at(i, k) = y[i];
         }
+        const auto t3 = clk::now();
         set_threads(threads);
         const PoissonSolution sol = solve(pb);
         set_threads(0);
+        const auto t4 = clk::now();
         if (X) from_matrix(sol.x, X);
         const BMCGrid ug = sample_grid(CoeffMatrix::from_dense(sol.x), m, n);
+        const auto t5 = clk::now();
         if (u) std::memcpy(u, ug.v.data(), sizeof(complex) * static_cast<size_t>(m) * n);
+        if (t) {
+            t[0] = sec(t0, t1);  // sample_dfs (+ copy into the BMCGrid)
+            t[1] = sec(t1, t2);  // analyze_2d
+            t[2] = sec(t2, t3);  // Msin^2 per column
+            t[3] = sec(t3, t4);  // solve
+            t[4] = sec(t4, t5);  // sample_grid (with its CoeffMatrix copies)
+        }
     });
+}
+
+int ref_grid_pipeline(int m, int n, const double* phys, double* X, double* u, int threads) {
+    return ref_grid_pipeline_timed(m, n, phys, X, u, threads, nullptr);
 }
 
 // bench_poisson's coefficient-space workload generator (poisson.cpp:190-216),
@@ -542,6 +561,166 @@ int ref_time_sample(int m, int n, int ncols, int nrows, int threads, double* t) 
         t[3] = sec(t3, t4) / std::max(1, ncols);
         t[4] = sec(t4, t5) / std::max(1, nrows);
         (void)w;
+    });
+}
+
+
+// Stock-composition sample for the CPU baseline (bench.py cpu_baseline /
+// --impl reference): the reference's grid composition (ref_grid_pipeline:
+// analyze_2d fourier.cpp:170-188 -> Msin^2 per column -> solve
+// poisson.cpp:121-161 -> sample_grid fourier.cpp:190-209) run with its OWN
+// loops and access patterns on full-size m x n matrices, restricted to a
+// block of `ncols` consecutive lambda-mode columns (kc0 .. kc0+ncols-1: the
+// strided column gathers / scatters of analyze_2d, solve and sample_grid
+// share cache lines between neighbouring columns exactly as in the full
+// loops) and `nrows` consecutive theta rows.  The column solves run on
+// solve()'s thread pool (min(hw, threads, 16) threads, round-robin,
+// poisson.cpp:147-159); the transforms are single-threaded as shipped.  The
+// matrices persist across calls (allocated and filled once per size).
+// Returns seconds: t[0] theta analysis per column, t[1] lambda analysis per
+// row, t[2] Msin^2 + solve per column, t[3] theta synthesis per column,
+// t[4] lambda synthesis per row, t[5] wall time of this sample, t[6]
+// sample_dfs per row (dfs_extend of every point of the row block from the
+// physical samples, as sample_dfs / ref_sample_dfs_phys evaluate them).
+int ref_time_stock_sample(int m, int n, int kc0, int ncols, int j0, int nrows, int threads, double* t) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        struct Mats {
+            int m = 0, n = 0;
+            Matrix a, half, f, x;
+            std::vector<double> phys;
+        };
+        static Mats S;
+        if (S.m != m || S.n != n) {
+            S = Mats{};
+            S.m = m;
+            S.n = n;
+            S.a = Matrix(m, n);
+            std::mt19937_64 rng(1234);
+            std::uniform_real_distribution<double> unit(-1.0, 1.0);
+            for (int i = 0; i < m; ++i)
+                for (int k = 0; k < n; ++k) S.a.at(i, k) = complex(unit(rng), unit(rng));
+            S.half = Matrix(m, n);
+            S.f = Matrix(m, n);
+            S.x = Matrix(m, n);
+            S.phys.assign(static_cast<size_t>(m / 2 + 1) * n, 0.0);
+            for (auto& v : S.phys) v = unit(rng);
+        }
+        kc0 = std::max(0, std::min(kc0, n - ncols));
+        j0 = std::max(0, std::min(j0, m - nrows));
+        const auto w0 = clk::now();
+        // sample_dfs on the row block (sphere_domain.cpp:46-52 over rows j0..)
+        {
+            const int prow = m / 2 + 1;
+            const double* ph = S.phys.data();
+            const sphere_fn fn = [=](double lam, double th) {
+                const long p = std::lround(th * m / kTwoPi);
+                long q = std::lround((lam + kPi) * n / kTwoPi);
+                q = ((q % n) + n) % n;
+                if (p < 0 || p >= prow) throw index_error("sample_dfs: theta out of range");
+                return complex(ph[static_cast<size_t>(p) * n + q], 0.0);
+            };
+            // grid coordinates as BMCGrid::theta / lambda define them (sphere_domain.hpp:54-55)
+            for (int j = j0; j < j0 + nrows; ++j) {
+                const double th = -kPi + kTwoPi * j / m;
+                for (int k = 0; k < n; ++k) {
+                    const double lam = -kPi + kTwoPi * k / n;
+                    S.a.at(j, k) = dfs_extend(fn, {lam, th});
+                }
+            }
+        }
+        const auto wd = clk::now();
+        const ThetaOperators ops = build_operators(m);
+        const std::vector<complex> w = integration_weights(m);
+        const BandMatrix msin2 = band_mul(ops.msin, ops.msin);
+        volatile double sink = 0;
+        // analyze_2d, column stage (fourier.cpp:176-180)
+        const auto t0 = clk::now();
+        {
+            std::vector<complex> col(m);
+            for (int k = kc0; k < kc0 + ncols; ++k) {
+                for (int j = 0; j < m; ++j) col[j] = S.a.at(j, k);
+                CoeffVec c = analyze_1d(col);
+                for (int j = 0; j < m; ++j) S.half.at(j, k) = c[j];
+            }
+        }
+        // analyze_2d, row stage (fourier.cpp:182-186)
+        const auto t1 = clk::now();
+        {
+            std::vector<complex> row(n);
+            for (int j = j0; j < j0 + nrows; ++j) {
+                for (int k = 0; k < n; ++k) row[k] = S.half.at(j, k);
+                CoeffVec c = analyze_1d(row);
+                for (int k = 0; k < n; ++k) S.f.at(j, k) = c[k];
+            }
+        }
+        // Msin^2 per column (the composition's assembly of F) + solve's
+        // solve_column on its thread pool (poisson.cpp:132-159)
+        const auto t2 = clk::now();
+        {
+            std::vector<complex> col(m);
+            for (int k = kc0; k < kc0 + ncols; ++k) {
+                for (int i = 0; i < m; ++i) col[i] = S.f.at(i, k);
+                const std::vector<complex> y = msin2.apply(col);
+                for (int i = 0; i < m; ++i) S.f.at(i, k) = y[i];
+            }
+            auto solve_column = [&](int kc) {
+                const int k = kc - n / 2;
+                std::vector<complex> rhs(m);
+                for (int i = 0; i < m; ++i) rhs[i] = S.f.at(i, kc);
+                std::vector<complex> x;
+                if (k != 0) {
+                    BandMatrix a = ops.lap;
+                    band_shift_diag(a, -static_cast<double>(k) * k);
+                    x = band_solve(a, rhs);
+                } else {
+                    x = band_solve_with_dense_row(ops.lap, m / 2, w, complex{}, rhs);
+                }
+                for (int i = 0; i < m; ++i) S.x.at(i, kc) = x[i];
+            };
+            unsigned hw = std::thread::hardware_concurrency();
+            const int T = static_cast<int>(std::max(1u, std::min({hw ? hw : 1u, static_cast<unsigned>(std::max(1, threads)), 16u})));
+            if (n < 64 || T <= 1) {
+                for (int kc = kc0; kc < kc0 + ncols; ++kc) solve_column(kc);
+            } else {
+                std::vector<std::thread> pool;
+                for (int th = 0; th < T; ++th)
+                    pool.emplace_back([&, th] {
+                        for (int kc = kc0 + th; kc < kc0 + ncols; kc += T) solve_column(kc);
+                    });
+                for (auto& p : pool) p.join();
+            }
+        }
+        // sample_grid, column stage (fourier.cpp:195-200)
+        const auto t3 = clk::now();
+        {
+            for (int k = kc0; k < kc0 + ncols; ++k) {
+                CoeffVec c(m);
+                for (int j = 0; j < m; ++j) c[j] = S.x.at(j, k);
+                std::vector<complex> vals = synthesize_1d(c, m);
+                for (int j = 0; j < m; ++j) S.half.at(j, k) = vals[j];
+            }
+        }
+        // sample_grid, row stage (fourier.cpp:201-207)
+        const auto t4 = clk::now();
+        {
+            for (int j = j0; j < j0 + nrows; ++j) {
+                CoeffVec c(n);
+                for (int k = 0; k < n; ++k) c[k] = S.half.at(j, k);
+                std::vector<complex> vals = synthesize_1d(c, n);
+                for (int k = 0; k < n; ++k) S.a.at(j, k) = vals[k];  // into the input grid: keeps it O(1)
+                sink = sink + std::abs(vals[0]);
+            }
+        }
+        const auto t5 = clk::now();
+        auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+        t[0] = sec(t0, t1) / std::max(1, ncols);
+        t[1] = sec(t1, t2) / std::max(1, nrows);
+        t[2] = sec(t2, t3) / std::max(1, ncols);
+        t[3] = sec(t3, t4) / std::max(1, ncols);
+        t[4] = sec(t4, t5) / std::max(1, nrows);
+        t[5] = sec(w0, t5);
+        t[6] = sec(w0, wd) / std::max(1, nrows);
     });
 }
 

@@ -1279,11 +1279,10 @@ int exit_relaxed() {
 template <bool SWZ, bool HI>
 static cudaError_t launch_lambda_fwd_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
                                        cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    configure_on_device(attr, [] {
         cudaFuncSetAttribute(lambda_fwd_kernel<SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    });
     lambda_fwd_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
@@ -1293,11 +1292,10 @@ bool lambda_pair_ok(const LambdaParams& P, int nthr) {
 }
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
     if ((P.pair & 1) && lambda_pair_ok(P, nthr)) {
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        configure_on_device(attr, [] {
             cudaFuncSetAttribute(lambda_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr = true;
-        }
+        });
         lambda_fwd_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P, exit_relaxed());
         return cudaGetLastError();
     }
@@ -1311,11 +1309,10 @@ cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int
 template <bool SWZ, bool HI>
 static cudaError_t launch_lambda_inv_t(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem,
                                        cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    configure_on_device(attr, [] {
         cudaFuncSetAttribute(lambda_inv_kernel<SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    });
     lambda_inv_kernel<SWZ, HI><<<P.rows_local * P.nrhs, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
@@ -1324,11 +1321,10 @@ bool lambda_inv_pair_ok(const LambdaParams& P, int nthr) {
 }
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
     if ((P.pair & 2) && lambda_inv_pair_ok(P, nthr)) {  // map has 2-row boxes (make_spec_map box_rows = 2)
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        configure_on_device(attr, [] {
             cudaFuncSetAttribute(lambda_inv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr = true;
-        }
+        });
         lambda_inv_pair_kernel<<<(P.rows_local + 1) & ~1, nthr, smem, st>>>(P, map);
         return cudaGetLastError();
     }
@@ -1341,12 +1337,11 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
 
 template <bool SWZ, int CH, bool HI = false>
 static cudaError_t launch_theta_t(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    configure_on_device(attr, [] {
         cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr = true;
-    }
+    });
     theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P, exit_relaxed());
     return cudaGetLastError();
 }

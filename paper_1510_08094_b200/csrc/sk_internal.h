@@ -3,9 +3,24 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace sk {
+
+// cudaFuncSetAttribute acts on the current device's context: launchers keep
+// one bit per device of the kernels they configured, set only after the
+// attribute calls returned (two threads may both configure; never neither),
+// so a plan on a second device configures its kernels again.
+template <class Fn>
+inline void configure_on_device(std::atomic<unsigned long long>& done, Fn&& set_attributes) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    set_attributes();
+    done.fetch_or(bit, std::memory_order_release);
+}
 
 constexpr int kMaxStages = 24;
 constexpr int kMaxRanks = 16;

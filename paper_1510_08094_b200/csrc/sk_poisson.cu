@@ -345,6 +345,7 @@ struct sk_plan_s {
     bool timing = false;
     cudaEvent_t ev[8] = {};
     double times[4] = {0, 0, 0, 0};
+    int ev_pending = 0;        // stages whose timing events were recorded but not yet read
     std::vector<double> host_stats;
     // standalone transforms / assemble: FFT plans per length, growable scratch
     std::map<int, DevFft> xf;
@@ -429,6 +430,8 @@ extern "C" int sk_debug_phases(unsigned long long* out) {
 #endif
 
 extern "C" {
+
+static void collect_times(sk_plan_t p, int stages);
 
 const char* sk_last_error(void) { return g_err.c_str(); }
 const char* sk_version(void) { return "sk_poisson 0.1 (sm_100a)"; }
@@ -674,6 +677,7 @@ sk_status sk_stage_times(sk_plan_t p, double t[4]) {
     sk_status s = check_plan(p);
     if (s != SK_OK) return s;
     if (!t) return fail(SK_ERR_ARGUMENT, "null output");
+    collect_times(p, 7);  // stage entry points (slab path) leave their events to be read here
     for (int i = 0; i < 4; ++i) t[i] = p->times[i];
     return SK_OK;
 }
@@ -802,7 +806,10 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
             if (ms != SK_OK) return ms;
             CU(sk::launch_lambda_fwd(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
         }
-        if (p->timing) CU(cudaEventRecord(p->ev[1], p->stream));
+        if (p->timing) {
+            CU(cudaEventRecord(p->ev[1], p->stream));
+            p->ev_pending |= 1;
+        }
         p->last_launches += 1;
     }
     if (stages & 2) {
@@ -846,7 +853,10 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         } else {
             CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
         }
-        if (p->timing) CU(cudaEventRecord(p->ev[3], p->stream));
+        if (p->timing) {
+            CU(cudaEventRecord(p->ev[3], p->stream));
+            p->ev_pending |= 2;
+        }
         p->last_launches += 1;
     }
     if (stages & 4) {
@@ -868,7 +878,10 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
             if (ms != SK_OK) return ms;
             CU(sk::launch_lambda_inv(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
         }
-        if (p->timing) CU(cudaEventRecord(p->ev[5], p->stream));
+        if (p->timing) {
+            CU(cudaEventRecord(p->ev[5], p->stream));
+            p->ev_pending |= 4;
+        }
         p->last_launches += 1;
     }
     return SK_OK;
@@ -876,6 +889,9 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
 
 static void collect_times(sk_plan_t p, int stages) {
     if (!p->timing) return;
+    stages &= p->ev_pending;
+    p->ev_pending &= ~stages;
+    if (!stages) return;
     cudaStreamSynchronize(p->stream);
     float ms = 0;
     if (stages & 1) {

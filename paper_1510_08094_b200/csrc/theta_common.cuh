@@ -17,6 +17,15 @@ namespace sk {
 // release would also wait for all of the CTA's global stores to complete
 // (ncu: 10 % membar stalls in lambda_fwd_pair_kernel). relaxed = 0 for A/B
 // (host side: exit_relaxed(), SK_PAIR_SYNC_EXIT=1).
+// CONTRACT at every call site: between the previous cluster barrier and this
+// one a CTA may only LOAD peer shared memory, and every loaded value must be
+// consumed (feed a store or a register the CTA later uses) before the
+// arrive.  A kernel that STORES to peer shared memory (st.shared::cluster,
+// DSMEM atomics), or issues a DSMEM load whose value is unused, must pass
+// relaxed = 0 (release-ordered cluster.sync()).  Kernels with no DSMEM
+// access after their last barrier need no exit barrier at all
+// (lambda_fwd_split_kernel).  tests/test_gpu_layer.py
+// test_exit_barrier_variants_bitwise runs every call site under both forms.
 __device__ __forceinline__ void cluster_exit_barrier(int relaxed) {
     if (relaxed) {
         asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");

@@ -87,11 +87,10 @@ size_t xform_smem_bytes(int n, int nhi, int nlo) {
 
 template <bool ANALYZE, bool SWZ, bool HI>
 static cudaError_t launch_xform_t(const XformParams& P, int nrows, int nthr, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    configure_on_device(attr, [] {
         cudaFuncSetAttribute(xform_kernel<ANALYZE, SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    });
     xform_kernel<ANALYZE, SWZ, HI><<<nrows, nthr, smem, st>>>(P);
     return cudaGetLastError();
 }

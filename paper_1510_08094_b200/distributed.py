@@ -58,6 +58,13 @@ class CudaStages:
     def lambda_inv(self, P, rb, cb, rank, back, u_rows):
         self.plan.stage_lambda_inv(P, rb, cb, rank, back, u_rows)
 
+    def stats(self):
+        """(mean re, mean im, max|F|) of this rank's last theta stage: the
+        k = 0 owner contributes the surface mean 2 pi w^T f~_0, every rank the
+        max |F| of its modes (poisson.cpp:101-117)."""
+        mean, fmax = self.plan.last_mean()
+        return mean.real, mean.imag, fmax
+
 
 class PeerBuffers:
     """A device buffer per rank, shared with every other rank through CUDA
@@ -155,7 +162,10 @@ class SlabSolver:
             plan.stage_lambda_fwd_peer(P, rb, cb, r, f_rows, self.recv_pb.ptrs)
             self._stage_barrier(plan)
             plan.stage_theta_peer(P, rb, cb, r, self.recv, self.back_pb.ptrs)
-            self._stage_barrier(plan)
+            plan.sync()
+            # the all-reduce of the precondition statistics is also the stage
+            # barrier: every rank's theta stores have landed once it returns
+            self.check_precondition()
             plan.stage_lambda_inv(P, rb, cb, r, self.back, u_rows)
             return u_rows
         self.backend.lambda_fwd(P, rb, cb, r, f_rows, self.send)
@@ -163,6 +173,9 @@ class SlabSolver:
         self.backend.theta(P, rb, cb, r, self.recv)
         dist.all_to_all_single(self.back, self.recv, self.send_split, self.recv_split, group=self.group)
         self.backend.lambda_inv(P, rb, cb, r, self.back, u_rows)
+        # the theta stage's statistics stay valid through lambda_inv; checking
+        # after it keeps the exchanges queued back to back
+        self.check_precondition()
         return u_rows
 
     def _stage_barrier(self, plan):
@@ -178,12 +191,20 @@ class SlabSolver:
             self.back_pb.close()
 
     def check_precondition(self):
-        """All-reduce of the mean / max|F| statistics of the last solve and
-        the reference's nonzero-mean test (poisson.cpp:111-116)."""
+        """All-reduce of the mean / max|F| statistics of the last theta stage
+        and the reference's nonzero-mean test (poisson.cpp:111-116): every
+        rank sees the same reduced values, so every rank raises the
+        reference's precondition_error together (the single-GPU sk_solve_grid
+        raises it for the same input)."""
         torch, dist = self.torch, self.dist
-        mean, fmax = self._plan.last_mean()
-        t = torch.tensor([mean.real, mean.imag], dtype=torch.float64, device=self.device)
-        m = torch.tensor([fmax], dtype=torch.float64, device=self.device)
+        stats = getattr(self.backend, "stats", None)
+        if stats is None:
+            return
+        mre, mim, fmax = stats()
+        # NCCL reduces device tensors; gloo (CPU tests, ranks sharing one GPU) host tensors
+        rdev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t = torch.tensor([mre, mim, fmax], dtype=torch.float64, device=rdev)
+        m = t[2:].clone()
         dist.all_reduce(t, group=self.group)
         dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
         mu = complex(t[0].item(), t[1].item())

@@ -37,10 +37,16 @@ class NumpyStages:
         for s in range(P):
             rs = rb[s + 1] - rb[s]
             cols[:, rb[s]: rb[s + 1]] = buf[nc * rb[s]: nc * rb[s + 1]].reshape(nc, rs)
+        # statistics as the CUDA theta stage reports them: the k = 0 owner the
+        # surface mean (here the mean of the k = 0 column), everyone max |F|
+        self._stats = (cols[0].real.mean() if c0 == 0 and nc else 0.0, 0.0, float(np.abs(cols).max()) if nc else 0.0)
         out = self.theta_map(cols, np.arange(c0, c1, dtype=float))
         for s in range(P):
             buf[nc * rb[s]: nc * rb[s + 1]] = out[:, rb[s]: rb[s + 1]].ravel()
         recv.copy_(torch.from_numpy(buf.view(np.float64)))
+
+    def stats(self):
+        return self._stats
 
     def lambda_inv(self, P, rb, cb, rank, back, u_rows):
         import torch
@@ -60,16 +66,26 @@ def _worker(rank, world, port, M, N, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1510_08094_b200._lib import precondition_error
     from paper_1510_08094_b200.distributed import SlabSolver, gather_rows
     rng = np.random.default_rng(7)
     f = rng.standard_normal((M // 2 + 1, N))
+    f -= f.mean()  # zero surface mean (of the stand-in's statistic)
     st = NumpyStages(M, N)
     solver = SlabSolver(M, N, rank, world, device=torch.device("cpu"), backend=st)
     rows = torch.from_numpy(f[solver.rb[rank]: solver.rb[rank + 1]].copy())
     u = solver.solve(rows)
     allu = gather_rows(u, solver.rb)
+    # a nonzero-mean right-hand side raises precondition_error on EVERY rank
+    raised = False
+    try:
+        solver.solve(rows + 1.0)
+    except precondition_error:
+        raised = True
+    flags = [None] * world
+    dist.all_gather_object(flags, raised)
     if rank == 0:
-        q.put((allu.numpy(), st.full(f)))
+        q.put((allu.numpy(), st.full(f), flags))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -91,11 +107,12 @@ def test_slab_orchestration_gloo(world, M, N):
     procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, ref = q.get(timeout=90)
+    got, ref, raised = q.get(timeout=90)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    assert raised == [True] * world, raised
 
 
 def test_slab_bounds_cover():
@@ -134,9 +151,19 @@ def _p2p_worker(rank, world, port, M, N, L, q):
     u = solver.solve(mine)  # second solve reuses the mapped buffers
     torch.cuda.synchronize()
     allu = gather_rows(u.cpu(), solver.rb)
+    # a nonzero-mean right-hand side raises the reference's precondition_error
+    # on every rank (as sk_solve_grid does on one GPU)
+    from paper_1510_08094_b200._lib import precondition_error
+    raised = False
+    try:
+        solver.solve(mine + 1.0)
+    except precondition_error:
+        raised = True
+    flags = [None] * world
+    dist.all_gather_object(flags, raised)
     solver.close()
     if rank == 0:
-        q.put((allu.numpy(), u1.numpy()))
+        q.put((allu.numpy(), u1.numpy(), flags))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -156,8 +183,9 @@ def test_p2p_fused_transposes_bitwise(world, M, N, L):
     procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, M, N, L, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, ref = q.get(timeout=240)
+    got, ref, raised = q.get(timeout=240)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     assert np.array_equal(got, ref)
+    assert raised == [True] * world, raised

@@ -158,3 +158,49 @@ def test_sample_dfs_then_analyze_matches_grid_pipeline(pkg):
     from oracle.oracle import Oracle
     Xo = Oracle().analyze_2d(Oracle().dfs_double(d["phys"], 64))
     assert _rel(X, Xo) <= 1e-14
+
+
+# ------------------------------------------------- cluster exit barriers
+_EXIT_SCRIPT = r'''
+import os, sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, os.path.join(sys.argv[1], "tests"))
+from conftest import zero_mean_noise
+from oracle.oracle import Oracle
+from paper_1510_08094_b200.poisson import Plan
+orc = Oracle()
+out = {}
+# lambda_fwd CTA pairs + theta pair kernel (64 x 3000), theta cluster kernel
+# (32768 x 24), lambda split kernels (64 x 32768), and a full-occupancy grid
+for m, n in [(64, 3000), (32768, 24), (64, 32768), (4000, 3000)]:
+    f = zero_mean_noise(orc, m, n, m + n)
+    with Plan(m, n) as plan:
+        for rep in range(4):
+            out[f"{m}x{n}_{rep}"] = plan.solve_grid(f)
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_exit_barrier_variants_bitwise(tmp_path):
+    """Every cluster kernel ending in cluster_exit_barrier (theta pair,
+    theta cluster, lambda_fwd pairs, lambda_inv split) gives bit-identical
+    results with the relaxed arrive (default) and with the release-ordered
+    cluster.sync() (SK_PAIR_SYNC_EXIT=1), repeatedly and under full
+    occupancy (theta_common.cuh contract)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "exit.py"
+    script.write_text(_EXIT_SCRIPT)
+    res = {}
+    for name, extra in [("relaxed", {}), ("sync", {"SK_PAIR_SYNC_EXIT": "1"})]:
+        env = dict(os.environ, **extra)
+        subprocess.run([sys.executable, str(script), root, str(tmp_path / f"{name}.npz")], check=True, env=env,
+                       timeout=600)
+        res[name] = np.load(tmp_path / f"{name}.npz")
+    keys = sorted(res["relaxed"].files)
+    assert keys and keys == sorted(res["sync"].files)
+    for k in keys:
+        assert np.array_equal(res["relaxed"][k], res["sync"][k]), k
+        base = k.rsplit("_", 1)[0] + "_0"
+        assert np.array_equal(res["relaxed"][k], res["relaxed"][base]), k

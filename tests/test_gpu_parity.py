@@ -399,3 +399,21 @@ def test_lambda_inv_row_pairs_bitwise(pkg, oracle, reference, m, n, paired, monk
     assert np.array_equal(u, u1)
     _, _, u_ref = ref_grid(reference, f, m)
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+def test_bench_multi_rank_launcher():
+    """bench.py --gpus 2 without a launcher re-runs itself under
+    torch.distributed.run with 2 ranks (on a one-GPU box both share GPU 0:
+    gloo plumbing, p2p transport): n_gpus = 2, a slab roofline, parity."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "slab2"
+    assert line["roofline"] is not None and line["roofline"]["slab"]["P"] == 2
+    assert line["parity_rel_err_vs_analytic"] <= 1e-10

@@ -22,6 +22,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 UNITS = [
     ("grid_kernels.cu", []),
     ("grid_large.cu", []),
+    ("theta_sym.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("assemble_kernels.cu", ["--fmad=false"]),
     ("transforms.cu", []),

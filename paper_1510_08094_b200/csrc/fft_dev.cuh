@@ -282,12 +282,15 @@ __device__ __forceinline__ void bf_dit(Bfly<R>& B, double2* a, int span, int tw,
 
 // One stage over all butterflies; small radices keep two butterflies'
 // shared-memory loads in flight.
+// nb_lim >= 0: only the first nb_lim butterflies (the leading sub-transforms
+// of a pruned forward transform, theta_sym.cu).
 template <int R, bool DIF, int SIGN, bool SWZ>
-__device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr) {
+__device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, const Tw& T, int tid, int nthr,
+                                          int nb_lim = -1) {
     const int span = d.span[s], tw = d.tw[s];
     const unsigned mag = d.mag[s];
     const int sh1 = d.sh1[s], sh2 = d.sh2[s];
-    const int nb = d.L / R;
+    const int nb = nb_lim >= 0 ? nb_lim : d.L / R;
     int b = tid;
     if constexpr (R <= 8) {
         for (; b + nthr < nb; b += 2 * nthr) {
@@ -315,28 +318,28 @@ __device__ __forceinline__ void fft_stage(double2* a, const FftDesc& d, int s, c
 // register budget only instantiate the small radices).
 template <bool DIF, int SIGN, bool SWZ, int MAXR = 25>
 __device__ __forceinline__ void fft_stage_dispatch(double2* a, const FftDesc& d, int s, const Tw& T, int tid,
-                                                   int nthr) {
+                                                   int nthr, int nb_lim = -1) {
     if constexpr (MAXR > 8) {
         switch (d.R[s]) {
-            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 8: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 10: fft_stage<10, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 16: fft_stage<16, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 20: fft_stage<20, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            default: fft_stage<25, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 8: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 10: fft_stage<10, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 16: fft_stage<16, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 20: fft_stage<20, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            default: fft_stage<25, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
         }
     } else {  // plans built with radices <= 8 (the plan checks this)
         switch (d.R[s]) {
-            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
-            default: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr); break;
+            case 2: fft_stage<2, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 3: fft_stage<3, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 4: fft_stage<4, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 5: fft_stage<5, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            case 7: fft_stage<7, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
+            default: fft_stage<8, DIF, SIGN, SWZ>(a, d, s, T, tid, nthr, nb_lim); break;
         }
     }
 }

@@ -664,8 +664,10 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
     double2 v[S];
     double ipv[S];
     // Loads with compile-time offsets from a per-thread base: element u sits at
-    // natural index tau0 + dtau (s + u); elements past the chain end read
-    // in-range table entries and slots (their values are masked below).
+    // natural index tau0 + dtau (s + u).  Elements past the chain end read
+    // slot 0 and no table entry: with the digit-reversal window (rev_win) the
+    // entries beyond the chain lie outside the window, and a stray slot index
+    // would address beyond the CTA's shared memory.
     auto load_seg = [&](auto dir) {
         constexpr int D = decltype(dir)::value;
         const int tb = ch.tau0 + (D > 0 ? s : -s);
@@ -673,12 +675,12 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
         const double* ib = ip + tb;
 #pragma unroll
         for (int u = 0; u < S; u += 2) {
-            const unsigned p0 = rb[D * u];
-            const unsigned p1 = (u + 1 < S) ? rb[D * (u + 1)] : 0u;
+            const unsigned p0 = (s + u < n) ? static_cast<unsigned>(rb[D * u]) : 0u;
+            const unsigned p1 = (u + 1 < S && s + u + 1 < n) ? static_cast<unsigned>(rb[D * (u + 1)]) : 0u;
             pk[u / 2] = p0 | (p1 << 16);
         }
 #pragma unroll
-        for (int u = 0; u < S; ++u) ipv[u] = ib[D * u];
+        for (int u = 0; u < S; ++u) ipv[u] = (s + u < n) ? ib[D * u] : 0.0;
     };
     if (ch.dtau > 0) load_seg(std::integral_constant<int, 1>{});
     else load_seg(std::integral_constant<int, -1>{});

@@ -46,6 +46,7 @@ struct ThetaParams {
     PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
     int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
     int hiocc;             // high-occupancy kernel variant (short columns: 64 registers, radices <= 8)
+    const uint32_t* sym_pos;  // theta_sym_kernel: per parity, chain element i -> slots of tau+ (lo 16) and tau- (hi 16)
 };
 
 struct AssembleParams {
@@ -128,6 +129,19 @@ __host__ __device__ inline int theta_data_slots(int L) { return ((L + 1) + 7) & 
 // Pivot-reciprocal slots of the theta kernel (even, so later regions stay
 // 16-byte aligned).
 __host__ __device__ inline int theta_chain_slots(int L) { return ((L / 2 + 4) + 1) & ~1; }
+
+// theta_sym_kernel (theta_sym.cu): pivot window (doubles, even) and chain
+// slot window (uint32, multiple of 4) per CTA; the per-plan tables use the
+// same row strides.
+__host__ __device__ inline int theta_sym_piv_slots(int L) { return ((L / 2 + 2) + 1) & ~1; }
+__host__ __device__ inline int theta_sym_pos_slots(int L) { return ((L / 2 + 1) + 3) & ~3; }
+__host__ __device__ inline size_t theta_sym_smem_bytes(int L, int nhi, int nlo) {
+    return static_cast<size_t>(theta_data_slots(L)) * 16 + static_cast<size_t>(nhi + nlo) * 16 +
+           static_cast<size_t>(theta_sym_piv_slots(L)) * 8 + static_cast<size_t>(theta_sym_pos_slots(L)) * 4 +
+           32 * 32 + 16 * 16 + 64 * 8 + 2 * 8;
+}
+cudaError_t launch_theta_sym(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_pivot_table_sym(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 
 // Dynamic shared memory of theta_kernel (bytes).
 // ints of the theta kernel's digit-reversal window (one chain's slots)

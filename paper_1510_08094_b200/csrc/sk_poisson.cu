@@ -332,6 +332,8 @@ struct sk_plan_s {
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
+    bool theta_sym = false;    // theta_sym_kernel (theta_sym.cu): pruned forward transform, both chains at once
+    uint32_t* sym_pos = nullptr;  // its per-parity chain slot table (2 x theta_sym_pos_slots(M/2))
     // pipelined host-memory solves (SK_HOST | SK_ASYNC)
     static constexpr int kPipe = 3;  // device slots: H2D(i+1), solve(i), D2H(i-1) all in flight
     bool pipe_ready = false;
@@ -587,13 +589,55 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
             const int need = (nmax + p->thr_theta - 1) / p->thr_theta;
             p->chain_mode = p->regsolve == 0 ? 0 : p->regsolve == 2 ? 2 : p->regsolve == 3 ? 1 : (need <= 6 ? 1 : 2);
         }
+        // theta_sym_kernel: long even columns on the one-CTA-per-parity path
+        // whose plan starts with a power-of-two radix over an odd span
+        {
+            const int Lt2 = p->g.Lt, R0 = p->ft.d.nst > 0 ? p->ft.d.R[0] : 0;
+            const bool pow2 = R0 >= 2 && R0 <= 16 && (R0 & (R0 - 1)) == 0;
+            const bool want = !std::getenv("SK_THETA_SYM") || std::atoi(std::getenv("SK_THETA_SYM")) != 0;
+            p->theta_sym = want && !p->theta_q && !p->theta_hiocc && p->kseq == 0 && Lt2 % 2 == 0 && Lt2 < 65536 &&
+                           pow2 && p->ft.d.span[0] % 2 == 1 && p->ft.d.nst >= 2 && Lt2 / 2 <= 12 * p->thr_theta &&
+                           sk::theta_sym_smem_bytes(Lt2, p->ft.d.nhi, p->ft.d.nlo) <= cap;
+        }
+        if (p->theta_sym) {
+            const int Lt2 = p->g.Lt;
+            p->piv_stride = sk::theta_sym_piv_slots(Lt2);
+            p->smem_theta = sk::theta_sym_smem_bytes(Lt2, p->ft.d.nhi, p->ft.d.nlo);
+            p->rev_win = 0;
+            // chain element i of parity par -> (slot of tau+ = tau0 + i) | (slot of tau- = L - 1 - i) << 16
+            const int ps = sk::theta_sym_pos_slots(Lt2);
+            std::vector<uint32_t> tab(2 * static_cast<size_t>(ps), 0u);
+            auto slot = [&](int tau) {
+                int kk = tau, pos = 0;
+                for (int st = 0; st < p->ft.d.nst; ++st) {
+                    pos += (kk % p->ft.d.R[st]) * p->ft.d.span[st];
+                    kk /= p->ft.d.R[st];
+                }
+                return static_cast<uint32_t>(pos);
+            };
+            for (int par = 0; par < 2; ++par)
+                for (int i = 0; i < Lt2 / 2; ++i) {
+                    const int tp = (par == 0 ? 1 : 0) + i, tm = Lt2 - 1 - i;
+                    tab[static_cast<size_t>(par) * ps + i] = (tp < Lt2 ? slot(tp) : 0u) | (slot(tm) << 16);
+                }
+            if ((s = ensure(reinterpret_cast<void**>(&p->sym_pos), sizeof(uint32_t) * tab.size())) != SK_OK) {
+                sk_plan_destroy(p);
+                return s;
+            }
+            if (cudaMemcpy(p->sym_pos, tab.data(), sizeof(uint32_t) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+                sk_plan_destroy(p);
+                return fail(SK_ERR_CUDA, "copy of the chain slot table failed");
+            }
+        }
         const size_t np = static_cast<size_t>(p->g.cols) * 2 * p->piv_stride;
         if ((s = ensure(reinterpret_cast<void**>(&p->pivots), sizeof(double) * np)) != SK_OK) {
             sk_plan_destroy(p);
             return s;
         }
-        if (sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream) != cudaSuccess ||
-            cudaStreamSynchronize(p->stream) != cudaSuccess) {
+        const cudaError_t pe = p->theta_sym
+                                   ? sk::launch_pivot_table_sym(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream)
+                                   : sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream);
+        if (pe != cudaSuccess || cudaStreamSynchronize(p->stream) != cudaSuccess) {
             sk_plan_destroy(p);
             return fail(SK_ERR_CUDA, "pivot table construction failed");
         }
@@ -612,7 +656,7 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
                     static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
                     static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
-                    static_cast<void*>(p->coef_stage), static_cast<void*>(p->pivots)})
+                    static_cast<void*>(p->coef_stage), static_cast<void*>(p->pivots), static_cast<void*>(p->sym_pos)})
         if (q) cudaFree(q);
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
@@ -709,6 +753,7 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     if (p->grid_ok && p->lambda_pair_inv && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda && (p->N / 2 / 256 + 1) % 2 == 0)
         info[13] |= 32;  // inverse lambda rows on CTA pairs (lambda_inv_pair_ok)
+    if (p->theta_sym) info[13] |= 64;  // theta_sym_kernel
     return SK_OK;
 }
 
@@ -830,6 +875,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.rev_win = p->theta_q ? 0 : p->rev_win;
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
         tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes
+        tp.sym_pos = p->sym_pos;
         tp.piv_stride = p->piv_stride;
         if (peers) tp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
@@ -850,6 +896,8 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
                 }
             }
             CU(sk::launch_theta_large(tl, cmap, p->theta_q, p->thr_theta, p->smem_theta, p->stream));
+        } else if (p->theta_sym) {
+            CU(sk::launch_theta_sym(tp, p->thr_theta, p->smem_theta, p->stream));
         } else {
             CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
         }

@@ -417,3 +417,38 @@ def test_bench_multi_rank_launcher():
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "slab2"
     assert line["roofline"] is not None and line["roofline"]["slab"]["P"] == 2
     assert line["parity_rel_err_vs_analytic"] <= 1e-10
+
+
+# --------------------------------------------- theta_sym_kernel (C3 path)
+@pytest.mark.parametrize("m,n", [(6000, 64), (12000, 48), (4200, 40), (20000, 24)])
+def test_theta_sym_rough_data_vs_reference(pkg, oracle, reference, m, n):
+    """Long even theta columns whose plan starts with a power-of-two radix
+    over an odd span run theta_sym_kernel (pruned forward transform through
+    the column's mirror symmetry, both chains of a parity from one solve plus
+    the boundary correction).  White-noise zero-mean data against the
+    reference's own composition: X to 1e-10, u to 1e-10 of the Hermitian
+    completion of the reference's X."""
+    f = zero_mean_noise(oracle, m, n, 5 * m + n)
+    X_ref, _, u_ref = ref_grid(reference, f, m)
+    with pkg.Plan(m, n) as plan:
+        assert plan.info()["variants"] & 64, plan.info()
+        u, Xh = plan.solve_grid(f, coeffs=True)
+    assert np.abs(Xh[: n // 2] - X_ref[:, n // 2:].T).max() <= 1e-10 * np.abs(X_ref).max()
+    assert np.abs(Xh[n // 2] - X_ref[:, 0]).max() <= 1e-10 * np.abs(X_ref).max()
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+@pytest.mark.parametrize("m,n", [(12000, 48), (6000, 64)])
+def test_theta_sym_matches_pair_kernel(pkg, oracle, m, n, monkeypatch):
+    """theta_sym_kernel against the pair kernel it replaces (SK_THETA_SYM=0)
+    on the same rough data: equal to rounding (different but exact
+    arithmetic), and the pair kernel's fast chain solver stays inside its
+    digit-reversal window past the chain ends (M = 12000)."""
+    f = zero_mean_noise(oracle, m, n, m - n)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    monkeypatch.setenv("SK_THETA_SYM", "0")
+    with pkg.Plan(m, n) as plan:
+        assert not plan.info()["variants"] & 64
+        u0 = plan.solve_grid(f)
+    assert np.abs(u - u0).max() <= 1e-12 * np.abs(u0).max()

@@ -42,7 +42,14 @@ __device__ __forceinline__ double lapc_diag(int i, int M) {
     return -__dmul_rn(__dmul_rn(j, j), 0.5);
 }
 
-// warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0
+// warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0.
+// Each thread's sweeps are a long dependent recurrence over M/4 rows; the
+// loads of the rows ahead (F forward, r and d' backward) do not depend on it,
+// so they are issued kPf rows ahead from a register ring (the pointers are
+// __restrict__: the stores of r and d' cannot alias the loads), which keeps
+// kPf * 16 B per thread in flight instead of one row's latency per step.
+constexpr int kPf = 16;
+
 __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     __shared__ double2 s_rm2[32];   // r'_{-2}
     __shared__ double s_dm2[32];    // d'_{-2}
@@ -53,9 +60,9 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     const int rhs = blockIdx.y;
     const bool live = kc < N;
     const size_t off = static_cast<size_t>(rhs) * M * N;
-    const double2* F = P.F + off;
-    double2* X = P.X + off;
-    double* D = P.D + off;
+    const double2* __restrict__ F = P.F + off;
+    double2* __restrict__ X = P.X + off;
+    double* __restrict__ D = P.D + off;
     const int k = kc - N / 2;
     const double negk2 = __dmul_rn(-static_cast<double>(k), static_cast<double>(k));  // -static_cast<double>(k) * k
     // chain rows (storage index i, ascending)
@@ -66,53 +73,86 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     else if (w == 2) { i0 = h + 2; i1 = ((M - 1 - (h + 2)) / 2) * 2 + h + 2; }
     else { i0 = h + 1; i1 = ((M - 1 - (h + 1)) / 2) * 2 + h + 1; }
     if (i1 > M - 1) i1 -= 2;
+    const int nrow = (live && i0 <= i1) ? (i1 - i0) / 2 + 1 : 0;  // rows i0, i0+2, ..., i1
     double fmx = 0.0;
     int bad = 0;
     // ---- forward elimination: d'_i = b_i - (a_i/d'_{i-2}) c_{i-2}; r_i = F_i - l r_{i-2}
     double dprev = 0.0;
     double2 rprev = make_double2(0.0, 0.0);
-    if (live && i0 <= i1) {
-        for (int i = i0; i <= i1; i += 2) {
-            const double2 f = F[static_cast<size_t>(i) * N + kc];
-            fmx = fmax(fmx, hypot(f.x, f.y));
-            const double b = __dadd_rn(lapc_diag(i, M), negk2);
-            double d = b;
-            double2 r = f;
-            if (i > i0) {
-                const double a = lapc_lower(i, M);
-                if (a != 0.0) {
-                    if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
-                    const double l = __ddiv_rn(a, dprev);
-                    d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
-                    r = make_double2(__dsub_rn(f.x, __dmul_rn(l, rprev.x)), __dsub_rn(f.y, __dmul_rn(l, rprev.y)));
+    if (nrow > 0) {
+        double2 ring[kPf];
+#pragma unroll
+        for (int u = 0; u < kPf; ++u)
+            ring[u] = u < nrow ? F[static_cast<size_t>(i0 + 2 * u) * N + kc] : make_double2(0.0, 0.0);
+        for (int q0 = 0; q0 < nrow; q0 += kPf) {
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                const int q = q0 + u;
+                if (q < nrow) {
+                    const int i = i0 + 2 * q;
+                    const double2 f = ring[u];
+                    if (q + kPf < nrow) ring[u] = F[static_cast<size_t>(i + 2 * kPf) * N + kc];
+                    fmx = fmax(fmx, f.x * f.x + f.y * f.y);  // squared (max|F| only scales the precondition test)
+                    const double b = __dadd_rn(lapc_diag(i, M), negk2);
+                    double d = b;
+                    double2 r = f;
+                    if (q > 0) {
+                        const double a = lapc_lower(i, M);
+                        if (a != 0.0) {
+                            if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
+                            const double l = __ddiv_rn(a, dprev);
+                            d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
+                            r = make_double2(__dsub_rn(f.x, __dmul_rn(l, rprev.x)), __dsub_rn(f.y, __dmul_rn(l, rprev.y)));
+                        }
+                    }
+                    if (fabs(d) < 1e-300) bad += 1 << 20;
+                    X[static_cast<size_t>(i) * N + kc] = r;
+                    D[static_cast<size_t>(i) * N + kc] = d;
+                    dprev = d;
+                    rprev = r;
                 }
             }
-            if (fabs(d) < 1e-300) bad += 1 << 20;
-            X[static_cast<size_t>(i) * N + kc] = r;
-            D[static_cast<size_t>(i) * N + kc] = d;
-            dprev = d;
-            rprev = r;
         }
     }
     if (w == 0 && live) {
         s_rm2[lane] = rprev;  // chain ends at j = -2
         s_dm2[lane] = dprev;
     }
-    // ---- back substitution: x_i = (r_i - c_i x_{i+2}) / d'_i
+    // ---- back substitution: x_i = (r_i - c_i x_{i+2}) / d'_i  (rows i1, i1-2, ..., i0)
     double2 xnext = make_double2(0.0, 0.0);
-    if (live && i0 <= i1) {
-        for (int i = i1; i >= i0; i -= 2) {
-            const double2 r = X[static_cast<size_t>(i) * N + kc];
-            const double d = D[static_cast<size_t>(i) * N + kc];
-            double2 acc = r;
-            if (i + 2 <= M - 1) {
-                const double c = lapc_upper(i, M);
-                if (c != 0.0)
-                    acc = make_double2(__dsub_rn(acc.x, __dmul_rn(c, xnext.x)), __dsub_rn(acc.y, __dmul_rn(c, xnext.y)));
+    if (nrow > 0) {
+        double2 rr[kPf];
+        double dr[kPf];
+#pragma unroll
+        for (int u = 0; u < kPf; ++u) {
+            const size_t at = static_cast<size_t>(i1 - 2 * u) * N + kc;
+            rr[u] = u < nrow ? X[at] : make_double2(0.0, 0.0);
+            dr[u] = u < nrow ? D[at] : 1.0;
+        }
+        for (int q0 = 0; q0 < nrow; q0 += kPf) {
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                const int q = q0 + u;
+                if (q < nrow) {
+                    const int i = i1 - 2 * q;
+                    const double2 r = rr[u];
+                    const double d = dr[u];
+                    if (q + kPf < nrow) {
+                        const size_t at = static_cast<size_t>(i - 2 * kPf) * N + kc;
+                        rr[u] = X[at];
+                        dr[u] = D[at];
+                    }
+                    double2 acc = r;
+                    if (i + 2 <= M - 1) {
+                        const double c = lapc_upper(i, M);
+                        if (c != 0.0)
+                            acc = make_double2(__dsub_rn(acc.x, __dmul_rn(c, xnext.x)), __dsub_rn(acc.y, __dmul_rn(c, xnext.y)));
+                    }
+                    const double2 x = make_double2(__ddiv_rn(acc.x, d), __ddiv_rn(acc.y, d));
+                    X[static_cast<size_t>(i) * N + kc] = x;
+                    xnext = x;
+                }
             }
-            const double2 x = make_double2(__ddiv_rn(acc.x, d), __ddiv_rn(acc.y, d));
-            X[static_cast<size_t>(i) * N + kc] = x;
-            xnext = x;
         }
     }
     if (w == 2 && live) s_x2[lane] = xnext;  // chain starts at j = 2
@@ -120,7 +160,7 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     // ---- row j = 0
     if (w == 0 && live) {
         const double2 f0 = F[static_cast<size_t>(h) * N + kc];
-        fmx = fmax(fmx, hypot(f0.x, f0.y));
+        fmx = fmax(fmx, f0.x * f0.x + f0.y * f0.y);
         const bool has_m2 = (h - 2) >= 0;
         const bool has_p2 = (h + 2) <= M - 1;
         if (k != 0) {
@@ -152,7 +192,7 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
         X[static_cast<size_t>(h) * N + kc] = make_double2(-__ddiv_rn(s.x, 2.0), -__ddiv_rn(s.y, 2.0));
     }
     // stats
-    const double fm = warp_max(live ? fmx : 0.0);
+    const double fm = sqrt(warp_max(live ? fmx : 0.0));
     if (lane == 0) atomic_max_nonneg(P.stats + 4 * rhs + 2, fm);
     if (bad) atomicAdd(P.stats + 4 * rhs + 3, static_cast<double>(bad));
 }

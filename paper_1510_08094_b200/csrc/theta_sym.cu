@@ -409,6 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     // ---- bulk copies: raw column (L+1), this (mode, parity)'s pivots, the chain slot window
     if (tid == 0) {
         mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -420,14 +421,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
         }
         const uint32_t pb = static_cast<uint32_t>(theta_sym_piv_slots(L)) * 8;
         const uint32_t qb = static_cast<uint32_t>(theta_sym_pos_slots(L)) * 4;
-        mbar_expect_tx(&bars[0], bytes + pb + qb);
+        // the column (needed first) and the chain windows (needed after the
+        // forward transform) complete on separate barriers
+        mbar_expect_tx(&bars[0], bytes);
+        mbar_expect_tx(&bars[1], pb + qb);
         for (int s = 0; s < P.sl.P; ++s) {
             const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
             if (r1 > r0)
                 bulk_g2s_chunked(a + r0, colbase + theta_addr(P.sl, P.ncols, kl, r0), (r1 - r0) * 16, &bars[0]);
         }
-        bulk_g2s_chunked(ip, P.pivots + prow, pb, &bars[0]);
-        bulk_g2s_chunked(pw, P.sym_pos + static_cast<size_t>(par) * theta_sym_pos_slots(L), qb, &bars[0]);
+        bulk_g2s_chunked(ip, P.pivots + prow, pb, &bars[1]);
+        bulk_g2s_chunked(pw, P.sym_pos + static_cast<size_t>(par) * theta_sym_pos_slots(L), qb, &bars[1]);
     }
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     mbar_wait(&bars[0], 0);
@@ -442,6 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     const double2 cofs = make_double2((1.0 - sgn) * c0.x, (1.0 - sgn) * c0.y);
     const int kcnt = R0 / 2 + 1 - par;
     fft_forward_sub<25>(a, P.fd, T, tid, nthr, kcnt);
+    mbar_wait(&bars[1], 0);  // pivot and chain slot windows
 
     const SymRead rd{a, pw, par == 0 ? 1 : 0, par, R0, sgn, cofs};
     // ---- k = 0, even class: surface mean 2 pi w^T X_0 (poisson.cpp:101-117)

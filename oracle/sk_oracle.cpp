@@ -481,11 +481,16 @@ void sample_grid(int rows, int cols, const cplx* X, int m, int n, cplx* g) {  //
 // evaluated on the grid of :46-52 — theta_i >= 0 (i >= M/2) reads physical
 // row i - M/2; theta_i < 0 reads row M/2 - i at longitude shifted by pi,
 // i.e. column (q + N/2) mod N.
+// theta_i is evaluated as sphere_domain.hpp:54 does (-kPi + kTwoPi i / m):
+// for some m (22, 30, 44, 60, ...) theta_{m/2} rounds below zero and the
+// reference glides the pole row p = 0 as well.
 void dfs_double(int m, int n, const double* phys, cplx* g) {
+    const double kPi_ = 3.141592653589793238462643383279502884, kTwoPi_ = 2.0 * kPi_;
     for (int i = 0; i < m; ++i)
         for (int q = 0; q < n; ++q) {
             double v;
-            if (i >= m / 2) v = phys[static_cast<size_t>(i - m / 2) * n + q];
+            const double th = -kPi_ + kTwoPi_ * i / m;
+            if (th >= 0.0) v = phys[static_cast<size_t>(i - m / 2) * n + q];
             else v = phys[static_cast<size_t>(m / 2 - i) * n + (q + n / 2) % n];
             g[static_cast<size_t>(i) * n + q] = cplx(v, 0.0);
         }

@@ -189,6 +189,89 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
     cluster_exit_barrier(relaxed_exit);
 }
 
+// Row groups of G = 4 (p .. p+3) on a 4-CTA cluster (single RHS, unswizzled
+// rows; C3), the generalisation of lambda_fwd_pair_kernel: each CTA
+// transforms its row and leaves the N/2+1 modes in natural order in shared
+// memory; CTA c then stores the modes of its quarter of k for all four rows,
+// four adjacent lanes writing (p .. p+3) of one mode: a warp's store covers 8
+// modes x 64 contiguous bytes (two full 32-byte sectors each) where the pair
+// kernel covered 16 x 32 and the one-row kernel 32 x 16.  The peers' rows are
+// read through DSMEM in natural order (eight consecutive modes per CTA per
+// warp access).  With peer stores (fused multi-GPU transpose) the same 64-byte
+// runs go to the owner of mode k over NVLink.  Grid = rows rounded up to a
+// multiple of 4; padding CTAs only take part in the cluster barriers.
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 2) lambda_fwd_quad_kernel(LambdaParams P, int relaxed_exit) {
+    constexpr int G = 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int L = P.fd.L;
+    const int Lpad = (L / kBoxModes + 1) * kBoxModes;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + Lpad;
+    double2* s_lo = s_hi + P.fd.nhi;
+    int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((L + 3) & ~3));
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int c = static_cast<int>(cluster.block_rank());
+    const int row = blockIdx.x;
+    const bool live = row < P.rows_local;  // CTA-uniform
+    if (live && tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, static_cast<uint32_t>(L) * 16);
+        bulk_g2s_chunked(a, reinterpret_cast<const double2*>(P.f + static_cast<long long>(row) * P.g.N),
+                         static_cast<uint32_t>(L) * 16, bar);
+    }
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    for (int i = tid; i < L; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
+    __syncthreads();
+    if (live) {
+        mbar_wait(bar, 0);
+        fft_forward<false, 25>(a, P.fd, T, tid, nthr);
+        const double invN = 1.0 / P.g.N;
+        double2 vk[kLamPairs], vm[kLamPairs];
+#pragma unroll
+        for (int u = 0; u < kLamPairs; ++u) {
+            const int k = tid + u * nthr;
+            if (k <= L / 2) {
+                const int km = L - k;
+                const double2 z = a[s_rev[k]];
+                const double2 zp = a[s_rev[km == L ? 0 : km]];
+                const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
+                const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
+                vk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
+                vm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kLamPairs; ++u) {
+            const int k = tid + u * nthr;
+            if (k <= L / 2) {
+                a[k] = vk[u];
+                if (L - k != k) a[L - k] = vm[u];
+            }
+        }
+    }
+    cluster.sync();
+    const double2* src[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) src[g] = cluster.map_shared_rank(a, g);
+    const int r0 = row - c;  // first row of the group
+    const int nk = L + 1;
+    const int k_lo = (c * nk) / G, k_hi = ((c + 1) * nk) / G;
+    const int sub_hi = min(G, P.rows_local - r0);  // rows of the group that exist
+    for (int i = tid; i < G * (k_hi - k_lo); i += nthr) {
+        const int k = k_lo + (i >> 2), sub = i & 3;
+        if (sub < sub_hi) {
+            const double2 v = src[sub][k];
+            if (P.peers.n) *peer_ptr(P.peers, k, k, r0 + sub) = v;  // fused transpose over NVLink
+            else P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = v;
+        }
+    }
+    cluster_exit_barrier(relaxed_exit);  // only consumed DSMEM loads since the last cluster barrier
+}
+
 // Inverse: TMA tensor loads gather the row's N/2+1 modes from the mode-major
 // spectrum; sample_grid's (-1)^k (fourier.cpp:61-62) and the packing into
 // N/2 complex go through registers into digit-reversed order; inverse DIT
@@ -1017,6 +1100,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
     }
     mbar_wait(&bars[0], 0);
     __syncthreads();
+    if (P.g.pole_glide && (kg & 1)) {  // the reference's doubled row j = M/2 (sk_internal.h GridGeom)
+        if (tid == 0) a[0] = make_double2(-a[0].x, -a[0].y);
+        __syncthreads();
+    }
 
     SK_PROBE(1);
     // ---- DFS fold (first radix-2 step), scaled by 1/M.  With the swizzled
@@ -1292,7 +1379,18 @@ bool lambda_pair_ok(const LambdaParams& P, int nthr) {
     return !P.swizzle && !P.hiocc && P.nrhs == 1 && P.peers.n == 0 && nthr <= 256 &&
            P.fd.L / 2 + 1 <= kLamPairs * nthr;
 }
+bool lambda_quad_ok(const LambdaParams& P, int nthr) {
+    return !P.swizzle && !P.hiocc && P.nrhs == 1 && nthr <= 256 && P.fd.L / 2 + 1 <= kLamPairs * nthr;
+}
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    if ((P.pair & 4) && lambda_quad_ok(P, nthr)) {
+        static std::atomic<unsigned long long> attr{0};
+        configure_on_device(attr, [] {
+            cudaFuncSetAttribute(lambda_fwd_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        });
+        lambda_fwd_quad_kernel<<<(P.rows_local + 3) & ~3, nthr, smem, st>>>(P, exit_relaxed());
+        return cudaGetLastError();
+    }
     if ((P.pair & 1) && lambda_pair_ok(P, nthr)) {
         static std::atomic<unsigned long long> attr{0};
         configure_on_device(attr, [] {

@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
                 const int r = c * CB + i;
                 if (r < Lq) {
                     const int j = Q * r + q;
-                    const double2 vj = aj[i];
+                    double2 vj = aj[i];
+                    if (j == 0 && P.g.pole_glide) vj = cscale(vj, sgn);  // sk_internal.h GridGeom::pole_glide
                     const double2 vm = (q == 0 && r == 0) ? aL : am[CB - 1 - i];
                     double2 x;
                     if (par == 0) x = make_double2((vj.x + sgn * vm.x) * invM, (vj.y + sgn * vm.y) * invM);
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(512, 1) theta_large_kernel(ThetaLargeParams PL
                     const int j = Q * r + q;
                     aj[u] = *gcol(j);
                     am[u] = *gcol(L - j);
+                    if (j == 0 && P.g.pole_glide) aj[u] = cscale(aj[u], sgn);  // sk_internal.h GridGeom::pole_glide
                 }
             }
 #pragma unroll

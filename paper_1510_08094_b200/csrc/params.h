@@ -24,7 +24,8 @@ struct LambdaParams {
     PeerMap peers;      // fwd: mode k of this rank's rows goes straight to its theta rank's receive buffer
     int swizzle;        // XOR-swizzled shared-memory slots (plans whose first FFT span is even)
     int hiocc;          // high-occupancy kernel variant (short rows: 64 registers, radices <= 8)
-    int pair;           // bit 0 fwd, bit 1 inv: row pairs on CTA pairs, 32-byte (p, p+1) segments (lambda_pair_ok decides)
+    int pair;           // bit 0 fwd, bit 1 inv: row pairs on CTA pairs, 32-byte (p, p+1) segments (lambda_pair_ok decides);
+                        // bit 2 fwd: row quads on 4-CTA clusters, 64-byte (p .. p+3) segments (lambda_quad_ok)
 };
 
 struct ThetaParams {
@@ -154,7 +155,8 @@ __host__ __device__ inline size_t theta_smem_bytes(int L, int nhi, int nlo, bool
 
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
 int exit_relaxed();  // 1 unless SK_PAIR_SYNC_EXIT is set: relaxed cluster exit barriers
-bool lambda_inv_pair_ok(const LambdaParams& P, int nthr);  // inverse on CTA pairs (needs 2-row boxes)
+bool lambda_inv_pair_ok(const LambdaParams& P, int nthr);
+bool lambda_quad_ok(const LambdaParams& P, int nthr);  // inverse on CTA pairs (needs 2-row boxes)
 cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st);
 // Lambda-stage shared memory (bytes) for transform length L and twiddle table sizes.
 inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
@@ -167,6 +169,15 @@ cudaError_t launch_assemble(const AssembleParams& P, cudaStream_t st);
 size_t xform_smem_bytes(int n, int nhi, int nlo);
 cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st);
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st);
+// theta_{m/2} = -pi + 2 pi (m/2) / m evaluated exactly as the reference does
+// (sphere_domain.hpp:54, types.hpp:12-13) is negative: the reference's
+// sample_dfs glides the pole row p = 0 (sk_internal.h GridGeom::pole_glide)
+inline int pole_glide(int m) {
+    const double kPi = 3.141592653589793238462643383279502884;
+    const double kTwoPi = 2.0 * kPi;
+    const int j = m / 2;
+    return (-kPi + kTwoPi * j / m) < 0.0 ? 1 : 0;
+}
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
 cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st);

@@ -79,6 +79,13 @@ struct GridGeom {
     int Ll = 0;   // lambda FFT length N/2
     int rows = 0; // M/2 + 1 physical rows
     int cols = 0; // N/2 + 1 lambda modes (k >= 0)
+    // The reference's sample_dfs evaluates theta_j = -pi + 2 pi j / M in
+    // floating point (sphere_domain.hpp:54) and dfs_extend glides every
+    // theta < 0 (sphere_domain.cpp:19-26).  For some M (22, 30, 44, 60, ...)
+    // theta_{M/2} rounds to a tiny negative number, so the doubled row j = M/2
+    // reads the pole row p = 0 at longitude lambda -+ pi: spectrally s = (-1)^k
+    // times its own coefficients.  Replicated when set (sk_pole_glide).
+    int pole_glide = 0;
 };
 
 }  // namespace sk

@@ -326,6 +326,11 @@ struct sk_plan_s {
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
     bool lambda_hiocc = false; // high-occupancy lambda kernel variant (short rows)
     bool lambda_pair = true;   // forward lambda rows on CTA pairs (32-byte stores); SK_LAMBDA_PAIR=0 for A/B
+    // forward lambda rows on 4-CTA clusters (64-byte stores): the default for peer stores (fused multi-GPU
+    // transpose; the pair kernel has no peer path); for local stores measured slower than the pair kernel at
+    // C3 (0.72 vs 0.665 ms: 3/4 of the modes come through DSMEM, half of them from the other SM), so opt-in
+    // there: SK_LAMBDA_QUAD=1 (=0 disables it for peer stores too)
+    int lambda_quad = -1;
     // inverse lambda rows on CTA pairs (32-byte gathers): opt-in, SK_LAMBDA_PAIR_INV=1. Measured slower at C3
     // (0.80 vs 0.57 ms: the peer's modes are 16-byte DSMEM reads at a 32-byte stride)
     bool lambda_pair_inv = false;
@@ -471,6 +476,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     p->g.Ll = N / 2;
     p->g.rows = M / 2 + 1;
     p->g.cols = N / 2 + 1;
+    p->g.pole_glide = sk::pole_glide(M);
     sk_status s;
     if ((s = ensure(reinterpret_cast<void**>(&p->stats), sizeof(double) * 4 * nrhs)) != SK_OK) {
         sk_plan_destroy(p);
@@ -547,6 +553,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // (64 registers, radices <= 8, <= 6 mode pairs per thread; SK_NO_HIOCC)
     p->lambda_hiocc = p->thr_lambda <= 128 && (Ll / 2 + 1) <= 6 * p->thr_lambda && !std::getenv("SK_NO_HIOCC");
     if (const char* e = std::getenv("SK_LAMBDA_PAIR")) p->lambda_pair = std::atoi(e) != 0;  // A/B
+    if (const char* e = std::getenv("SK_LAMBDA_QUAD")) p->lambda_quad = std::atoi(e) != 0 ? 1 : 0;  // A/B
     if (const char* e = std::getenv("SK_LAMBDA_PAIR_INV")) p->lambda_pair_inv = std::atoi(e) != 0;  // opt-in A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
@@ -749,11 +756,14 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     const bool hi_l = p->lambda_hiocc && !p->lambda_split;
     if (p->grid_ok && p->lambda_pair && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 && p->thr_lambda <= 256 &&
         p->N / 4 + 1 <= 12 * p->thr_lambda)
-        info[13] |= 16;  // forward lambda rows on CTA pairs (lambda_pair_ok, single GPU)
+        info[13] |= 16;  // forward lambda rows on CTA pairs (lambda_pair_ok, local stores)
     if (p->grid_ok && p->lambda_pair_inv && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda && (p->N / 2 / 256 + 1) % 2 == 0)
         info[13] |= 32;  // inverse lambda rows on CTA pairs (lambda_inv_pair_ok)
     if (p->theta_sym) info[13] |= 64;  // theta_sym_kernel
+    if (p->grid_ok && p->lambda_quad != 0 && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
+        p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda)
+        info[13] |= 128;  // forward lambda rows on 4-CTA clusters: peer stores (default) or any (SK_LAMBDA_QUAD=1)
     return SK_OK;
 }
 
@@ -832,7 +842,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
     lp.fd = p->fl.d;
     lp.swizzle = (p->fl.d.nst > 0 && p->fl.d.span[0] % 2 == 0) ? 1 : 0;  // power-of-two rows
     lp.hiocc = p->lambda_hiocc && !p->lambda_split ? 1 : 0;
-    lp.pair = p->lambda_pair ? 1 : 0;
+    lp.pair = (p->lambda_pair ? 1 : 0) | ((p->lambda_quad == 1 || (p->lambda_quad < 0 && peers)) ? 4 : 0);
     lp.rows_local = rows_local;
     lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
     if (stages & 1) {

@@ -436,6 +436,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     mbar_wait(&bars[0], 0);
     __syncthreads();
+    if (P.g.pole_glide && (kg & 1)) {  // the reference's doubled row j = M/2 (sk_internal.h GridGeom)
+        if (tid == 0) a[0] = make_double2(-a[0].x, -a[0].y);
+        __syncthreads();
+    }
 
     // ---- fused fold + first DIF stage (butterfly pairs), then the computed sub-transforms
     const double invM = 1.0 / P.g.M;

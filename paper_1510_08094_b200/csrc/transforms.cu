@@ -72,12 +72,15 @@ __global__ void __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) xform_kernel(Xform
 // doubled[j][k] = phys[j - m/2][k] (j >= m/2), phys[m/2 - j][(k + n/2) mod n]
 // (j < m/2): the glide reflection f(lambda -+ pi, -theta) of dfs_extend as an
 // index map on the physical rows theta_p = 2 pi p / m, p = 0..m/2.
-__global__ void dfs_double_kernel(int m, int n, const double* phys, double2* grid) {
+// pole_glide: row j = m/2 glides too (theta_{m/2} rounds below zero in the
+// reference for some m; sk_internal.h GridGeom::pole_glide).
+__global__ void dfs_double_kernel(int m, int n, const double* phys, double2* grid, int pole_glide) {
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= static_cast<long long>(m) * n) return;
     const int j = static_cast<int>(idx / n), k = static_cast<int>(idx - static_cast<long long>(j) * n);
-    const double v = (j >= m / 2) ? phys[static_cast<long long>(j - m / 2) * n + k]
-                                  : phys[static_cast<long long>(m / 2 - j) * n + (k + n / 2) % n];
+    const bool glide = j < m / 2 || (pole_glide && j == m / 2);
+    const double v = glide ? phys[static_cast<long long>(m / 2 - j) * n + (k + n / 2) % n]
+                           : phys[static_cast<long long>(j - m / 2) * n + k];
     grid[idx] = make_double2(v, 0.0);
 }
 
@@ -112,7 +115,8 @@ cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr
 
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st) {
     const long long tot = static_cast<long long>(m) * n;
-    if (tot > 0) dfs_double_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(m, n, phys, grid);
+    if (tot > 0)
+        dfs_double_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(m, n, phys, grid, pole_glide(m));
     return cudaGetLastError();
 }
 

@@ -169,10 +169,11 @@ def _p2p_worker(rank, world, port, M, N, L, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,M,N,L", [(2, 512, 256, 40), (3, 240, 200, 30)])
+@pytest.mark.parametrize("world,M,N,L", [(2, 512, 256, 40), (3, 240, 200, 30), (2, 64, 3000, 12)])
 def test_p2p_fused_transposes_bitwise(world, M, N, L):
     """The fused peer-store slab solve equals the single-GPU grid solve bit
-    for bit (the theta stage is slab-invariant)."""
+    for bit (the theta stage is slab-invariant); 64 x 3000 runs the forward
+    lambda stage on 4-CTA clusters with 64-byte peer stores."""
     import torch
     if not torch.cuda.is_available():
         pytest.fail("no CUDA device")

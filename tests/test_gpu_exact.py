@@ -28,7 +28,7 @@ def _rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-@pytest.mark.parametrize("m,n", [(64, 48), (256, 128), (512, 256), (150, 150), (96, 160), (18, 24)])
+@pytest.mark.parametrize("m,n", [(64, 48), (256, 128), (512, 256), (150, 150), (96, 160), (18, 24), (60, 32), (120, 40)])
 def test_exact_white_noise_vs_reference(pkg, oracle, reference, m, n):
     f = zero_mean_noise(oracle, m, n, 11 * m + n)
     X_ref, U_ref, u_herm = ref_grid(reference, f, m)

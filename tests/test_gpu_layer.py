@@ -204,3 +204,13 @@ def test_exit_barrier_variants_bitwise(tmp_path):
         assert np.array_equal(res["relaxed"][k], res["sync"][k]), k
         base = k.rsplit("_", 1)[0] + "_0"
         assert np.array_equal(res["relaxed"][k], res["relaxed"][base]), k
+
+
+@pytest.mark.parametrize("m,n", [(60, 8), (30, 6), (22, 10), (64, 8)])
+def test_sample_dfs_pole_row_quirk(pkg, oracle, m, n):
+    """sk_sample_dfs replicates the reference's floating-point pole row (for
+    m = 22, 30, 60 theta_{m/2} < 0 in the reference: the row p = 0 glides),
+    bit for bit against the reference-pinned restatement."""
+    rng = np.random.default_rng(m + n)
+    phys = rng.standard_normal((m // 2 + 1, n))
+    np.testing.assert_array_equal(pkg.sample_dfs(phys, m), oracle.dfs_double(phys, m))

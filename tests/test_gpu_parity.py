@@ -143,7 +143,7 @@ def test_grid_solve_vs_reference(pkg, oracle, reference, m, n, L):
     assert np.abs(Xh[: n // 2] - X_ref[:, n // 2:].T).max() <= 1e-10 * np.abs(X_ref).max()
 
 
-@pytest.mark.parametrize("m,n", [(64, 48), (256, 128), (150, 150)])
+@pytest.mark.parametrize("m,n", [(64, 48), (256, 128), (150, 150), (60, 32), (120, 40), (30, 64)])
 def test_grid_solve_rough_data_vs_reference(pkg, oracle, reference, m, n):
     """Non-band-limited (white-noise) data with zero mean, against the
     reference's own composition (oracle/_ref).  The reference solves every
@@ -362,21 +362,28 @@ def test_pipelined_host_solves(pkg, oracle):
             plan.sync()
 
 
-@pytest.mark.parametrize("m,n", [(64, 3000), (128, 3000), (40, 2400)])
-def test_lambda_row_pairs_bitwise(pkg, oracle, reference, m, n, monkeypatch):
+@pytest.mark.parametrize("m,n", [(64, 3000), (128, 3000), (40, 2400), (54, 3000), (50, 3000), (60, 3000)])
+def test_lambda_row_groups_bitwise(pkg, oracle, reference, m, n, monkeypatch):
     """Long non-power-of-two lambda rows run the forward lambda transform on
-    CTA pairs (row pairs, 32-byte stores; the odd row count M/2+1 leaves a padding
-    CTA): bit-identical to the one-row-per-CTA kernel, and against the
-    oracle on rough zero-mean data."""
+    CTA pairs (row pairs, 32-byte stores; default), on 4-CTA clusters
+    (SK_LAMBDA_QUAD=1: row quads, 64-byte stores; the default for peer
+    stores) or one row per CTA (SK_LAMBDA_QUAD=0 SK_LAMBDA_PAIR=0); row counts
+    M/2+1 = 33, 65, 21, 28, 26, 31 cover every padding case.  All three are
+    bit-identical, and against the reference on rough zero-mean data."""
     f = zero_mean_noise(oracle, m, n, m * n)
+    monkeypatch.setenv("SK_LAMBDA_QUAD", "1")
     with pkg.Plan(m, n) as plan:
-        assert plan.info()["variants"] & 16, plan.info()
+        assert plan.info()["variants"] & 128, plan.info()
         u = plan.solve_grid(f)
+    monkeypatch.setenv("SK_LAMBDA_QUAD", "0")
+    with pkg.Plan(m, n) as plan:
+        assert not plan.info()["variants"] & 128 and plan.info()["variants"] & 16
+        u2 = plan.solve_grid(f)
     monkeypatch.setenv("SK_LAMBDA_PAIR", "0")
     with pkg.Plan(m, n) as plan:
         assert not plan.info()["variants"] & 16
         u1 = plan.solve_grid(f)
-    assert np.array_equal(u, u1)
+    assert np.array_equal(u, u1) and np.array_equal(u2, u1)
     _, _, u_ref = ref_grid(reference, f, m)
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 

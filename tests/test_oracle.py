@@ -148,3 +148,15 @@ def test_oracle_transforms_match_reference_golden(oracle, name):
 def test_oracle_dfs_double_golden(oracle, name):
     d = golden(name)
     assert np.array_equal(oracle.dfs_double(d["phys"], d["grid"].shape[0]), d["grid"])
+
+
+@pytest.mark.parametrize("m,n", [(60, 8), (30, 6), (22, 10), (64, 8), (150, 12), (44, 4)])
+def test_dfs_doubling_pole_row_matches_reference(oracle, reference, m, n):
+    """The reference's sample_dfs evaluates theta_j = -pi + 2 pi j/m in floating
+    point (sphere_domain.hpp:54) and glides every theta < 0
+    (sphere_domain.cpp:19-26): for m = 22, 30, 44, 60, ... theta_{m/2} rounds
+    below zero, so the pole row p = 0 is read at longitude lambda -+ pi.  The
+    restatement's index map reproduces the reference bit for bit."""
+    rng = np.random.default_rng(m * n)
+    phys = rng.standard_normal((m // 2 + 1, n))
+    np.testing.assert_array_equal(oracle.dfs_double(phys, m), reference.sample_dfs_phys(phys, m))

@@ -126,7 +126,7 @@ sk_status sk_solve_grid(sk_plan_t plan, const double* f, double* u, double* X_ha
  * solve above (the reference's truncated theta operators are not mirror-
  * symmetric at j = -M/2).  f: nrhs x (M/2+1) x N real; U: nrhs x M x N
  * complex; X (may be NULL): nrhs x M x N complex solution coefficients.
- * M and N must factor into 2,3,5,7 and fit one CTA (<= ~12000).  Same
+ * M and N: any even sizes the standalone transforms take (below).  Same
  * precondition / error behaviour as sk_solve_coeffs. */
 sk_status sk_solve_grid_exact(sk_plan_t plan, const double* f, double* U, double* X, unsigned flags);
 
@@ -150,8 +150,11 @@ sk_status sk_assemble(sk_plan_t plan, int K, int mf, int nf, const double* d, co
 
 /* Standalone transforms of the reference's Fourier layer on complex data of
  * any even size (the plan supplies device, stream and scratch; its own M, N
- * are not used).  Transform lengths must factor into 2, 3, 5, 7 and fit one
- * CTA (<= ~12000), else SK_ERR_UNSUPPORTED.  Layouts: row-major complex.
+ * are not used).  Lengths that factor into 2, 3, 5, 7 run the mixed-radix
+ * engine (<= ~12000 per CTA); lengths with a larger prime factor (e.g. 602 =
+ * 2 * 7 * 43, acceptance c11) a Bluestein chirp-z convolution of a smooth
+ * length >= 2n - 1 (n <= ~6000); beyond, SK_ERR_UNSUPPORTED.  Layouts:
+ * row-major complex.
  *   sk_analyze_2d   analyze_2d(BMCGrid) (fourier.hpp:107, fourier.cpp:170-188):
  *                   m x n doubled sample grid -> m x n coefficients X.
  *   sk_sample_grid  sample_grid(X, m_out, n_out) (fourier.hpp:108,
@@ -220,7 +223,8 @@ sk_status sk_ipc_close(void* ptr);
  * walk), [13] = kernel variants (bit 0 high-occupancy theta kernel, bit 1
  * high-occupancy lambda kernels, bit 2 swizzled theta slots, bit 3 swizzled
  * lambda slots, bit 4 forward lambda rows on CTA pairs, bit 5 inverse lambda
- * rows on CTA pairs). */
+ * rows on CTA pairs, bit 6 theta_sym_kernel (pruned forward transform, paired
+ * chains), bit 7 forward lambda rows on 4-CTA clusters (peer stores / opt-in)). */
 sk_status sk_plan_info(sk_plan_t plan, long long info[16]);
 
 /* Time one launch of each stage (device events, ms): t[0] lambda_fwd,

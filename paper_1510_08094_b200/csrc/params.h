@@ -72,7 +72,17 @@ struct XformParams {
     double2* dst;
     int swizzle;           // XOR-swizzled shared-memory slots (first FFT span even)
     int hiocc;             // high-occupancy variant (<= 256 threads: 64 registers, radices <= 8)
+    // Bluestein (chirp-z) for lengths with a prime factor > 7 (xform_blue_kernel):
+    // nb = the DFT length (0: plain transform of length fd.L); fd is then the
+    // convolution FFT of length Lb >= 2 nb - 1, chirp[j] = exp(-i pi j^2 / nb),
+    // bhat = FFT_Lb of the direction's chirp kernel / Lb in the engine's
+    // digit-reversed physical slot order
+    int nb;
+    const double2* chirp;
+    const double2* bhat;
 };
+cudaError_t launch_blue_prep(const FftDesc& fd, int nb, const double2* chirp, bool analyze, int nthr, size_t smem,
+                             int swizzle, double2* bhat, cudaStream_t st);
 
 struct ShgenParams {
     GridGeom g;

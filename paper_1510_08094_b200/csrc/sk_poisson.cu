@@ -356,6 +356,13 @@ struct sk_plan_s {
     std::vector<double> host_stats;
     // standalone transforms / assemble: FFT plans per length, growable scratch
     std::map<int, DevFft> xf;
+    struct BlueFft {
+        DevFft f;                   // the convolution FFT, length Lb >= 2n - 1
+        double2* chirp = nullptr;   // exp(-i pi j^2 / n), j < n
+        double2* bhat_a = nullptr;  // FFT(conj chirp kernel) / Lb, forward transforms (analyze)
+        double2* bhat_s = nullptr;  // FFT(chirp kernel) / Lb, backward transforms (synthesize)
+    };
+    std::map<int, BlueFft> xb;  // Bluestein plans of lengths with a prime factor > 7
     static constexpr int kScratch = 8;  // 0-3 assemble / transforms, 4-7 reference-semantics grid solve
     void* scratch[kScratch] = {};
     size_t scratch_bytes[kScratch] = {};
@@ -668,6 +675,12 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
     for (auto& kv : p->xf) free_fft(kv.second);
+    for (auto& kv : p->xb) {
+        free_fft(kv.second.f);
+        cudaFree(kv.second.chirp);
+        cudaFree(kv.second.bhat_a);
+        cudaFree(kv.second.bhat_s);
+    }
     for (void* q : p->scratch)
         if (q) cudaFree(q);
     if (p->pipe_ready) {
@@ -1141,14 +1154,80 @@ sk_status xform_fft(sk_plan_t p, int n, const DevFft** out) {
     return SK_OK;
 }
 
+bool smooth7(long long n) {
+    for (int q : {2, 3, 5, 7})
+        while (n > 1 && n % q == 0) n /= q;
+    return n == 1;
+}
+
+// Bluestein plan for a length n with a prime factor > 7: the smallest
+// 2,3,5,7-smooth Lb >= 2n - 1 whose in-shared-memory FFT fits one CTA, the
+// chirp (long double angles from the exact j^2 mod 2n) and both directions'
+// kernel transforms (xform_blue_prep_kernel).
+sk_status xform_blue(sk_plan_t p, int n, const sk_plan_s::BlueFft** out) {
+    auto it = p->xb.find(n);
+    if (it == p->xb.end()) {
+        sk_plan_s::BlueFft b;
+        int Lb = 2 * n - 1;
+        bool ok = false;
+        for (; Lb <= 4 * n + 64; ++Lb) {
+            if (!smooth7(Lb)) continue;
+            if (build_fft(Lb, xform_threads(Lb), b.f, false, false, 25) != SK_OK) continue;
+            if (sk::xform_smem_bytes(Lb, b.f.d.nhi, b.f.d.nlo) <= 227 * 1024) {
+                ok = true;
+                break;
+            }
+            free_fft(b.f);
+            b.f = DevFft{};
+        }
+        if (!ok)
+            return fail(SK_ERR_UNSUPPORTED, "transform length " + std::to_string(n) +
+                                                ": its Bluestein convolution exceeds one CTA's shared memory");
+        std::vector<double2> ch(n);
+        const long double pi = 3.141592653589793238462643383279502884L;
+        for (int j = 0; j < n; ++j) {
+            const long long e = (static_cast<long long>(j) * j) % (2LL * n);
+            const long double ang = pi * static_cast<long double>(e) / static_cast<long double>(n);
+            ch[j].x = static_cast<double>(cosl(ang));
+            ch[j].y = static_cast<double>(-sinl(ang));
+        }
+        const size_t lp = static_cast<size_t>((Lb + 7) & ~7);
+        CU(cudaMalloc(&b.chirp, sizeof(double2) * n));
+        CU(cudaMalloc(&b.bhat_a, sizeof(double2) * lp));
+        CU(cudaMalloc(&b.bhat_s, sizeof(double2) * lp));
+        CU(cudaMemcpy(b.chirp, ch.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+        const int swz = (b.f.d.nst > 0 && b.f.d.span[0] % 2 == 0) ? 1 : 0;
+        const size_t smem = sk::xform_smem_bytes(Lb, b.f.d.nhi, b.f.d.nlo);
+        CU(sk::launch_blue_prep(b.f.d, n, b.chirp, true, xform_threads(Lb), smem, swz, b.bhat_a, p->stream));
+        CU(sk::launch_blue_prep(b.f.d, n, b.chirp, false, xform_threads(Lb), smem, swz, b.bhat_s, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        it = p->xb.emplace(n, b).first;
+    }
+    *out = &it->second;
+    return SK_OK;
+}
+
 // One pass: nrows sequences of the input (row stride ld_in) -> transform of
-// length n -> transposed store (output stride ld_out).
+// length n -> transposed store (output stride ld_out).  Lengths with a prime
+// factor > 7 go through Bluestein (xform_blue_kernel).
 sk_status xform_pass(sk_plan_t p, bool analyze, int nrows, int n, int n_in, long long ld_in, const double2* src,
                      long long ld_out, double2* dst) {
+    if (!smooth7(n)) {
+        const sk_plan_s::BlueFft* b = nullptr;
+        sk_status s = xform_blue(p, n, &b);
+        if (s != SK_OK) return s;
+        const int Lb = b->f.d.L;
+        sk::XformParams xp{b->f.d, n_in, ld_in, ld_out, src, dst, (b->f.d.nst > 0 && b->f.d.span[0] % 2 == 0) ? 1 : 0,
+                           0, n, b->chirp, analyze ? b->bhat_a : b->bhat_s};
+        CU(sk::launch_xform(xp, analyze, nrows, xform_threads(Lb), sk::xform_smem_bytes(Lb, b->f.d.nhi, b->f.d.nlo),
+                            p->stream));
+        return SK_OK;
+    }
     const DevFft* f = nullptr;
     sk_status s = xform_fft(p, n, &f);
     if (s != SK_OK) return s;
-    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0, 0};
+    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0, 0, 0,
+                       nullptr, nullptr};
     xp.hiocc = xform_threads(n) <= 256 ? 1 : 0;
     for (int st = 0; st < f->d.nst; ++st)
         if (f->d.R[st] > 8) xp.hiocc = 0;  // the variant only instantiates radices <= 8

@@ -69,6 +69,116 @@ __global__ void __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) xform_kernel(Xform
     }
 }
 
+// Bluestein (chirp-z) transforms for lengths n with a prime factor > 7 (the
+// reference accepts any even length through FFTW, fourier.cpp:22-35;
+// acceptance c11 round-trips n = 602 = 2 * 7 * 43):
+//   X_k = sum_j x_j e^{-2 pi i jk/n} = w_k (a * b)_k,  a_j = x_j w_j,
+//   b_m = conj(w_m),  w_m = exp(-i pi m^2 / n)
+// (the backward transform of SYNTH uses the conjugate chirps), with the
+// cyclic convolution of length Lb >= 2n - 1 done by the same in-shared-memory
+// engine: forward DIF, slot-wise product with bhat = FFT(b)/Lb (precomputed
+// in the engine's output slot order by xform_blue_prep_kernel), inverse DIT.
+// One CTA per sequence; loads and transposed stores as xform_kernel.
+template <bool ANALYZE, bool SWZ>
+__global__ void __launch_bounds__(512, 1) xform_blue_kernel(XformParams P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int Lb = P.fd.L, n = P.nb;
+    const int Lp = (Lb + 7) & ~7;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + Lp;
+    double2* s_lo = s_hi + P.fd.nhi;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int r = blockIdx.x;
+    const double2* src = P.src + static_cast<long long>(r) * P.ld_in;
+    const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+    if constexpr (ANALYZE) {
+        for (int j = tid; j < Lp; j += nthr) {
+            double2 v = make_double2(0.0, 0.0);
+            if (j < n) v = cmul(src[j], __ldg(P.chirp + j));
+            if (j < Lb) a[swz<SWZ>(j)] = v;
+        }
+    } else {
+        // synthesize_1d placement g[(k + n) mod n] = (-1)^k c_k, then * conj(w)
+        const int lo = max(-P.n_in / 2, -n / 2), hi = min(P.n_in / 2, n / 2);
+        for (int j = tid; j < Lb; j += nthr) a[swz<SWZ>(j)] = make_double2(0.0, 0.0);
+        __syncthreads();
+        for (int k = lo + tid; k < hi; k += nthr) {
+            const double2 c = src[k + P.n_in / 2];
+            const int t = k < 0 ? k + n : k;
+            const double2 g = (k % 2 == 0) ? c : make_double2(-c.x, -c.y);
+            a[swz<SWZ>(t)] = cmulc(g, __ldg(P.chirp + t));
+        }
+    }
+    __syncthreads();
+    fft_forward<SWZ, 25>(a, P.fd, T, tid, nthr);
+    for (int i = tid; i < Lp; i += nthr) a[i] = cmul(a[i], __ldg(P.bhat + i));
+    __syncthreads();
+    fft_inverse<SWZ, 25>(a, P.fd, T, tid, nthr);
+    if constexpr (ANALYZE) {
+        const double inv = 1.0 / n;
+        for (int kp = tid; kp < n; kp += nthr) {
+            const int k = kp - n / 2;
+            const int t = k < 0 ? k + n : k;
+            const double s = (k % 2 == 0) ? inv : -inv;
+            const double2 v = cmul(a[swz<SWZ>(t)], __ldg(P.chirp + t));
+            P.dst[static_cast<long long>(kp) * P.ld_out + r] = make_double2(s * v.x, s * v.y);
+        }
+    } else {
+        for (int j = tid; j < n; j += nthr)
+            P.dst[static_cast<long long>(j) * P.ld_out + r] = cmulc(a[swz<SWZ>(j)], __ldg(P.chirp + j));
+    }
+}
+
+// bhat = FFT_Lb(b) / Lb in physical slot order: b_m = conj(w_m) (ANALYZE) or
+// w_m (SYNTH) for m in (-n, n), wrapped cyclically.
+template <bool SWZ>
+__global__ void __launch_bounds__(512, 1) xform_blue_prep_kernel(FftDesc fd, int n, const double2* chirp, int analyze,
+                                                                 double2* bhat) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int Lb = fd.L;
+    const int Lp = (Lb + 7) & ~7;
+    double2* a = reinterpret_cast<double2*>(smem_raw);
+    double2* s_hi = a + Lp;
+    double2* s_lo = s_hi + fd.nhi;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const Tw T = load_tw(fd, s_hi, s_lo, tid, nthr);
+    for (int j = tid; j < Lb; j += nthr) {
+        const int m = j < n ? j : (j > Lb - n ? Lb - j : -1);
+        double2 v = make_double2(0.0, 0.0);
+        if (m >= 0) {
+            const double2 w = chirp[m];
+            v = analyze ? make_double2(w.x, -w.y) : w;
+        }
+        a[swz<SWZ>(j)] = v;
+    }
+    __syncthreads();
+    fft_forward<SWZ, 25>(a, fd, T, tid, nthr);
+    const double inv = 1.0 / Lb;
+    for (int i = tid; i < Lp; i += nthr) bhat[i] = (i < Lb || SWZ) ? cscale(a[i], inv) : make_double2(0.0, 0.0);
+}
+
+cudaError_t launch_blue_prep(const FftDesc& fd, int nb, const double2* chirp, bool analyze, int nthr, size_t smem,
+                             int swizzle, double2* bhat, cudaStream_t st) {
+    if (swizzle) {
+        cudaFuncSetAttribute(xform_blue_prep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        xform_blue_prep_kernel<true><<<1, nthr, smem, st>>>(fd, nb, chirp, analyze ? 1 : 0, bhat);
+    } else {
+        cudaFuncSetAttribute(xform_blue_prep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        xform_blue_prep_kernel<false><<<1, nthr, smem, st>>>(fd, nb, chirp, analyze ? 1 : 0, bhat);
+    }
+    return cudaGetLastError();
+}
+
+template <bool ANALYZE, bool SWZ>
+static cudaError_t launch_blue_t(const XformParams& P, int nrows, int nthr, size_t smem, cudaStream_t st) {
+    static std::atomic<unsigned long long> attr{0};
+    configure_on_device(attr, [] {
+        cudaFuncSetAttribute(xform_blue_kernel<ANALYZE, SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    xform_blue_kernel<ANALYZE, SWZ><<<nrows, nthr, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
 // doubled[j][k] = phys[j - m/2][k] (j >= m/2), phys[m/2 - j][(k + n/2) mod n]
 // (j < m/2): the glide reflection f(lambda -+ pi, -theta) of dfs_extend as an
 // index map on the physical rows theta_p = 2 pi p / m, p = 0..m/2.
@@ -100,6 +210,12 @@ static cudaError_t launch_xform_t(const XformParams& P, int nrows, int nthr, siz
 
 cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
     if (nrows <= 0) return cudaSuccess;
+    if (P.nb) {
+        if (analyze) return P.swizzle ? launch_blue_t<true, true>(P, nrows, nthr, smem, st)
+                                      : launch_blue_t<true, false>(P, nrows, nthr, smem, st);
+        return P.swizzle ? launch_blue_t<false, true>(P, nrows, nthr, smem, st)
+                         : launch_blue_t<false, false>(P, nrows, nthr, smem, st);
+    }
     const bool hi = P.hiocc && nthr <= 256;
     if (analyze) {
         if (hi) return P.swizzle ? launch_xform_t<true, true, true>(P, nrows, nthr, smem, st)

@@ -100,6 +100,20 @@ def test_exact_precondition_and_sizes(pkg):
             plan.solve_grid_exact(np.ones((m // 2 + 1, n)))
         with pytest.raises(pkg.size_error):
             plan.solve_grid_exact(np.ones((m // 2, n)))
-    with pkg.Plan(8, 602) as plan:  # 602 = 2 * 7 * 43
-        with pytest.raises(pkg.UnsupportedError):
-            plan.solve_grid_exact(np.zeros((5, 602)))
+    with pkg.Plan(8, 602) as plan:  # 602 = 2 * 7 * 43: Bluestein transforms; zero input -> zero output
+        assert not np.abs(plan.solve_grid_exact(np.zeros((5, 602)))).any()
+
+
+@pytest.mark.parametrize("m,n", [(44, 22), (18, 22), (52, 26), (34, 602)])
+def test_exact_bluestein_sizes_vs_reference(pkg, oracle, reference, m, n):
+    """Lengths with a prime factor > 7 (22 = 2 * 11, 44 = 4 * 11, 26 = 2 * 13,
+    34 = 2 * 17, 602 = 2 * 7 * 43): the reference accepts any even size through
+    FFTW (fourier.cpp:22-35); the device transforms use Bluestein (chirp-z)
+    convolutions of a smooth length.  White noise against the reference's own
+    composition to 1e-10."""
+    f = zero_mean_noise(oracle, m, n, m + 7 * n)
+    X_ref, U_ref, _ = ref_grid(reference, f, m)
+    with pkg.Plan(m, n) as plan:
+        U, X = plan.solve_grid_exact(f, coeffs=True)
+    assert _rel(U, U_ref) <= TOL
+    assert _rel(X, X_ref) <= TOL

@@ -139,8 +139,23 @@ def test_transform_errors(pkg):
         pkg.analyze_2d(np.zeros((6, 5), complex))
     with pytest.raises(pkg.size_error):
         pkg.sample_grid(np.zeros((6, 4), complex), 5, 4)
-    with pytest.raises(pkg.UnsupportedError):
-        pkg.analyze_2d(np.zeros((8, 602), complex))  # 602 = 2 * 7 * 43: prime factor > 7
+
+
+
+@pytest.mark.parametrize("m,n", [(8, 602), (602, 16), (22, 34), (150, 602)])
+def test_transforms_bluestein_vs_reference(pkg, reference, m, n):
+    """Transform lengths with a prime factor > 7 (602 = 2 * 7 * 43, 22, 34) run
+    Bluestein convolutions on the device: analyze_2d and sample_grid (equal,
+    padded and truncated sizes) against the reference itself, and the round
+    trip of acceptance c11 (acceptance_main.cpp:242-257) to 1e-13."""
+    rng = np.random.default_rng(m * n)
+    g = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    X = pkg.analyze_2d(g)
+    Xr = reference.analyze_2d(g)
+    assert _rel(X, Xr) <= 1e-13
+    for mo, no in [(m, n), (m + 4, n + 2), (max(2, m - 4), max(2, n - 2))]:
+        assert _rel(pkg.sample_grid(Xr, mo, no), reference.sample_grid(Xr, mo, no)) <= 1e-13
+    assert _rel(pkg.sample_grid(X, m, n), g) <= 1e-13
 
 
 # ------------------------------------------------------------- DFS doubling

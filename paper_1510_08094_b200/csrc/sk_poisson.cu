@@ -320,7 +320,8 @@ struct sk_plan_s {
     double* hu = nullptr;
     double* rbuf = nullptr;    // residual output (4)
     double2* coef_stage = nullptr;  // shgen coefficients
-    double* pivots = nullptr;  // theta-stage pivot table, cols x 2 x M/2
+    double* pivots = nullptr;  // theta-stage pivot table, rows (k - piv_k0, parity) for modes [piv_k0, piv_k0 + piv_n)
+    int piv_k0 = 0, piv_n = 0;
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
     int piv_stride = 0;        // doubles per pivot-table row
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
@@ -373,6 +374,33 @@ namespace {
 sk_status ensure(void** p, size_t bytes) {
     if (*p) return SK_OK;
     CU(cudaMalloc(p, bytes));
+    return SK_OK;
+}
+
+// Half spectrum of single-GPU grid solves (nrhs x (N/2+1) x (M/2+1) complex).
+sk_status ensure_spec(sk_plan_t p) {
+    return ensure(reinterpret_cast<void**>(&p->spec), sizeof(double2) * p->nrhs * p->g.rows * p->g.cols);
+}
+
+// Pivot rows of the modes [k0, k0 + n): built by the plan's pivot kernel on
+// first use (a slab rank asks for its own modes only), rebuilt if a later
+// call needs modes outside the cached range.
+sk_status ensure_pivots(sk_plan_t p, int k0, int n) {
+    if (p->pivots && k0 >= p->piv_k0 && k0 + n <= p->piv_k0 + p->piv_n) return SK_OK;
+    if (p->pivots) {
+        CU(cudaStreamSynchronize(p->stream));
+        CU(cudaFree(p->pivots));
+        p->pivots = nullptr;
+    }
+    const size_t np = static_cast<size_t>(n) * 2 * p->piv_stride;
+    sk_status s = ensure(reinterpret_cast<void**>(&p->pivots), sizeof(double) * (np ? np : 2));
+    if (s != SK_OK) return s;
+    p->piv_k0 = k0;
+    p->piv_n = n;
+    if (n > 0) {
+        CU(p->theta_sym ? sk::launch_pivot_table_sym(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream)
+                        : sk::launch_pivot_table(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream));
+    }
     return SK_OK;
 }
 
@@ -588,11 +616,9 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
         }
     }
     if (p->grid_ok) {
-        const size_t n = static_cast<size_t>(nrhs) * p->g.rows * p->g.cols;
-        if ((s = ensure(reinterpret_cast<void**>(&p->spec), sizeof(double2) * n)) != SK_OK) {
-            sk_plan_destroy(p);
-            return s;
-        }
+        // the half spectrum (single-GPU solves) and the pivot table are
+        // allocated on first use (ensure_spec / ensure_pivots): a slab rank
+        // never holds the whole spectrum, only its own modes' pivots
         // data-independent Thomas pivots of every (lambda mode, parity) chain
         p->piv_stride = p->g.Lt + (p->g.Lt & 1);
         // chain solver: fixed short segments up to 6 elements per thread, the
@@ -642,18 +668,6 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
                 sk_plan_destroy(p);
                 return fail(SK_ERR_CUDA, "copy of the chain slot table failed");
             }
-        }
-        const size_t np = static_cast<size_t>(p->g.cols) * 2 * p->piv_stride;
-        if ((s = ensure(reinterpret_cast<void**>(&p->pivots), sizeof(double) * np)) != SK_OK) {
-            sk_plan_destroy(p);
-            return s;
-        }
-        const cudaError_t pe = p->theta_sym
-                                   ? sk::launch_pivot_table_sym(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream)
-                                   : sk::launch_pivot_table(p->g.Lt, 0, p->g.cols, p->pivots, p->piv_stride, p->stream);
-        if (pe != cudaSuccess || cudaStreamSynchronize(p->stream) != cudaSuccess) {
-            sk_plan_destroy(p);
-            return fail(SK_ERR_CUDA, "pivot table construction failed");
         }
     }
     *out = p;
@@ -897,7 +911,11 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.hiocc = p->theta_hiocc ? 1 : 0;
         tp.rev_win = p->theta_q ? 0 : p->rev_win;
         tp.swizzle = p->ft.d.nst > 0 && (p->ft.d.span[0] % 2 == 0) ? 1 : 0;
-        tp.pivots = p->pivots + static_cast<size_t>(k0) * 2 * p->piv_stride;  // rows for this rank's modes
+        {
+            const sk_status ps = ensure_pivots(p, k0, ncols_local);
+            if (ps != SK_OK) return ps;
+        }
+        tp.pivots = p->pivots + static_cast<size_t>(k0 - p->piv_k0) * 2 * p->piv_stride;  // rows for this rank's modes
         tp.sym_pos = p->sym_pos;
         tp.piv_stride = p->piv_stride;
         if (peers) tp.peers = *peers;
@@ -985,6 +1003,7 @@ sk_status sk_solve_grid(sk_plan_t p, const double* f, double* u, double* X_half,
     if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
     if (!f || !u) return fail(SK_ERR_ARGUMENT, "null f or u");
     const size_t ng = static_cast<size_t>(p->nrhs) * p->g.rows * p->N;
+    if ((s = ensure_spec(p)) != SK_OK) return s;
     if (!(flags & SK_DEVICE) && (flags & SK_ASYNC)) {
         if (X_half) return fail(SK_ERR_ARGUMENT, "X_half is not available with asynchronous host-memory solves");
         if ((s = pipe_init(p, ng)) != SK_OK) return s;
@@ -1075,6 +1094,7 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     if (!p->grid_ok) return fail(SK_ERR_UNSUPPORTED, p->grid_why);
     if (!coeffs_dev || !phys_dev || L < 0) return fail(SK_ERR_ARGUMENT, "bad shgen arguments");
     if (L >= p->N / 2) return fail(SK_ERR_ARGUMENT, "degree L must be below N/2");
+    if ((s = ensure_spec(p)) != SK_OK) return s;
     sk::ShgenParams sp{p->g, L, coeffs_dev, p->spec, p->g.rows};
     CU(sk::launch_shgen(sp, p->stream));
     sk::LambdaParams lp{};

@@ -214,6 +214,22 @@ sk_status sk_ipc_handle(const void* ptr, unsigned char handle[64]);
 sk_status sk_ipc_open(int device, const unsigned char handle[64], void** ptr);
 sk_status sk_ipc_close(void* ptr);
 
+/* Stream-ordered hand-over between ranks of the fused slab solve without
+ * draining a stream: interprocess events (cudaEventInterprocess) recorded
+ * on a plan's stream behind a stage, opened by the peers from their 64-byte
+ * handles, and waited on by the peers' streams before the stage that reads
+ * what it wrote (the host only orders the record before the wait).  No
+ * kernel ever spins on another rank. */
+sk_status sk_ipc_event_create(int device, unsigned char handle[64], void** event);
+sk_status sk_ipc_event_open(int device, const unsigned char handle[64], void** event);
+sk_status sk_event_destroy(void* event);
+sk_status sk_event_record(sk_plan_t plan, void* event);
+sk_status sk_stream_wait_event(sk_plan_t plan, void* event);
+/* Mean / max|F| statistics of the plan's last theta stage entry point
+ * (out[0..1] the surface mean of the k = 0 owner, out[2] max|F| of its modes),
+ * waiting only for that stage's copy to the host. */
+sk_status sk_stage_stats(sk_plan_t plan, double out[3]);
+
 /* Plan facts: info[0] = M, [1] = N, [2] = nrhs, [3] = device,
  * [4] = grid path supported (1/0), [5] = spectrum leading dimension,
  * [6] = theta-stage split (CTAs per column), [7] = theta-stage threads,

@@ -32,7 +32,8 @@ EXPORTS = [
     "sk_plan_info", "sk_stage_times", "sk_enable_stage_timing", "sk_last_error", "sk_version",
     "sk_stage_lambda_fwd_peer", "sk_stage_theta_peer", "sk_device_alloc", "sk_device_free", "sk_ipc_handle",
     "sk_ipc_open", "sk_ipc_close", "sk_assemble", "sk_analyze_2d", "sk_sample_grid", "sk_sample_dfs",
-    "sk_solve_grid_exact",
+    "sk_solve_grid_exact", "sk_ipc_event_create", "sk_ipc_event_open", "sk_event_destroy", "sk_event_record",
+    "sk_stream_wait_event", "sk_stage_stats",
 ]
 
 
@@ -113,6 +114,12 @@ def load() -> ctypes.CDLL:
         "sk_sample_grid": (I, [P, I, I, P, I, I, P, U]),
         "sk_sample_dfs": (I, [P, I, I, P, P, U]),
         "sk_solve_grid_exact": (I, [P, P, P, P, U]),
+        "sk_ipc_event_create": (I, [I, ctypes.c_char_p, ctypes.POINTER(P)]),
+        "sk_ipc_event_open": (I, [I, ctypes.c_char_p, ctypes.POINTER(P)]),
+        "sk_event_destroy": (I, [P]),
+        "sk_event_record": (I, [P, P]),
+        "sk_stream_wait_event": (I, [P, P]),
+        "sk_stage_stats": (I, [P, D]),
         "sk_last_error": (ctypes.c_char_p, []),
         "sk_version": (ctypes.c_char_p, []),
     }

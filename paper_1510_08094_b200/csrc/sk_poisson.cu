@@ -322,6 +322,10 @@ struct sk_plan_s {
     double2* coef_stage = nullptr;  // shgen coefficients
     double* pivots = nullptr;  // theta-stage pivot table, rows (k - piv_k0, parity) for modes [piv_k0, piv_k0 + piv_n)
     int piv_k0 = 0, piv_n = 0;
+    // theta-stage statistics of the stage entry points, copied to pinned host
+    // memory behind the stage (sk_stage_stats waits for this event only)
+    double* stage_stats_h = nullptr;
+    cudaEvent_t ev_stats = nullptr;
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
     int piv_stride = 0;        // doubles per pivot-table row
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
@@ -711,6 +715,8 @@ sk_status sk_plan_destroy(sk_plan_t p) {
         cudaStreamDestroy(p->pipe_h2d);
         cudaStreamDestroy(p->pipe_d2h);
     }
+    if (p->stage_stats_h) cudaFreeHost(p->stage_stats_h);
+    if (p->ev_stats) cudaEventDestroy(p->ev_stats);
     if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return SK_OK;
@@ -1419,6 +1425,19 @@ sk_status sk_solve_grid_exact(sk_plan_t p, const double* f, double* U, double* X
     return check_precondition(p, p->nrhs);
 }
 
+// Queue the copy of the theta stage's statistics to pinned host memory and
+// mark it with an event, so that a rank can check the precondition without
+// draining its stream (sk_stage_stats).
+static sk_status stage_stats_async(sk_plan_t p) {
+    if (!p->stage_stats_h) {
+        CU(cudaMallocHost(&p->stage_stats_h, sizeof(double) * 4));
+        CU(cudaEventCreateWithFlags(&p->ev_stats, cudaEventDisableTiming));
+    }
+    CU(cudaMemcpyAsync(p->stage_stats_h, p->stats, sizeof(double) * 4, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaEventRecord(p->ev_stats, p->stream));
+    return SK_OK;
+}
+
 static sk_status make_slabs(sk_plan_t p, int P, const int* rb, const int* cb, int rank, sk::Slabs& sl) {
     if (P < 1 || P > sk::kMaxRanks || rank < 0 || rank >= P || !rb || !cb)
         return fail(SK_ERR_ARGUMENT, "bad slab description");
@@ -1458,7 +1477,10 @@ sk_status sk_stage_theta(sk_plan_t p, int P, const int* rb, const int* cb, int r
     CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4, p->stream));
     if (ncols == 0) return SK_OK;
     p->last_launches = 0;
-    return run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2);
+    if ((s = run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2)) !=
+        SK_OK)
+        return s;
+    return stage_stats_async(p);
 }
 
 sk_status sk_stage_lambda_inv(sk_plan_t p, int P, const int* rb, const int* cb, int rank, const double* back_dev,
@@ -1509,7 +1531,7 @@ sk_status sk_stage_theta_peer(sk_plan_t p, int P, const int* rb, const int* cb, 
     if (!peer_back) return fail(SK_ERR_ARGUMENT, "null peer buffer table");
     const int ncols = cb[rank + 1] - cb[rank];
     CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4, p->stream));
-    if (ncols == 0) return SK_OK;
+    if (ncols == 0) return stage_stats_async(p);
     sk::PeerMap pm{};
     pm.n = P;
     for (int r = 0; r < P; ++r) {
@@ -1521,8 +1543,10 @@ sk_status sk_stage_theta_peer(sk_plan_t p, int P, const int* rb, const int* cb, 
     }
     pm.bound[P] = rb[P];
     p->last_launches = 0;
-    return run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2,
-                    &pm);
+    if ((s = run_grid(p, sl, 0, ncols, cb[rank], nullptr, reinterpret_cast<double2*>(recv_dev), nullptr, nullptr, 2,
+                      &pm)) != SK_OK)
+        return s;
+    return stage_stats_async(p);
 }
 
 sk_status sk_device_alloc(int device, size_t bytes, void** ptr) {
@@ -1559,6 +1583,58 @@ sk_status sk_ipc_open(int device, const unsigned char handle[64], void** ptr) {
 
 sk_status sk_ipc_close(void* ptr) {
     if (ptr) CU(cudaIpcCloseMemHandle(ptr));
+    return SK_OK;
+}
+
+sk_status sk_stage_stats(sk_plan_t p, double out[3]) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!out) return fail(SK_ERR_ARGUMENT, "null output");
+    if (!p->stage_stats_h) return fail(SK_ERR_ARGUMENT, "no theta stage has run on this plan");
+    CU(cudaEventSynchronize(p->ev_stats));
+    for (int i = 0; i < 3; ++i) out[i] = p->stage_stats_h[i];
+    return SK_OK;
+}
+
+sk_status sk_ipc_event_create(int device, unsigned char handle[64], void** event) {
+    if (!handle || !event) return fail(SK_ERR_ARGUMENT, "null argument");
+    CU(cudaSetDevice(device));
+    cudaEvent_t e = nullptr;
+    CU(cudaEventCreateWithFlags(&e, cudaEventInterprocess | cudaEventDisableTiming));
+    cudaIpcEventHandle_t h;
+    CU(cudaIpcGetEventHandle(&h, e));
+    std::memcpy(handle, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+    *event = e;
+    return SK_OK;
+}
+
+sk_status sk_ipc_event_open(int device, const unsigned char handle[64], void** event) {
+    if (!handle || !event) return fail(SK_ERR_ARGUMENT, "null argument");
+    CU(cudaSetDevice(device));
+    cudaIpcEventHandle_t h;
+    std::memcpy(&h, handle, sizeof(h) < 64 ? sizeof(h) : 64);
+    cudaEvent_t e = nullptr;
+    CU(cudaIpcOpenEventHandle(&e, h));
+    *event = e;
+    return SK_OK;
+}
+
+sk_status sk_event_destroy(void* event) {
+    if (event) CU(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+    return SK_OK;
+}
+
+sk_status sk_event_record(sk_plan_t p, void* event) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    CU(cudaEventRecord(static_cast<cudaEvent_t>(event), p->stream));
+    return SK_OK;
+}
+
+sk_status sk_stream_wait_event(sk_plan_t p, void* event) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    CU(cudaStreamWaitEvent(p->stream, static_cast<cudaEvent_t>(event), 0));
     return SK_OK;
 }
 

@@ -22,8 +22,13 @@ Two transports (``SlabSolver(transport=...)``):
   lambda kernel then stores mode k of its rows straight into the receive
   buffer of the rank owning k, and the theta kernel stores row p of its
   solved columns straight into the return buffer of the rank owning p (NVLink
-  stores over NVSwitch); a barrier between stages is the only
-  synchronisation, no collective moves data.
+  stores over NVSwitch); no collective moves data.  The hand-over between
+  stages is stream-ordered: each rank records an interprocess CUDA event
+  behind each stage, and a peer's stream waits on it before the stage that
+  reads what it wrote (``PeerEvents``); the host only orders every record
+  before the matching waits with a barrier that runs while the stage itself
+  is still on the GPU, so no stream drains between stages and no kernel ever
+  waits on another rank.
 * ``"nccl"``: the two exchanges as ``all_to_all_single`` over NCCL — the
   comparison baseline.
 
@@ -61,9 +66,9 @@ class CudaStages:
     def stats(self):
         """(mean re, mean im, max|F|) of this rank's last theta stage: the
         k = 0 owner contributes the surface mean 2 pi w^T f~_0, every rank the
-        max |F| of its modes (poisson.cpp:101-117)."""
-        mean, fmax = self.plan.last_mean()
-        return mean.real, mean.imag, fmax
+        max |F| of its modes (poisson.cpp:101-117).  Waits for that stage only
+        (sk_stage_stats), not for what is queued behind it."""
+        return self.plan.stage_stats()
 
 
 class PeerBuffers:
@@ -106,6 +111,41 @@ class PeerBuffers:
             self.own = 0
 
 
+class PeerEvents:
+    """An interprocess CUDA event per rank (sk_ipc_event_create), opened by
+    every other rank: ``evs[d]`` is rank d's event in this process."""
+
+    def __init__(self, device_index: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+        self._lib = _lib.load()
+        own = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        _lib.check(self._lib.sk_ipc_event_create(device_index, h, ctypes.byref(own)))
+        self.own = int(own.value)
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        me = dist.get_rank(group)
+        self.evs, self._opened = [], []
+        for d, hd in enumerate(handles):
+            if d == me:
+                self.evs.append(self.own)
+                continue
+            e = ctypes.c_void_p()
+            _lib.check(self._lib.sk_ipc_event_open(device_index, ctypes.create_string_buffer(hd, 64), ctypes.byref(e)))
+            self.evs.append(int(e.value))
+            self._opened.append(int(e.value))
+
+    def close(self):
+        import ctypes
+        for e in self._opened + ([self.own] if self.own else []):
+            self._lib.sk_event_destroy(ctypes.c_void_p(e))
+        self._opened, self.own = [], 0
+
+
 class SlabSolver:
     """One rank of the P-way slab-decomposed grid solve.
 
@@ -145,6 +185,12 @@ class SlabSolver:
             self.recv_pb = PeerBuffers(8 * sum(self.recv_split), dev, group)
             self.back_pb = PeerBuffers(8 * sum(self.send_split), dev, group)
             self.recv, self.back = self.recv_pb.own, self.back_pb.own
+            # one event per stage and rank: forward lambda done (its stores into
+            # the peers' receive buffers landed), theta done (return buffers),
+            # inverse lambda done (this rank's return buffer free again)
+            self.ev_fwd = PeerEvents(dev, group)
+            self.ev_theta = PeerEvents(dev, group)
+            self.ev_inv = PeerEvents(dev, group)
         elif transport == "nccl":
             self.send = torch.empty(sum(self.send_split), **kw)
             self.recv = torch.empty(sum(self.recv_split), **kw)
@@ -159,14 +205,23 @@ class SlabSolver:
         P, rb, cb, r = self.P, self.rb, self.cb, self.rank
         if self.transport == "p2p":
             plan = self.backend.plan
+            peers = [d for d in range(P) if d != r]
             plan.stage_lambda_fwd_peer(P, rb, cb, r, f_rows, self.recv_pb.ptrs)
-            self._stage_barrier(plan)
+            plan.event_record(self.ev_fwd.own)
+            self._host_barrier()  # every rank's record is queued before any wait below
+            for d in peers:
+                plan.stream_wait(self.ev_fwd.evs[d])  # their stores into our receive buffer
+                plan.stream_wait(self.ev_inv.evs[d])  # they have read their return buffers (last solve)
             plan.stage_theta_peer(P, rb, cb, r, self.recv, self.back_pb.ptrs)
-            plan.sync()
-            # the all-reduce of the precondition statistics is also the stage
-            # barrier: every rank's theta stores have landed once it returns
-            self.check_precondition()
+            plan.event_record(self.ev_theta.own)
+            self._host_barrier()
+            for d in peers:
+                plan.stream_wait(self.ev_theta.evs[d])  # their stores into our return buffer
             plan.stage_lambda_inv(P, rb, cb, r, self.back, u_rows)
+            plan.event_record(self.ev_inv.own)
+            # the statistics of this rank's theta stage (the inverse stage is
+            # already queued behind it); raised on every rank together
+            self.check_precondition()
             return u_rows
         self.backend.lambda_fwd(P, rb, cb, r, f_rows, self.send)
         dist.all_to_all_single(self.recv, self.send, self.recv_split, self.send_split, group=self.group)
@@ -178,17 +233,19 @@ class SlabSolver:
         self.check_precondition()
         return u_rows
 
-    def _stage_barrier(self, plan):
-        """Every rank's stores into its peers' buffers are complete (the
-        stage's kernel finished) before any rank reads them."""
-        plan.sync()
+    def _host_barrier(self):
+        """Orders every rank's event records before the peers' waits (host
+        side only: the stages keep running on the GPUs meanwhile)."""
         self.dist.barrier(group=self.group)
 
     def close(self):
         if self.transport == "p2p":
+            self.backend.plan.sync()
             self.dist.barrier(group=self.group)  # no peer still reads our buffers
             self.recv_pb.close()
             self.back_pb.close()
+            for ev in (self.ev_fwd, self.ev_theta, self.ev_inv):
+                ev.close()
 
     def check_precondition(self):
         """All-reduce of the mean / max|F| statistics of the last theta stage

@@ -259,6 +259,21 @@ class Plan:
         tab = (ctypes.c_void_p * P)(*[_ptr(b) for b in peer_back])
         _lib.check(self.lib.sk_stage_theta_peer(self._h, P, rb, cb, rank, _ptr(recv), tab))
 
+    def event_record(self, event: int) -> None:
+        """Record an (interprocess) event on the plan's stream (sk_event_record)."""
+        _lib.check(self.lib.sk_event_record(self._h, ctypes.c_void_p(event)))
+
+    def stream_wait(self, event: int) -> None:
+        """Make the plan's stream wait for an event (sk_stream_wait_event)."""
+        _lib.check(self.lib.sk_stream_wait_event(self._h, ctypes.c_void_p(event)))
+
+    def stage_stats(self):
+        """(mean re, mean im, max|F|) of the last theta stage entry point,
+        waiting for that stage only (sk_stage_stats)."""
+        out = (ctypes.c_double * 3)()
+        _lib.check(self.lib.sk_stage_stats(self._h, out))
+        return out[0], out[1], out[2]
+
     def stage_lambda_inv(self, P, row_b, col_b, rank, back, u_rows):
         rb, cb = self._bounds(P, row_b, col_b)
         self._follow_torch(back)

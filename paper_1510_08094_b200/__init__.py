@@ -7,6 +7,7 @@ reference's spherekit Poisson interface (poisson.hpp) on top of it.
 from .poisson import (  # noqa: F401
     AssembleReport, BenchRow, DeviceError, LowRankSphereFun, Plan, PoissonProblem, PoissonSolution, ResidualReport,
     UnsupportedError, analyze_2d, assemble_poisson, bench_poisson, integration_weights, precondition_error, residual,
-    sample_dfs, sample_grid, size_error, solve, solve_grid, structure_error)
+    sample_dfs, sample_grid, size_error, solve, solve_grid, solve_grid_exact, structure_error, coefficients_from_half,
+    rhs_coefficients)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -40,7 +40,7 @@ __all__ = [
     "Plan", "PoissonProblem", "PoissonSolution", "ResidualReport", "BenchRow", "solve", "residual", "solve_grid",
     "bench_poisson", "integration_weights", "size_error", "precondition_error", "structure_error", "DeviceError",
     "UnsupportedError", "LowRankSphereFun", "AssembleReport", "assemble_poisson", "analyze_2d", "sample_grid",
-    "sample_dfs", "solve_grid_exact",
+    "sample_dfs", "solve_grid_exact", "coefficients_from_half", "rhs_coefficients",
 ]
 
 
@@ -437,6 +437,39 @@ def solve_grid_exact(f_phys: np.ndarray, m: Optional[int] = None, coeffs: bool =
     m = 2 * (rows - 1) if m is None else m
     _check_sizes(m, n)
     return _plan(m, n).solve_grid_exact(f_phys, coeffs=coeffs)
+
+
+def coefficients_from_half(X_half, m: int, n: int) -> np.ndarray:
+    """The full m x n coefficient matrix of the real grid solve from its
+    k >= 0 half X_half[k][i] (sk_solve_grid): the k < 0 columns are the
+    Hermitian mirror X(t, -k) = conj X(-t, k) (the unpaired t = -m/2 row maps
+    to itself), k = -n/2 is the Nyquist column X_half[n/2]."""
+    Xh = np.asarray(X_half)
+    L = m // 2
+    t = np.arange(m) - L
+    tt = np.where(t == -L, -L, -t) + L
+    X = np.empty((m, n), np.complex128)
+    X[:, n // 2:] = Xh[: n // 2].T
+    X[:, 0] = Xh[n // 2]
+    for kc in range(1, n // 2):
+        X[:, kc] = np.conj(Xh[n // 2 - kc][tt])
+    return X
+
+
+def rhs_coefficients(f_phys, m: Optional[int] = None) -> np.ndarray:
+    """F = Msin^2 analyze_2d(sample_dfs(f)) of physical samples: the
+    PoissonProblem the grid solve answers; the transforms run on
+    the device, the Msin^2 column apply in the reference's accumulation order
+    (banded.cpp:8-19)."""
+    rows, n = f_phys.shape[-2:]
+    m = 2 * (rows - 1) if m is None else m
+    A = analyze_2d(sample_dfs(np.ascontiguousarray(f_phys, np.float64), m))
+    d = np.full((m, 1), 0.5)
+    d[0] = d[-1] = 0.25
+    F = d * A
+    F[2:] = -0.25 * A[:-2] + F[2:]   # acc = (-1/4) x_{i-2}, then + diag x_i
+    F[:-2] = F[:-2] + (-0.25) * A[2:]  # then + (-1/4) x_{i+2}
+    return F
 
 
 def integration_weights(m: int) -> np.ndarray:

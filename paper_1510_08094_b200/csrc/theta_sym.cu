@@ -48,6 +48,19 @@ namespace cg = cooperative_groups;
 
 namespace sk {
 
+#ifdef SK_PHASES
+extern __device__ unsigned long long g_phase[4096][24];  // grid_kernels.cu (-rdc debug build, tools/build_phases.sh)
+#define SK_PROBE_S(i)                                                       \
+    do {                                                                    \
+        __syncthreads();                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_phase[blockIdx.x][i] = clock64(); \
+    } while (0)
+#else
+#define SK_PROBE_S(i) \
+    do {              \
+    } while (0)
+#endif
+
 namespace {
 
 // Sizes of the chains of parity class par (theta_common make_chains, L even):
@@ -176,6 +189,7 @@ __device__ __noinline__ void solve_chains_sym(double2* a, const uint32_t* __rest
         ip_before = ip[s - 1];
     }
     if (s + S < n) xhi = rd(s + S);
+    SK_PROBE_S(12);
     const int ulast = n - 1 - s;  // index of chain+'s last element in this segment (if 0 <= ulast < S)
     const double tl = static_cast<double>(L - 1);
     // ---- pass 1: F = Msin^2 X (d2 = 1/4 only on the truncation row t = L-1)
@@ -207,7 +221,9 @@ __device__ __noinline__ void solve_chains_sym(double2* a, const uint32_t* __rest
         }
         *fmax_hi = max(*fmax_hi, fh);
     }
+    SK_PROBE_S(13);
     const Aff3 rin = block_scan_aff1<false>(aff, wsc);  // also orders every X read above before the writes below
+    SK_PROBE_S(14);
     // ---- pass 2
     Aff3 baff;
     double2 rlast = make_double2(0.0, 0.0);
@@ -284,7 +300,9 @@ __device__ __noinline__ void solve_chains_sym(double2* a, const uint32_t* __rest
         misc[5] = make_double2(xm_last.x - sgn * xp_last.x, xm_last.y - sgn * xp_last.y);  // Delta
         misc[6] = xm_extra;
     }
+    SK_PROBE_S(15);
     const Aff3 xin = block_scan_aff1<true>(baff, wsc + 16);  // publishes Delta (misc) as well
+    SK_PROBE_S(16);
     const double2 Dl = misc[5];
     // ---- pass 3
     double2 x = make_double2(xin.b, xin.c);
@@ -333,11 +351,14 @@ __device__ __noinline__ void solve_chains_sym(double2* a, const uint32_t* __rest
         misc[4] = xf_m;  // x-_0 (t = -2 or -1)
     }
     __syncthreads();
+    SK_PROBE_S(17);
 }
 
+// Odd segment lengths: a warp's per-element loads of the pivot (8 B) and
+// slot (4 B) windows then stride an odd number of words, conflict-free.
 __device__ __forceinline__ int sym_segment(int n, int nthr) {
     const int need = (n + nthr - 1) / nthr;
-    return need <= 4 ? 4 : need <= 6 ? 6 : need <= 8 ? 8 : need <= 10 ? 10 : need <= 12 ? 12 : 0;
+    return need <= 5 ? 5 : need <= 7 ? 7 : need <= 9 ? 9 : need <= 11 ? 11 : need <= 13 ? 13 : 0;
 }
 
 }  // namespace
@@ -407,6 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     const size_t prow = (static_cast<size_t>(kl) * 2 + par) * P.piv_stride;
 
     // ---- bulk copies: raw column (L+1), this (mode, parity)'s pivots, the chain slot window
+    SK_PROBE_S(0);
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -440,6 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
         if (tid == 0) a[0] = make_double2(-a[0].x, -a[0].y);
         __syncthreads();
     }
+    SK_PROBE_S(1);
 
     // ---- fused fold + first DIF stage (butterfly pairs), then the computed sub-transforms
     const double invM = 1.0 / P.g.M;
@@ -448,8 +471,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     __syncthreads();
     const double2 c0 = misc[7];
     const double2 cofs = make_double2((1.0 - sgn) * c0.x, (1.0 - sgn) * c0.y);
+    SK_PROBE_S(2);
     const int kcnt = R0 / 2 + 1 - par;
     fft_forward_sub<25>(a, P.fd, T, tid, nthr, kcnt);
+    SK_PROBE_S(3);
     mbar_wait(&bars[1], 0);  // pivot and chain slot windows
 
     const SymRead rd{a, pw, par == 0 ? 1 : 0, par, R0, sgn, cofs};
@@ -503,16 +528,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     double2 wsum = make_double2(0.0, 0.0);
     const bool want_wsum = (kg == 0 && par == 0);
     Aff3* wsc3 = reinterpret_cast<Aff3*>(wsc);
+    SK_PROBE_S(4);
 #define SK_SYM(S) \
     solve_chains_sym<S>(a, pw, ip, wsc3, misc, par, L, R0, sgn, k2, inner, cofs, &fmax_hi, &wsum, want_wsum)
     switch (sym_segment(nplus(par, L), nthr)) {
-        case 4: SK_SYM(4); break;
-        case 6: SK_SYM(6); break;
-        case 8: SK_SYM(8); break;
-        case 10: SK_SYM(10); break;
-        default: SK_SYM(12); break;  // the plan guarantees n+ <= 12 nthr
+        case 5: SK_SYM(5); break;
+        case 7: SK_SYM(7); break;
+        case 9: SK_SYM(9); break;
+        case 11: SK_SYM(11); break;
+        default: SK_SYM(13); break;  // the plan guarantees n+ <= 12 nthr
     }
 #undef SK_SYM
+    SK_PROBE_S(5);
     if (want_wsum) wsum = block_sum2(wsum, red);
     if (par == 0 && tid == 0) {
         double2 x0;
@@ -541,7 +568,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     }
     __syncthreads();
 
+    SK_PROBE_S(6);
     fft_inverse<false, 25>(a, P.fd, T, tid, nthr);
+    SK_PROBE_S(7);
 
     // ---- recombine the parity classes: v_p = Ve_p + w_M^p Vo_p, p = 0..M/2
     cluster.sync();
@@ -555,7 +584,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
         if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
         else colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
     }
+    SK_PROBE_S(8);
     cluster_exit_barrier(relaxed_exit);  // only consumed DSMEM loads since the last cluster barrier
+    SK_PROBE_S(9);
 }
 
 cudaError_t launch_pivot_table_sym(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st) {

@@ -55,6 +55,14 @@ def _ptr(a) -> Optional[int]:
     return int(a.data_ptr())  # torch.Tensor
 
 
+def _pinned_like(a: np.ndarray) -> np.ndarray:
+    """A page-locked host array shaped like `a` (torch's pinned allocator; the
+    numpy view keeps the tensor alive)."""
+    import torch
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    return t.numpy()
+
+
 def _is_device(a) -> bool:
     return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
 
@@ -181,14 +189,17 @@ class Plan:
         else:
             f = np.ascontiguousarray(f, dtype=np.float64)
             if u is None:
-                u = np.empty_like(f)
+                # asynchronous host solves copy into u on a side stream: a pageable
+                # destination would make that copy synchronous, so allocate pinned
+                u = _pinned_like(f) if not sync else np.empty_like(f)
             if coeffs:
                 Xh = np.empty((self.nrhs, self.N // 2 + 1, self.M), np.complex128)
         self._follow_torch(f)
         flags = (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (0 if sync else _lib.SK_ASYNC)
         if not sync and not dev:
-            # pipelined host solve: the arrays must outlive the queued copies
-            self._inflight = (getattr(self, "_inflight", []) + [(f, u)])[-4:]
+            # pipelined host solve: every (f, u) pair must outlive its queued
+            # copies, i.e. stay referenced until sync() (the C contract)
+            self._inflight = getattr(self, "_inflight", []) + [(f, u)]
         _lib.check(self.lib.sk_solve_grid(self._h, _ptr(f), _ptr(u), _ptr(Xh), flags))
         if coeffs:
             if self.nrhs == 1:

@@ -26,15 +26,20 @@ n = min(4096, 2 * (cfg.N // 2 + 1))
 a = a[:n]
 names = ["bars+issue+twiddles+TMA wait", "fold", "fft fwd", "mean+inner+chain+ solve", "pivot- TMA wait",
          "chain- solve", "x0/fmax/export", "fft inv", "cluster sync+combine+stores", "final cluster sync", ""]
-d = np.diff(a[:, :11], axis=1)
-tot = (a[:, 10] - a[:, 0])
+if plan.info()["variants"] & 64:  # theta_sym_kernel's probes
+    names = ["loads (column TMA wait)", "fold + paired stage 0", "restricted fwd stages", "window wait+mean+inner",
+             "both chains", "x0/fmax/export", "fft inv", "cluster sync+combine+stores", "final cluster sync", "", ""]
+last = 9 if plan.info()["variants"] & 64 else 10
+d = np.diff(a[:, :last + 1], axis=1)
+tot = (a[:, last] - a[:, 0])
 print(f"{cfg.name}: CTAs sampled {n}, mean cycles per CTA {tot.mean():.0f}")
-for i in range(10):
+for i in range(last):
     print(f"  {names[i]:28s} {d[:, i].mean():9.0f} cyc  {100 * d[:, i].mean() / tot.mean():5.1f}%")
 
 sub = a[:, 12:18]
 if (sub > 0).all():
     sn = ["loads+sync", "pass1 (F, fwd map)", "scan1", "pass2 (sweep, bwd map)", "scan2", "pass3 (back subst)"]
-    dd = np.diff(np.concatenate([a[:, 3:4], sub], axis=1), axis=1)
+    base = a[:, 4:5] if plan.info()["variants"] & 64 else a[:, 3:4]
+    dd = np.diff(np.concatenate([base, sub], axis=1), axis=1)
     for i, nm in enumerate(sn):
         print(f"    chain+ {nm:18s} {dd[:, i].mean():8.0f} cyc")

@@ -23,6 +23,7 @@ UNITS = [
     ("grid_kernels.cu", []),
     ("grid_large.cu", []),
     ("theta_sym.cu", []),
+    ("theta_mp.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("assemble_kernels.cu", ["--fmad=false"]),
     ("transforms.cu", []),

@@ -117,6 +117,18 @@ struct ThetaLargeParams {
     int use_cmap;    // fold inputs through the column tensor map (single rank: contiguous columns)
     int fold_chunk;  // r per TMA stage of the fold (256 or 512, sized to the pivot window)
 };
+// Multi-pass theta stage (theta_mp.cu): the theta length L = L1 L2 through five
+// coalesced passes; w1 / w2 hold 2 L complex per column (both parities).
+struct ThetaMpParams {
+    ThetaParams t;
+    FftDesc f1;   // length L1, 16 threads per sequence
+    FftDesc f2;   // length L2, 16 threads per sequence
+    double2* w1;
+    double2* w2;
+};
+size_t theta_mp_smem_bytes(int which, int L1, int L2, int nhi1, int nlo1, int nhi2, int nlo2, int nhiM, int nloM);
+int theta_mp_chain_cap();
+cudaError_t launch_theta_mp(const ThetaMpParams& Q, cudaStream_t st);
 struct LambdaSplitParams {
     LambdaParams l;
     FftDesc fh;

@@ -343,6 +343,11 @@ struct sk_plan_s {
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
     bool theta_sym = false;    // theta_sym_kernel (theta_sym.cu): pruned forward transform, both chains at once
+    bool theta_mp = false;     // multi-pass theta stage (theta_mp.cu) for columns longer than one CTA
+    DevFft fm1, fm2;           // its length-L1 / length-L2 transforms (16 threads per sequence)
+    double2* mp_w1 = nullptr;  // its intermediates, 2 L complex per column each
+    double2* mp_w2 = nullptr;
+    size_t mp_cols = 0;        // columns the intermediates hold
     uint32_t* sym_pos = nullptr;  // its per-parity chain slot table (2 x theta_sym_pos_slots(M/2))
     // pipelined host-memory solves (SK_HOST | SK_ASYNC)
     static constexpr int kPipe = 3;  // device slots: H2D(i+1), solve(i), D2H(i-1) all in flight
@@ -402,8 +407,8 @@ sk_status ensure_pivots(sk_plan_t p, int k0, int n) {
     p->piv_k0 = k0;
     p->piv_n = n;
     if (n > 0) {
-        CU(p->theta_sym ? sk::launch_pivot_table_sym(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream)
-                        : sk::launch_pivot_table(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream));
+        CU((p->theta_sym || p->theta_mp) ? sk::launch_pivot_table_sym(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream)
+                                         : sk::launch_pivot_table(p->g.Lt, k0, n, p->pivots, p->piv_stride, p->stream));
     }
     return SK_OK;
 }
@@ -567,7 +572,42 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
             p->rev_win = 1;
         }
         const bool fits = p->smem_theta <= cap && (Lt / 2 + 1) <= 12 * p->thr_theta;
-        if (!fits) {
+        const bool want_mp = !std::getenv("SK_THETA_MP") || std::atoi(std::getenv("SK_THETA_MP")) != 0;
+        if (!fits && want_mp && p->kseq == 0 && Lt % 2 == 0 && Lt / 2 <= sk::theta_mp_chain_cap()) {
+            // multi-pass theta stage: L = L1 L2 with L1 % 16 == 0, L2 % 32 == 0,
+            // both <= 384 (a CTA's 16 sequences in shared memory), L1 <= L2 closest
+            int best1 = 0;
+            const bool wide = std::getenv("SK_MP_WIDE") && std::atoi(std::getenv("SK_MP_WIDE")) != 0;  // A/B: L1 >= L2
+            for (int l1 = 16; l1 <= 256; l1 *= 2) {  // powers of two (the passes index by shifts)
+                if (Lt % l1) continue;
+                const int l2 = Lt / l1;
+                if (l2 % 32 || l2 > 384 || (l2 & (l2 - 1))) continue;
+                if (!wide && l1 > l2) continue;
+                if (wide && l1 < l2) continue;
+                if (!wide || !best1) best1 = l1;  // narrow: the most balanced (last); wide: the first with L1 >= L2
+            }
+            if (best1) {
+                const int l1 = best1, l2 = Lt / best1;
+                if (build_fft(l1, 16, p->fm1, false, false, 8) == SK_OK &&
+                    build_fft(l2, 16, p->fm2, false, false, 8) == SK_OK) {
+                    p->theta_mp = true;
+                    p->thr_theta = 512;
+                    p->smem_theta = std::max({sk::theta_mp_smem_bytes(0, l1, l2, p->fm1.d.nhi, p->fm1.d.nlo, p->fm2.d.nhi,
+                                                                      p->fm2.d.nlo, p->ft.d.nhi, p->ft.d.nlo),
+                                              sk::theta_mp_smem_bytes(2, l1, l2, p->fm1.d.nhi, p->fm1.d.nlo, p->fm2.d.nhi,
+                                                                      p->fm2.d.nlo, p->ft.d.nhi, p->ft.d.nlo),
+                                              sk::theta_mp_smem_bytes(3, l1, l2, 0, 0, 0, 0, 0, 0)});
+                    if (p->smem_theta > cap) p->theta_mp = false;
+                }
+                if (!p->theta_mp) {
+                    free_fft(p->fm1);
+                    free_fft(p->fm2);
+                    p->fm1 = DevFft{};
+                    p->fm2 = DevFft{};
+                }
+            }
+        }
+        if (!fits && !p->theta_mp) {
             const int Q = 4;
             const int Lq = Lt / Q;
             p->theta_q = Q;
@@ -643,6 +683,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
                            pow2 && p->ft.d.span[0] % 2 == 1 && p->ft.d.nst >= 2 && Lt2 / 2 <= 12 * p->thr_theta &&
                            sk::theta_sym_smem_bytes(Lt2, p->ft.d.nhi, p->ft.d.nlo) <= cap;
         }
+        if (p->theta_mp) p->piv_stride = sk::theta_sym_piv_slots(p->g.Lt);  // pivot_table_sym_kernel rows
         if (p->theta_sym) {
             const int Lt2 = p->g.Lt;
             p->piv_stride = sk::theta_sym_piv_slots(Lt2);
@@ -685,6 +726,10 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     free_fft(p->fl);
     free_fft(p->ftq);
     free_fft(p->flh);
+    free_fft(p->fm1);
+    free_fft(p->fm2);
+    if (p->mp_w1) cudaFree(p->mp_w1);
+    if (p->mp_w2) cudaFree(p->mp_w2);
     for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
                     static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
                     static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
@@ -794,6 +839,7 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda && (p->N / 2 / 256 + 1) % 2 == 0)
         info[13] |= 32;  // inverse lambda rows on CTA pairs (lambda_inv_pair_ok)
     if (p->theta_sym) info[13] |= 64;  // theta_sym_kernel
+    if (p->theta_mp) info[13] |= 256;  // multi-pass theta stage (theta_mp.cu)
     if (p->grid_ok && p->lambda_quad != 0 && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda)
         info[13] |= 128;  // forward lambda rows on 4-CTA clusters: peer stores (default) or any (SK_LAMBDA_QUAD=1)
@@ -926,7 +972,22 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.piv_stride = p->piv_stride;
         if (peers) tp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[2], p->stream));
-        if (p->theta_q) {
+        if (p->theta_mp) {
+            const size_t cols = static_cast<size_t>(ncols_local) * tp.nrhs;
+            if (cols > p->mp_cols) {
+                if (p->mp_w1) {
+                    CU(cudaStreamSynchronize(p->stream));
+                    CU(cudaFree(p->mp_w1));
+                    CU(cudaFree(p->mp_w2));
+                    p->mp_w1 = p->mp_w2 = nullptr;
+                }
+                CU(cudaMalloc(&p->mp_w1, sizeof(double2) * 2 * p->g.Lt * cols));
+                CU(cudaMalloc(&p->mp_w2, sizeof(double2) * 2 * p->g.Lt * cols));
+                p->mp_cols = cols;
+            }
+            sk::ThetaMpParams mq{tp, p->fm1.d, p->fm2.d, p->mp_w1, p->mp_w2};
+            CU(sk::launch_theta_mp(mq, p->stream));
+        } else if (p->theta_q) {
             sk::ThetaLargeParams tl{tp, p->ftq.d, 0, 0};
             CUtensorMap cmap{};
             {

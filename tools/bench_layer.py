@@ -120,6 +120,30 @@ def main():
     by = 8.0 * (m // 2 + 1) * n + 16.0 * m * n
     out.append({"op": "sample_dfs", "m": m, "n": n, "ms": best, "ms_median": med, "achieved_gbs": by / best / 1e6,
                 "peak_gbs": pk, "frac": by / best / 1e6 / pk})
+    # Bluestein transforms (prime factor > 7): 602 = 2 * 7 * 43 and 4 * 1031
+    for m, n in [(602, 602), (4124, 1024)]:
+        grid = crand(m, n)
+        X = torch.empty_like(grid)
+        best, med = timed(xp, lambda: xp.analyze_2d(grid, X))
+        by = 2 * 32.0 * m * n
+        rec = {"op": "analyze_2d (Bluestein)", "m": m, "n": n, "ms": best, "ms_median": med,
+               "achieved_gbs": by / best / 1e6, "peak_gbs": pk, "frac": by / best / 1e6 / pk}
+        if R is not None and m * n <= 1 << 22:
+            gn = grid.cpu().numpy()
+            rec["cpu_reference_ms"] = 1e3 * cpu_time(lambda: R.analyze_2d(gn))
+        out.append(rec)
+    # the reference-semantics grid solve (composition of the device stages)
+    for M, N in [(4096, 2048), (2048, 1024)]:
+        plan = Plan(M, N)
+        rows = M // 2 + 1
+        from paper_1510_08094_b200 import inputs
+        f = torch.empty((rows, N), dtype=torch.float64, device=dev)
+        plan.shgen(64, torch.from_numpy(inputs.sh_coeffs(3, 64, 2.0)).cuda(), f)
+        best, med = timed(plan, lambda: plan.solve_grid_exact(f))
+        rec = {"op": "solve_grid_exact", "M": M, "N": N, "ms": best, "ms_median": med,
+               "dof_per_s": M * N / 2 / (best * 1e-3)}
+        out.append(rec)
+        plan.close()
     for r in out:
         print(json.dumps(r))
 

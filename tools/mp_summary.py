@@ -10,4 +10,4 @@ for r in rows:
 for k, v in out.items():
     t = float(v['gpu__time_duration.sum']) / 1e6
     rb = float(v['dram__bytes_read.sum']) / 1e9; wb = float(v['dram__bytes_write.sum']) / 1e9
-    print(f"{k:28s} {t:7.2f} ms  R {rb:6.2f} GB W {wb:6.2f} GB  {(rb + wb) / t:6.0f} GB/s  warps {float(v['sm__warps_active.avg.pct_of_peak_sustained_active']):5.1f}%  occ-lim reg {v.get('launch__occupancy_limit_registers')} smem {v.get('launch__occupancy_limit_shared_mem')}")
+    print(f"{k:28s} {t:7.2f} ms  R {rb:6.2f} GB W {wb:6.2f} GB  {(rb + wb) / (t * 1e-3):6.0f} GB/s  warps {float(v['sm__warps_active.avg.pct_of_peak_sustained_active']):5.1f}%  occ-lim reg {v.get('launch__occupancy_limit_registers')} smem {v.get('launch__occupancy_limit_shared_mem')}")

@@ -81,11 +81,13 @@ __device__ __forceinline__ double2 half_root(int q) {
 }
 
 // Fused fold + first DIF stage over butterfly pairs (j, S0 - j).
-template <int R0>
-__device__ __forceinline__ void fold_stage0(double2* a, int L, int par, double sgn, double invM, const Tw& T, int tid,
+// (par is a template parameter: the mirror index km below must be a compile-time
+// register index, a runtime one puts x[] in local memory)
+template <int R0, int par>
+__device__ __forceinline__ void fold_stage0(double2* a, int L, double sgn, double invM, const Tw& T, int tid,
                                             int nthr, double2* c0_out) {
     const int S0 = L / R0;
-    const int kcnt = R0 / 2 + 1 - par;
+    constexpr int kcnt = R0 / 2 + 1 - par;
     for (int j = tid; 2 * j <= S0; j += nthr) {  // j = 0 .. (S0-1)/2 (S0 odd)
         double2 x[R0];
 #pragma unroll
@@ -150,9 +152,8 @@ struct SymRead {
         const uint32_t pk = pw[i];
         const int d0 = (tau0 + i) & (R0 - 1);
         const bool direct = par == 0 ? d0 <= R0 / 2 : d0 < R0 / 2;
-        if (direct) return a[pk & 0xffffu];
-        const double2 v = a[pk >> 16];
-        return make_double2(fma(sgn, v.x, cofs.x), fma(sgn, v.y, cofs.y));
+        const double2 v = a[direct ? (pk & 0xffffu) : (pk >> 16)];  // one load either way
+        return direct ? v : make_double2(fma(sgn, v.x, cofs.x), fma(sgn, v.y, cofs.y));
     }
 };
 
@@ -162,8 +163,10 @@ struct SymRead {
 // to 1 so that the scan's product is Phi); the owner of the last element
 // computes Delta from the boundary rows; scan; pass 3: x+ = g + c x+ and
 // x- = s x+ + Phi Delta into both chains' slots.
+// (inlined: as a called function it saved and restored ~100 callee-saved
+// registers per thread around the body, 200 KB of local-memory traffic per CTA)
 template <int S>
-__device__ __noinline__ void solve_chains_sym(double2* a, const uint32_t* __restrict__ pw, const double* ip, Aff3* wsc,
+__device__ __forceinline__ void solve_chains_sym(double2* a, const uint32_t* __restrict__ pw, const double* ip, Aff3* wsc,
                                               double2* misc, int par, int L, int R0, double sgn, double k2,
                                               double2 inner, double2 cofs, unsigned* fmax_hi, double2* wsum,
                                               bool want_wsum) {
@@ -467,7 +470,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     // ---- fused fold + first DIF stage (butterfly pairs), then the computed sub-transforms
     const double invM = 1.0 / P.g.M;
     if (tid == 0) misc[7] = make_double2(0.0, 0.0);
-    fold_stage0<R0>(a, L, par, sgn, invM, T, tid, nthr, &misc[7]);
+    if (par == 0) fold_stage0<R0, 0>(a, L, sgn, invM, T, tid, nthr, &misc[7]);
+    else fold_stage0<R0, 1>(a, L, sgn, invM, T, tid, nthr, &misc[7]);
     __syncthreads();
     const double2 c0 = misc[7];
     const double2 cofs = make_double2((1.0 - sgn) * c0.x, (1.0 - sgn) * c0.y);
@@ -578,11 +582,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
     const double2* vo = par == 1 ? a : cluster.map_shared_rank(a, 1);
     const int p_lo = par == 0 ? 0 : half;
     const int p_hi = par == 0 ? half : L + 1;
-    for (int p = p_lo + tid; p < p_hi; p += nthr) {
-        const int pm = (p == L) ? 0 : p;
-        const double2 v = cadd(ve[pm], cmulc(vo[pm], T(p)));
-        if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
-        else colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
+    // four rows per thread and trip: the (remote) loads of all four issue
+    // before the first is used
+    constexpr int kU = 4;
+    for (int p0 = p_lo + tid; p0 < p_hi; p0 += kU * nthr) {
+        double2 e[kU], o[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int p = min(p0 + u * nthr, p_hi - 1);
+            const int pm = (p == L) ? 0 : p;
+            e[u] = ve[pm];
+            o[u] = vo[pm];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int p = p0 + u * nthr;
+            if (p < p_hi) {
+                const double2 v = cadd(e[u], cmulc(o[u], T(p)));
+                if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
+                else colbase[theta_addr(P.sl, P.ncols, kl, p)] = v;
+            }
+        }
     }
     SK_PROBE_S(8);
     cluster_exit_barrier(relaxed_exit);  // only consumed DSMEM loads since the last cluster barrier

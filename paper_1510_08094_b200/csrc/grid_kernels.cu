@@ -182,9 +182,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
     const int k_lo = c == 0 ? 0 : nk / 2;
     const int k_hi = c == 0 ? nk / 2 : nk;
     const int sub_hi = min(2, P.rows_local - r0);  // 1 when the padding CTA is the partner
-    for (int i = tid; i < 2 * (k_hi - k_lo); i += nthr) {
-        const int k = k_lo + (i >> 1), sub = i & 1;
-        if (sub < sub_hi) P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = (sub == c) ? a[k] : other[k];
+    // four (mode, row) entries per thread and trip, their (half remote) loads
+    // issued together through one generic pointer: the DSMEM latency is paid
+    // once per four stores
+    constexpr int kU = 4;
+    const int tot = 2 * (k_hi - k_lo);
+    for (int i0 = tid; i0 < tot; i0 += kU * nthr) {
+        double2 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = min(i0 + u * nthr, tot - 1);
+            const double2* src = ((i & 1) == c) ? a : other;
+            v[u] = src[k_lo + (i >> 1)];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * nthr;
+            const int k = k_lo + (i >> 1), sub = i & 1;
+            if (i < tot && sub < sub_hi) P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = v[u];
+        }
     }
     cluster_exit_barrier(relaxed_exit);
 }

@@ -159,7 +159,7 @@ struct SymRead {
 
 // Both chains of parity `par`, S chain+ elements per thread (S * nthr >= n+).
 // Pass 1: X -> F = Msin^2 X, forward affine summary; scan; pass 2: r' and
-// g = r'/d' (g to chain+'s slot), backward summary (the last multiplier set
+// g = r'/d' (kept in F's registers), backward summary (the last multiplier set
 // to 1 so that the scan's product is Phi); the owner of the last element
 // computes Delta from the boundary rows; scan; pass 3: x+ = g + c x+ and
 // x- = s x+ + Phi Delta into both chains' slots.
@@ -251,7 +251,7 @@ __device__ __forceinline__ void solve_chains_sym(double2* a, const uint32_t* __r
             if (!ok) c = 1.0;
             G = make_double2(fma(Pm, g.x, G.x), fma(Pm, g.y, G.y));
             Pm *= c;
-            if (ok) a[pw[s + u] & 0xffffu] = g;
+            v[u] = g;  // F is dead: g stays in its registers for pass 3
             ipv[u] = c;
             ipp = iv;
             t += 2.0;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void solve_chains_sym(double2* a, const uint32_t* __r
     for (int u = S - 1; u >= 0; --u) {
         if (s + u < n) {
             const uint32_t pk = pw[s + u];
-            const double2 g = a[pk & 0xffffu];
+            const double2 g = v[u];
             const double c = ipv[u];
             if (u != ulast) {
                 x = make_double2(fma(c, x.x, g.x), fma(c, x.y, g.y));

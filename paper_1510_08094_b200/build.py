@@ -24,6 +24,7 @@ UNITS = [
     ("grid_large.cu", []),
     ("theta_sym.cu", []),
     ("theta_mp.cu", []),
+    ("lambda_duo.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("assemble_kernels.cu", ["--fmad=false"]),
     ("transforms.cu", []),

@@ -186,6 +186,11 @@ inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
     return lpad * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>((L + 3) & ~3) * 4 + 32;
 }
 cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
+// lambda stages on row pairs inside one CTA (lambda_duo.cu); nthr = threads per row
+size_t lambda_duo_smem_bytes(int L, int nhi, int nlo);
+bool lambda_duo_ok(const LambdaParams& P, int nthr);
+cudaError_t launch_lambda_fwd_duo(const LambdaParams& P, int nthr, cudaStream_t st);
+cudaError_t launch_lambda_inv_duo(const LambdaParams& P, const CUtensorMap& map, int nthr, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
 cudaError_t launch_assemble(const AssembleParams& P, cudaStream_t st);
 size_t xform_smem_bytes(int n, int nhi, int nlo);

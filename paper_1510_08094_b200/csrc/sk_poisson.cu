@@ -339,6 +339,8 @@ struct sk_plan_s {
     // inverse lambda rows on CTA pairs (32-byte gathers): opt-in, SK_LAMBDA_PAIR_INV=1. Measured slower at C3
     // (0.80 vs 0.57 ms: the peer's modes are 16-byte DSMEM reads at a 32-byte stride)
     bool lambda_pair_inv = false;
+    bool lambda_duo = false;   // opt-in A/B (SK_LAMBDA_DUO=1): both lambda stages on row pairs inside one CTA
+                               // (lambda_duo.cu); measured slower at C3 than two independent CTAs per SM
     int regsolve = 1;          // chain solver request (SK_REGSOLVE): 1 auto, 0 shared-memory walk, 2 SMAX=12 registers, 3 fixed short segments
     int chain_mode = 1;        // the theta kernel's chain solver (ThetaParams::regsolve)
     int rev_win = 0;           // theta kernel stages the chains' digit-reversal windows (ThetaParams::rev_win)
@@ -634,6 +636,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     if (const char* e = std::getenv("SK_LAMBDA_PAIR")) p->lambda_pair = std::atoi(e) != 0;  // A/B
     if (const char* e = std::getenv("SK_LAMBDA_QUAD")) p->lambda_quad = std::atoi(e) != 0 ? 1 : 0;  // A/B
     if (const char* e = std::getenv("SK_LAMBDA_PAIR_INV")) p->lambda_pair_inv = std::atoi(e) != 0;  // opt-in A/B
+    if (const char* e = std::getenv("SK_LAMBDA_DUO")) p->lambda_duo = std::atoi(e) != 0;  // A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
@@ -838,6 +841,10 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
     if (p->grid_ok && p->lambda_pair_inv && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda && (p->N / 2 / 256 + 1) % 2 == 0)
         info[13] |= 32;  // inverse lambda rows on CTA pairs (lambda_inv_pair_ok)
+    if (p->grid_ok && p->lambda_duo && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 && p->thr_lambda <= 256 &&
+        p->N / 4 + 1 <= 12 * p->thr_lambda &&
+        sk::lambda_duo_smem_bytes(p->g.Ll, p->fl.d.nhi, p->fl.d.nlo) <= 227 * 1024)
+        info[13] |= 512;  // lambda stages on row pairs inside one CTA (lambda_duo_ok; the forward one for local stores)
     if (p->theta_sym) info[13] |= 64;  // theta_sym_kernel
     if (p->theta_mp) info[13] |= 256;  // multi-pass theta stage (theta_mp.cu)
     if (p->grid_ok && p->lambda_quad != 0 && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
@@ -934,6 +941,8 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         if (p->lambda_split) {
             sk::LambdaSplitParams sp{lp, p->flh.d};
             CU(sk::launch_lambda_fwd_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+        } else if (p->lambda_duo && !peers && sk::lambda_duo_ok(lp, p->thr_lambda)) {
+            CU(sk::launch_lambda_fwd_duo(lp, p->thr_lambda, p->stream));
         } else {
             CUtensorMap map;
             sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
@@ -1026,6 +1035,11 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         if (p->lambda_split) {
             sk::LambdaSplitParams sp{lp, p->flh.d};
             CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+        } else if (p->lambda_duo && sk::lambda_duo_ok(lp, p->thr_lambda)) {
+            CUtensorMap map;
+            sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs, 2);
+            if (ms != SK_OK) return ms;
+            CU(sk::launch_lambda_inv_duo(lp, map, p->thr_lambda, p->stream));
         } else {
             CUtensorMap map;
             if (p->lambda_pair_inv) lp.pair |= 2;

@@ -353,8 +353,8 @@ __device__ __forceinline__ void solve_chains_sym(double2* a, const uint32_t* __r
         misc[3] = xf_p;  // x+_0 (t = 2 or 1)
         misc[4] = xf_m;  // x-_0 (t = -2 or -1)
     }
-    __syncthreads();
-    SK_PROBE_S(17);
+    // no trailing barrier: the caller publishes its per-warp max|F|^2 first and
+    // then synchronises once for both
 }
 
 // Odd segment lengths: a warp's per-element loads of the pivot (8 B) and
@@ -543,22 +543,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
         default: SK_SYM(13); break;  // the plan guarantees n+ <= 12 nthr
     }
 #undef SK_SYM
+    // per-warp max|F|^2 (high words), one barrier for them and the chain's
+    // results, then thread 0 alone finishes: CTA maximum -> stats, x_0 -> slot 0
+    unsigned* redu = reinterpret_cast<unsigned*>(red + 48);
+    {
+        const unsigned wm = __reduce_max_sync(0xffffffffu, fmax_hi);
+        if ((tid & 31) == 0) redu[tid >> 5] = wm;
+    }
+    __syncthreads();
+    SK_PROBE_S(17);
     SK_PROBE_S(5);
     if (want_wsum) wsum = block_sum2(wsum, red);
-    if (par == 0 && tid == 0) {
-        double2 x0;
-        if (kg != 0) {
-            // row j = 0: 1/2 x_{-2} - k^2 x_0 + 1/2 x_2 = F_0
-            const double2 xp2 = misc[3], xm2 = misc[4];
-            x0 = make_double2((F0.x - 0.5 * xm2.x - 0.5 * xp2.x) / (-k2), (F0.y - 0.5 * xm2.y - 0.5 * xp2.y) / (-k2));
-        } else {
-            // constraint row 2 pi w^T X_0 = 0 replaces row j = 0 (w_0 = 2)
-            x0 = make_double2(-0.5 * wsum.x, -0.5 * wsum.y);
+    if (tid == 0) {
+        unsigned m = 0u;
+        for (int w = 0; w < (nthr >> 5); ++w) m = max(m, redu[w]);
+        atomic_max_nonneg(st + 2, sqrt(__hiloint2double(static_cast<int>(m), 0)));
+        if (par == 0) {
+            double2 x0;
+            if (kg != 0) {
+                // row j = 0: 1/2 x_{-2} - k^2 x_0 + 1/2 x_2 = F_0
+                const double2 xp2 = misc[3], xm2 = misc[4];
+                x0 = make_double2((F0.x - 0.5 * xm2.x - 0.5 * xp2.x) / (-k2), (F0.y - 0.5 * xm2.y - 0.5 * xp2.y) / (-k2));
+            } else {
+                // constraint row 2 pi w^T X_0 = 0 replaces row j = 0 (w_0 = 2)
+                x0 = make_double2(-0.5 * wsum.x, -0.5 * wsum.y);
+            }
+            a[0] = x0;
         }
-        a[0] = x0;
     }
-    const double fm = sqrt(block_max(__hiloint2double(static_cast<int>(fmax_hi), 0), red));
-    if (tid == 0) atomic_max_nonneg(st + 2, fm);
     __syncthreads();
 
     // optional: export the solution coefficients of this parity class
@@ -569,8 +581,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) theta_sym_ke
             const int t = t_of(tau, par, L);
             xo[t + L] = a[__ldg(P.fd.rev + tau)];
         }
+        __syncthreads();
     }
-    __syncthreads();
 
     SK_PROBE_S(6);
     fft_inverse<false, 25>(a, P.fd, T, tid, nthr);

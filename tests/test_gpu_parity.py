@@ -408,6 +408,29 @@ def test_lambda_inv_row_pairs_bitwise(pkg, oracle, reference, m, n, paired, monk
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n", [(64, 3000), (54, 3000), (40, 2400), (50, 3000), (128, 10000)])
+def test_lambda_duo_bitwise(pkg, oracle, reference, m, n, monkeypatch):
+    """The opt-in lambda stages on row pairs inside one CTA (SK_LAMBDA_DUO=1,
+    lambda_duo.cu: local 32-byte (p, p+1) stores, 2-row TMA boxes in the
+    inverse; measured slower at C3 than two independent CTAs per SM, so not
+    the default): bit-identical to the one-row-per-CTA kernels for odd (33,
+    21) and even (28, 26) row counts and at C3's row length, and against the
+    reference on rough zero-mean data."""
+    f = zero_mean_noise(oracle, m, n, m * n + 2)
+    monkeypatch.setenv("SK_LAMBDA_DUO", "1")
+    with pkg.Plan(m, n) as plan:
+        assert plan.info()["variants"] & 512, plan.info()
+        u = plan.solve_grid(f)
+    monkeypatch.setenv("SK_LAMBDA_DUO", "0")
+    monkeypatch.setenv("SK_LAMBDA_PAIR", "0")
+    with pkg.Plan(m, n) as plan:
+        assert not plan.info()["variants"] & (512 | 16)
+        u1 = plan.solve_grid(f)
+    assert np.array_equal(u, u1)
+    _, _, u_ref = ref_grid(reference, f, m)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
 def test_bench_multi_rank_launcher():
     """bench.py --gpus 2 without a launcher re-runs itself under
     torch.distributed.run with 2 ranks (on a one-GPU box both share GPU 0:

@@ -622,7 +622,7 @@ def main():
             # the FP64 pipe and shared memory near 30 % at 16 warps/SM (latency)
             roof["theta_profile"] = {"fp64_pipe_frac": prof["theta_fp64_pipe"],
                                      "warps_per_sm": prof.get("theta_warps_per_sm"),
-                                     "note": "latency-bound; ncu --set full, profiles/r1_phases_and_ab.md"}
+                                     "note": "latency-bound; ncu --set full, profiles/r2_theta_sym_c3.md"}
     line = {
         "metric": "sphere Poisson DOF/s (FP64)", "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -50,6 +50,13 @@ constexpr int kLgT = 4;    // log2 kBlkT
 constexpr int kSeg = 8;    // chain elements per thread in TC (registers: no spills)
 constexpr int kCq = 8;     // CTAs per TC cluster (portable maximum)
 constexpr int kCthr = 256; // threads per TC CTA
+// A CTA's sequences sit L + kPad slots apart in shared memory: the tile loads
+// and stores of every pass walk the SEQUENCE index fastest (8 or 16
+// neighbouring lanes, the contiguous direction in HBM), and with a stride of
+// L slots (a multiple of 128 bytes) those lanes all hit one bank group (ncu:
+// shared-memory pipe 80-92 % busy, short-scoreboard stalls on top); one slot
+// of padding rotates consecutive sequences through the eight bank groups.
+constexpr int kPad = 1;
 
 // raw column element p of column c (rhs-major) in the (slab) spectrum layout
 __device__ __forceinline__ double2* raw_ptr(const ThetaParams& P, int c, int p) {
@@ -78,8 +85,9 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_a_kernel(ThetaMpParams Q) {
     const ThetaParams& P = Q.t;
     const int L = P.fd.L, L1 = Q.f1.L, L2 = Q.f2.L;
     const int nb = L1 / kBlkR;
-    double2* a = reinterpret_cast<double2*>(smem_raw);  // 32 sequences of L2 (par * 16 + q)
-    double2* t2hi = a + kSeqs * L2;
+    const int S2 = L2 + kPad;
+    double2* a = reinterpret_cast<double2*>(smem_raw);  // 16 sequences of L2 (par * 8 + q), S2 slots apart
+    double2* t2hi = a + kSeqs * S2;
     double2* t2lo = t2hi + Q.f2.nhi;
     double2* tmhi = t2lo + Q.f2.nlo;  // 2L-th roots (the theta plan's table)
     double2* tmlo = tmhi + P.fd.nhi;
@@ -106,17 +114,17 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_a_kernel(ThetaMpParams Q) {
         if (r == 0 && P.g.pole_glide) ar = cscale(ar, sgn);  // sk_internal.h GridGeom::pole_glide
         const double2 ev = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
         const double2 od = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), TM(r)), invM);
-        a[q * L2 + swz<true>(r2)] = ev;
-        a[(kBlkR + q) * L2 + swz<true>(r2)] = od;
+        a[q * S2 + swz<true>(r2)] = ev;
+        a[(kBlkR + q) * S2 + swz<true>(r2)] = od;
     }
     __syncthreads();
     const int seq = tid / kGrp, g = tid - seq * kGrp;
-    fft_forward<true, 8>(a + seq * L2, Q.f2, T2, g, kGrp);  // t2 at slot swz(rev2[t2])
+    fft_forward<true, 8>(a + seq * S2, Q.f2, T2, g, kGrp);  // t2 at slot swz(rev2[t2])
     // twiddle w_L^(r1 t2) = T(2 r1 t2) and the store of (par, t2, r1)
     for (int e = tid; e < 2 * kBlkR * L2; e += nthr) {
         const int q = e & (kBlkR - 1), t2 = (e >> kLgR) & (L2 - 1), par = e >> (kLgR + lg2);
         const int r1 = kBlkR * b + q;
-        const double2 v = a[(par * kBlkR + q) * L2 + swz<true>(rev2[t2])];
+        const double2 v = a[(par * kBlkR + q) * S2 + swz<true>(rev2[t2])];
         const int m = 2 * r1 * t2;  // < 2 L1 L2 = 2L: no reduction
         Q.w1[((static_cast<size_t>(c) * 2 + par) * L2 + t2) * L1 + r1] = cmul(v, TM(m));
     }
@@ -128,8 +136,9 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_b_kernel(ThetaMpParams Q) {
     const ThetaParams& P = Q.t;
     const int L = P.fd.L, L1 = Q.f1.L, L2 = Q.f2.L;
     const int nb = L2 / kBlkT;
-    double2* a = reinterpret_cast<double2*>(smem_raw);  // 32 sequences of L1
-    double2* t1hi = a + kSeqs * L1;
+    const int S1 = L1 + kPad;
+    double2* a = reinterpret_cast<double2*>(smem_raw);  // 16 sequences of L1, S1 slots apart
+    double2* t1hi = a + kSeqs * S1;
     double2* t1lo = t1hi + Q.f1.nhi;
     int* rev1 = reinterpret_cast<int*>(t1lo + Q.f1.nlo);
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -141,15 +150,15 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_b_kernel(ThetaMpParams Q) {
 #pragma unroll 4
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int r1 = e & (L1 - 1), q = e >> lg1;
-        a[q * L1 + swz<true>(r1)] = src[static_cast<size_t>(kBlkT * b + q) * L1 + r1];
+        a[q * S1 + swz<true>(r1)] = src[static_cast<size_t>(kBlkT * b + q) * L1 + r1];
     }
     __syncthreads();
     const int seq = tid / kGrp, g = tid - seq * kGrp;
-    fft_forward<true, 8>(a + seq * L1, Q.f1, T1, g, kGrp);
+    fft_forward<true, 8>(a + seq * S1, Q.f1, T1, g, kGrp);
     double2* dst = Q.w2 + static_cast<size_t>(cp) * L;
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int q = e & (kBlkT - 1), t1 = e >> kLgT;
-        dst[static_cast<size_t>(t1) * L2 + kBlkT * b + q] = a[q * L1 + swz<true>(rev1[t1])];
+        dst[static_cast<size_t>(t1) * L2 + kBlkT * b + q] = a[q * S1 + swz<true>(rev1[t1])];
     }
 }
 
@@ -493,8 +502,9 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_d_kernel(ThetaMpParams Q) {
     const ThetaParams& P = Q.t;
     const int L = P.fd.L, L1 = Q.f1.L, L2 = Q.f2.L;
     const int nb = L2 / kBlkT;
+    const int S1 = L1 + kPad;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* t1hi = a + kSeqs * L1;
+    double2* t1hi = a + kSeqs * S1;
     double2* t1lo = t1hi + Q.f1.nhi;
     double2* tmhi = t1lo + Q.f1.nlo;
     double2* tmlo = tmhi + P.fd.nhi;
@@ -509,17 +519,17 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_d_kernel(ThetaMpParams Q) {
 #pragma unroll 4
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int q = e & (kBlkT - 1), t1 = e >> kLgT;
-        a[q * L1 + swz<true>(rev1[t1])] = src[static_cast<size_t>(t1) * L2 + kBlkT * b + q];  // DIT input order
+        a[q * S1 + swz<true>(rev1[t1])] = src[static_cast<size_t>(t1) * L2 + kBlkT * b + q];  // DIT input order
     }
     __syncthreads();
     const int seq = tid / kGrp, g = tid - seq * kGrp;
-    fft_inverse<true, 8>(a + seq * L1, Q.f1, T1, g, kGrp);  // natural p1
+    fft_inverse<true, 8>(a + seq * S1, Q.f1, T1, g, kGrp);  // natural p1
     double2* dst = Q.w1 + static_cast<size_t>(cp) * L1 * L2;
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int q = e & (kBlkT - 1), p1 = e >> kLgT;
         const int t2 = kBlkT * b + q;
         const int m = 2 * p1 * t2;  // < 2L
-        dst[static_cast<size_t>(p1) * L2 + t2] = cmulc(a[q * L1 + swz<true>(p1)], TM(m));  // w_L^-(p1 t2)
+        dst[static_cast<size_t>(p1) * L2 + t2] = cmulc(a[q * S1 + swz<true>(p1)], TM(m));  // w_L^-(p1 t2)
     }
 }
 
@@ -529,8 +539,9 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
     const ThetaParams& P = Q.t;
     const int L = P.fd.L, L1 = Q.f1.L, L2 = Q.f2.L;
     const int nb = L1 / kBlkR;
+    const int S2 = L2 + kPad;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* t2hi = a + kSeqs * L2;
+    double2* t2hi = a + kSeqs * S2;
     double2* t2lo = t2hi + Q.f2.nhi;
     double2* tmhi = t2lo + Q.f2.nlo;
     double2* tmlo = tmhi + P.fd.nhi;
@@ -547,12 +558,12 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
     for (int e = tid; e < 2 * kBlkR * L2; e += nthr) {
         const int t2 = e & (L2 - 1), q = (e >> lg2) & (kBlkR - 1), par = e >> (lg2 + kLgR);
         const int p1 = kBlkR * b + q;
-        a[(par * kBlkR + q) * L2 + swz<true>(rev2[t2])] =
+        a[(par * kBlkR + q) * S2 + swz<true>(rev2[t2])] =
             Q.w1[((static_cast<size_t>(c) * 2 + par) * L1 + p1) * L2 + t2];
     }
     __syncthreads();
     const int seq = tid / kGrp, g = tid - seq * kGrp;
-    fft_inverse<true, 8>(a + seq * L2, Q.f2, T2, g, kGrp);  // natural p2
+    fft_inverse<true, 8>(a + seq * S2, Q.f2, T2, g, kGrp);  // natural p2
     // v_p = Ve_p + w_M^-p Vo_p, p = p1 + L1 p2 (and p = L = Ve_0 - Vo_0 from p1 = 0)
     const ColRef cr = col_ref(P, c);
     for (int e = tid; e < kBlkR * (L2 + 1); e += nthr) {
@@ -561,8 +572,8 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
         if (p2 == L2 && p1 != 0) continue;
         const int p = (p2 == L2) ? L : p1 + L1 * p2;
         const int sl = (p2 == L2) ? 0 : p2;
-        const double2 ve = a[q * L2 + swz<true>(sl)];
-        const double2 vo = a[(kBlkR + q) * L2 + swz<true>(sl)];
+        const double2 ve = a[q * S2 + swz<true>(sl)];
+        const double2 vo = a[(kBlkR + q) * S2 + swz<true>(sl)];
         const double2 v = cadd(ve, cmulc(vo, TM(p)));
         if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
         else cr[p] = v;
@@ -572,12 +583,13 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
 size_t theta_mp_smem_bytes(int which, int L1, int L2, int nhi1, int nlo1, int nhi2, int nlo2, int nhiM, int nloM) {
     switch (which) {
         case 0:  // TA / TE
-            return static_cast<size_t>(kSeqs) * L2 * 16 + static_cast<size_t>(nhi2 + nlo2 + nhiM + nloM) * 16 +
+            return static_cast<size_t>(kSeqs) * (L2 + kPad) * 16 + static_cast<size_t>(nhi2 + nlo2 + nhiM + nloM) * 16 +
                    static_cast<size_t>(L2) * 4;
         case 1:  // TB
-            return static_cast<size_t>(kSeqs) * L1 * 16 + static_cast<size_t>(nhi1 + nlo1) * 16 + static_cast<size_t>(L1) * 4;
+            return static_cast<size_t>(kSeqs) * (L1 + kPad) * 16 + static_cast<size_t>(nhi1 + nlo1) * 16 +
+                   static_cast<size_t>(L1) * 4;
         case 2:  // TD
-            return static_cast<size_t>(kSeqs) * L1 * 16 + static_cast<size_t>(nhi1 + nlo1 + nhiM + nloM) * 16 +
+            return static_cast<size_t>(kSeqs) * (L1 + kPad) * 16 + static_cast<size_t>(nhi1 + nlo1 + nhiM + nloM) * 16 +
                    static_cast<size_t>(L1) * 4;
         default:  // TC
             return static_cast<size_t>(kCthr * kSeg + 2) * 16 + static_cast<size_t>(kCthr * kSeg + 2 + 2) * 8 + 32 * 24 +

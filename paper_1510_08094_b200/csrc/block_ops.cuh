@@ -277,8 +277,13 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 }
 
 // atomic max of a non-negative double (IEEE order == unsigned order)
+// (the maximum only grows: a plain read first spares the atomic whenever the
+// stored value already dominates — hundreds of thousands of CTAs update one
+// address in the multi-pass theta stage, and same-address atomics serialise)
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
-    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (bits > *reinterpret_cast<volatile unsigned long long*>(addr))
+        atomicMax(reinterpret_cast<unsigned long long*>(addr), bits);
 }
 
 }  // namespace sk

@@ -47,7 +47,11 @@ constexpr int kBlkR = 8;   // r1 / p1 per CTA in TA / TE (two parities -> 16 seq
 constexpr int kLgR = 3;    // log2 kBlkR
 constexpr int kBlkT = 16;  // t2 per CTA in TB / TD
 constexpr int kLgT = 4;    // log2 kBlkT
-constexpr int kSeg = 8;    // chain elements per thread in TC (registers: no spills)
+// chain elements per thread in TC: ODD, so that a warp's per-element accesses
+// to the CTA's staged X (16 B) and pivots (8 B), a segment apart from lane to
+// lane, rotate through the bank groups (with 8 every lane hit the same one:
+// 32-way conflicts, the shared-memory pipe was TC's bound)
+constexpr int kSeg = 9;
 constexpr int kCq = 8;     // CTAs per TC cluster (portable maximum)
 constexpr int kCthr = 256; // threads per TC CTA
 // A CTA's sequences sit L + kPad slots apart in shared memory: the tile loads
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_b_kernel(ThetaMpParams Q) {
 // ----------------------------------------------------------------- TC
 // Cluster of kCq CTAs per (column, parity); CTA h owns chain+ elements
 // [h H, h H + H) (H = kCthr kSeg) in shared memory with one neighbour either side.
-__global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp_c_kernel(ThetaMpParams Q) {
+__global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp_c_kernel(ThetaMpParams Q, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const ThetaParams& P = Q.t;
@@ -311,9 +315,16 @@ __global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp
         }
         cluster.sync();
         if (h > 0) {
-            Aff3 pre = reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 10, 0))[0];
-            for (int o = 1; o < h; ++o)
-                pre = aff_combine(pre, reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 10, o))[0]);
+            // the totals of the CTAs before this one: all remote loads issue
+            // together (one DSMEM latency), then the ordered composition
+            Aff3 tot[kCq - 1];
+#pragma unroll
+            for (int o = 0; o < kCq - 1; ++o)
+                tot[o] = reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 10, o < h ? o : 0))[0];
+            Aff3 pre = tot[0];
+#pragma unroll
+            for (int o = 1; o < kCq - 1; ++o)
+                if (o < h) pre = aff_combine(pre, tot[o]);
             rin = aff_combine(pre, rin);
         }
     }
@@ -389,9 +400,16 @@ __global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp
     const int owner = (n - 1) / H;  // CTA holding the last element (Delta)
     const double2 Dl = cluster.map_shared_rank(misc, owner)[5];
     if (h < kCq - 1) {
-        Aff3 pre = reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 12, kCq - 1))[0];
-        for (int o = kCq - 2; o > h; --o)
-            pre = aff_combine(pre, reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 12, o))[0]);
+        Aff3 tot[kCq - 1];  // tot[j]: total of CTA kCq - 1 - j (loads issued together, as above)
+#pragma unroll
+        for (int j = 0; j < kCq - 1; ++j) {
+            const int o = kCq - 1 - j;
+            tot[j] = reinterpret_cast<const Aff3*>(cluster.map_shared_rank(misc + 12, o > h ? o : kCq - 1))[0];
+        }
+        Aff3 pre = tot[0];
+#pragma unroll
+        for (int j = 1; j < kCq - 1; ++j)
+            if (kCq - 1 - j > h) pre = aff_combine(pre, tot[j]);
         xin = aff_combine(pre, xin);
     }
     double2 xr = make_double2(xin.b, xin.c);
@@ -448,7 +466,10 @@ __global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp
         ws = block_sum2(ws, red);
         if (tid == 0) misc[9] = ws;
     }
-    cluster.sync();
+    // only the k = 0 constraint needs the other CTAs' sums; otherwise x_0 comes
+    // from CTA 0's own values and the cluster meets again only to keep every
+    // CTA's shared memory alive until the peers' DSMEM reads above are done
+    if (kg == 0) cluster.sync();
     if (h == 0 && tid == 0) {
         double fmx = fm;
         if (par == 0) {
@@ -479,7 +500,9 @@ __global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp
     } else if (tid == 0) {
         atomic_max_nonneg(st + 2, fm);
     }
-    cluster.sync();  // the peer's DSMEM reads are done
+    // exit: only consumed DSMEM loads since the last cluster barrier
+    // (theta_common.cuh cluster_exit_barrier's contract)
+    cluster_exit_barrier(relaxed_exit);
 }
 
 // X_half export of the multi-pass path: X(t) of column c at t = t_of(tau, par) + L
@@ -617,7 +640,7 @@ cudaError_t launch_theta_mp(const ThetaMpParams& Q, cudaStream_t st) {
     });
     theta_mp_a_kernel<<<NC * (L1 / kBlkR), kThr, sa, st>>>(Q);
     theta_mp_b_kernel<<<NC * 2 * (L2 / kBlkT), kThr, sb, st>>>(Q);
-    theta_mp_c_kernel<<<NC * 2 * kCq, kCthr, sc, st>>>(Q);
+    theta_mp_c_kernel<<<NC * 2 * kCq, kCthr, sc, st>>>(Q, exit_relaxed());
     if (Q.t.xhalf) {
         const long long tot = 2LL * Q.t.fd.L * NC;
         theta_mp_export_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(Q);

@@ -880,6 +880,206 @@ __device__ SK_CHAIN_ATTR void solve_chain_fast(double2* a, const int* __restrict
     __syncthreads();
 }
 
+// Both chains of a parity class from ONE segmented solve (the pairing of
+// theta_sym.cu, here on the unpruned transform of short columns, L even):
+// chain- (t < 0) sees s = (-1)^k times chain+'s right-hand side except on its
+// last rows (X_{-t} = s X_t + (1 - s) X_0 makes F- = s F+ in the interior and
+// at the inner end) and the same pivots up to there, so x- = s x+ + Phi Delta
+// with Phi_i = prod_{j=i}^{n-2} c_j the backward sweep's own product and Delta
+// the difference of the chains' last unknowns, computed by the thread that
+// owns chain+'s last element from the boundary rows (chain- values are read
+// directly: the whole transform is present).  ip: chain+'s pivot window
+// (ip[tau]); ip_extra: table entry tau = L/2 (par 0: chain-'s extra element
+// t = -L; par 1: chain-'s last element, an interior row where chain+ ends on
+// the truncation row).  g = r'/d' stays in F's registers between the sweeps.
+template <int S, bool HI>
+__device__ SK_CHAIN_ATTR void solve_chains_pair_fast(double2* a, const int* __restrict__ rev, const double* ip, Aff3* wsc,
+                                                     double2* misc, int par, int L, double sgn, double2 inner,
+                                                     double ip_extra, unsigned* fmax_hi, double2* wsum,
+                                                     bool want_wsum) {
+    constexpr int SP = (S + 1) / 2;
+    const int tid = threadIdx.x;
+    const int n = par == 0 ? L / 2 - 1 : L / 2;  // chain+ length
+    const int tau0 = par == 0 ? 1 : 0;
+    const int s = tid * S;
+    const double t_s = (par == 0 ? 2.0 : 1.0) + 2.0 * static_cast<double>(s);
+    const double tl = static_cast<double>(L - 1);
+    unsigned pk[SP];
+    double2 v[S];
+    double ipv[S];
+    {
+        const int* rb = rev + tau0 + s;
+        const double* ib = ip + tau0 + s;
+#pragma unroll
+        for (int u = 0; u < S; u += 2) {
+            const unsigned p0 = (s + u < n) ? static_cast<unsigned>(rb[u]) : 0u;
+            const unsigned p1 = (u + 1 < S && s + u + 1 < n) ? static_cast<unsigned>(rb[u + 1]) : 0u;
+            pk[u / 2] = p0 | (p1 << 16);
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) ipv[u] = (s + u < n) ? ib[u] : 0.0;
+    }
+    auto posu = [&](int u) { return static_cast<int>((u & 1) ? (pk[u / 2] >> 16) : (pk[u / 2] & 0xffffu)); };
+    double2 xlo = inner, xhi = make_double2(0.0, 0.0);
+    double ip_before = 0.0;
+    if (s > 0 && s <= n) {
+        xlo = a[rev[tau0 + s - 1]];
+        ip_before = ip[tau0 + s - 1];
+    }
+    if (s + S < n) xhi = a[rev[tau0 + s + S]];
+#pragma unroll
+    for (int u = 0; u < S; ++u) {
+        const bool ok = s + u < n;
+        const double2 x = a[posu(u)];
+        v[u] = ok ? x : make_double2(0.0, 0.0);
+        if (!ok) ipv[u] = 0.0;
+    }
+    const int ulast = n - 1 - s;  // chain+'s last element in this segment if 0 <= ulast < S
+    // ---- pass 1: F = Msin^2 X, forward affine summary
+    Aff3 aff = aff_identity();
+    double2 xlast = make_double2(0.0, 0.0), xlast_m = make_double2(0.0, 0.0);
+    unsigned fh = 0u;
+    {
+        double2 xm = xlo;
+        double ipp = ip_before;
+        double t = t_s;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            const double2 x0 = v[u];
+            const double2 xp = (u + 1 < S) ? v[u + 1] : xhi;
+            if (u == ulast) {
+                xlast = x0;
+                xlast_m = xm;
+            }
+            const double d2 = (t == tl) ? 0.25 : 0.5;
+            double2 F = make_double2(d2 * x0.x - 0.25 * (xm.x + xp.x), d2 * x0.y - 0.25 * (xm.y + xp.y));
+            if (s + u >= n) F = make_double2(0.0, 0.0);
+            fh = max(fh, static_cast<unsigned>(__double2hiint(fma(F.x, F.x, F.y * F.y))));
+            const double al = (-0.25 * ipp) * fma(t, t - 3.0, 2.0);
+            aff = Aff3{al * aff.a, fma(al, aff.b, F.x), fma(al, aff.c, F.y)};
+            v[u] = F;
+            ipp = ipv[u];
+            xm = x0;
+            t += 2.0;
+        }
+    }
+    const Aff3 rin = block_scan_aff1<false>(aff, wsc);
+#pragma unroll
+    for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
+    // ---- pass 2: r', g = r'/d' (registers), backward summary with the last multiplier 1
+    Aff3 baff;
+    double2 rlast = make_double2(0.0, 0.0);
+    {
+        double2 rp = make_double2(rin.b, rin.c);
+        double ipp = ip_before;
+        double t = launder(t_s);
+        double Pm = 1.0;
+        double2 G = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            const double al = (-0.25 * ipp) * fma(t, t - 3.0, 2.0);
+            rp = make_double2(fma(al, rp.x, v[u].x), fma(al, rp.y, v[u].y));
+            if (u == ulast) rlast = rp;
+            const double iv = ipv[u];
+            const double2 g = make_double2(rp.x * iv, rp.y * iv);
+            double c = (-0.25 * iv) * fma(t, t + 3.0, 2.0);
+            if (u == ulast || s + u >= n) c = 1.0;
+            G = make_double2(fma(Pm, g.x, G.x), fma(Pm, g.y, G.y));
+            Pm *= c;
+            v[u] = g;
+            ipv[u] = c;
+            ipp = iv;
+            t += 2.0;
+        }
+        baff = Aff3{Pm, G.x, G.y};
+    }
+    // ---- the boundary rows (theta_mp.cu TC): Delta = x-_{n-1} - s x+_{n-1}
+    if (ulast >= 0 && ulast < S) {
+        const double ipl = ip[tau0 + n - 1];
+        const double2 xp_last = make_double2(rlast.x * ipl, rlast.y * ipl);
+        const double2 Xm_last = a[rev[L - 1 - (n - 1)]];   // chain- element n-1
+        const double2 Xm_last2 = a[rev[L - 1 - (n - 2)]];  // chain- element n-2
+        double2 xm_last, xm_extra = make_double2(0.0, 0.0);
+        unsigned fb;
+        const double2 Fp = make_double2((par ? 0.25 : 0.5) * xlast.x - 0.25 * xlast_m.x,
+                                        (par ? 0.25 : 0.5) * xlast.y - 0.25 * xlast_m.y);  // F+_{n-1}
+        if (par == 0) {
+            const double Ld = L;
+            const double2 XmL = a[rev[L / 2]];  // X at t = -L
+            const double2 Fm1 = make_double2(0.5 * Xm_last.x - 0.25 * (Xm_last2.x + XmL.x),
+                                             0.5 * Xm_last.y - 0.25 * (Xm_last2.y + XmL.y));
+            const double2 rm1 = make_double2(sgn * rlast.x + (Fm1.x - sgn * Fp.x), sgn * rlast.y + (Fm1.y - sgn * Fp.y));
+            const double2 Fn = make_double2(0.25 * (XmL.x - Xm_last.x), 0.25 * (XmL.y - Xm_last.y));
+            const double An = 0.25 * (Ld - 2.0) * (Ld - 1.0);  // coupling of t = -L to t = -(L-2)
+            const double Cm = 0.25 * Ld * (Ld - 1.0);          // coupling of t = -(L-2) to t = -L
+            const double al = -An * ipl;
+            const double2 rn = make_double2(fma(al, rm1.x, Fn.x), fma(al, rm1.y, Fn.y));
+            xm_extra = make_double2(rn.x * ip_extra, rn.y * ip_extra);
+            const double be = -Cm * ipl;
+            xm_last = make_double2(fma(be, xm_extra.x, rm1.x * ipl), fma(be, xm_extra.y, rm1.y * ipl));
+            fb = max(static_cast<unsigned>(__double2hiint(fma(Fm1.x, Fm1.x, Fm1.y * Fm1.y))),
+                     static_cast<unsigned>(__double2hiint(fma(Fn.x, Fn.x, Fn.y * Fn.y))));
+        } else {
+            const double2 Fm1 = make_double2(0.5 * Xm_last.x - 0.25 * Xm_last2.x, 0.5 * Xm_last.y - 0.25 * Xm_last2.y);
+            const double2 rm1 = make_double2(sgn * rlast.x + (Fm1.x - sgn * Fp.x), sgn * rlast.y + (Fm1.y - sgn * Fp.y));
+            xm_last = make_double2(rm1.x * ip_extra, rm1.y * ip_extra);
+            fb = static_cast<unsigned>(__double2hiint(fma(Fm1.x, Fm1.x, Fm1.y * Fm1.y)));
+        }
+        fh = max(fh, fb);
+        misc[5] = make_double2(xm_last.x - sgn * xp_last.x, xm_last.y - sgn * xp_last.y);  // Delta
+        misc[6] = xm_extra;
+    }
+    *fmax_hi = max(*fmax_hi, fh);
+    const Aff3 xin = block_scan_aff1<true>(baff, wsc + 16);  // its barrier publishes Delta and orders the X reads above
+    const double2 Dl = misc[5];
+    // ---- pass 3: x+ = g + c x+, x- = s x+ + Phi Delta into both chains' slots
+#pragma unroll
+    for (int u = 0; u < SP; ++u) pk[u] = launder(pk[u]);
+    const double t_s3 = launder(t_s);
+    double2 x = make_double2(xin.b, xin.c);
+    double phi = xin.a;
+    double2 ws = make_double2(0.0, 0.0);
+    double2 xf_p = make_double2(0.0, 0.0), xf_m = make_double2(0.0, 0.0);
+    const int* rm = rev + (L - 1 - s);  // chain- element i at natural index L - 1 - i
+#pragma unroll
+    for (int u = S - 1; u >= 0; --u) {
+        if (s + u < n) {
+            const double c = ipv[u];
+            const double2 g = v[u];
+            x = (u != ulast) ? make_double2(fma(c, x.x, g.x), fma(c, x.y, g.y)) : g;
+            phi *= c;
+            const double2 xm = make_double2(fma(phi, Dl.x, sgn * x.x), fma(phi, Dl.y, sgn * x.y));
+            a[posu(u)] = x;
+            a[rm[-u]] = xm;
+            if (want_wsum) {
+                const double t = t_s3 + 2.0 * u;
+                const double w = 2.0 / (1.0 - t * t);  // w(t) = w(-t)
+                ws.x = fma(w, x.x + xm.x, ws.x);
+                ws.y = fma(w, x.y + xm.y, ws.y);
+            }
+            xf_p = x;
+            xf_m = xm;
+        }
+    }
+    if (par == 0 && ulast >= 0 && ulast < S) {
+        const double2 xe = misc[6];
+        a[rev[L / 2]] = xe;  // x at t = -L
+        if (want_wsum) {
+            const double Ld = L;
+            const double w = 2.0 / (1.0 - Ld * Ld);
+            ws.x = fma(w, xe.x, ws.x);
+            ws.y = fma(w, xe.y, ws.y);
+        }
+    }
+    wsum->x += ws.x;
+    wsum->y += ws.y;
+    if (tid == 0) {
+        misc[3] = xf_p;  // x+_0
+        misc[4] = xf_m;  // x-_0
+    }
+    __syncthreads();
+}
+
 // Smallest register segment S with ceil(n / S) <= nthr; 0 if none fits.
 __device__ __forceinline__ int chain_segment(int n, int nthr) {
     const int need = (n + nthr - 1) / nthr;
@@ -904,6 +1104,22 @@ __device__ __forceinline__ bool solve_chain_fast_dispatch(double2* a, const int*
         case 8: SK_CH(8); return true;
         case 10: SK_CH(10); return true;
         case 12: SK_CH(12); return true;
+        default: return false;
+    }
+#undef SK_CH
+}
+
+template <bool HI>
+__device__ __forceinline__ bool solve_chains_pair_dispatch(double2* a, const int* rev, const double* ip, Aff3* wsc,
+                                                           double2* misc, int par, int L, double sgn, double2 inner,
+                                                           double ip_extra, unsigned* fmax_hi, double2* wsum,
+                                                           bool want_wsum) {
+    const int n = par == 0 ? L / 2 - 1 : L / 2;
+#define SK_CH(S) solve_chains_pair_fast<S, HI>(a, rev, ip, wsc, misc, par, L, sgn, inner, ip_extra, fmax_hi, wsum, want_wsum)
+    switch (chain_segment(n, blockDim.x)) {
+        case 2: SK_CH(2); return true;
+        case 4: SK_CH(4); return true;
+        case 6: SK_CH(6); return true;
         default: return false;
     }
 #undef SK_CH
@@ -1214,6 +1430,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
         }
         misc[3] = make_double2(0.0, 0.0);
         misc[4] = make_double2(0.0, 0.0);
+        misc[5] = misc[6] = make_double2(0.0, 0.0);
+        // pivot table entry tau = L/2 (solve_chains_pair_fast's ip_extra)
+        misc[8] = make_double2(__ldg(P.pivots + prow + L / 2), 0.0);
     }
     __syncthreads();
     const double2 inner_p = misc[0], inner_m = misc[1], F0 = misc[2];
@@ -1237,12 +1456,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
             solve_chain(a, rev, ipc, wsc, ch, L, inner, fmax_acc, wsum, want_wsum, xf);
         }
     };
-    solve_side(cp, ipp, rev_p, inner_p, &misc[3]);
+    // short even columns on the segment solver: both chains from one solve
+    // (no second pivot window, no second solve)
+    bool paired = false;
+    if constexpr (CH == 1) {
+        if (P.pair_chains && !seq && !P.rev_win && (L & 1) == 0 && L >= 16)
+            paired = solve_chains_pair_dispatch<HI>(a, rev, ipp, wsc3, misc, par, L, sgn, inner_p, misc[8].x, &fmax_hi,
+                                                    &wsum, want_wsum);
+    }
+    if (!paired) solve_side(cp, ipp, rev_p, inner_p, &misc[3]);
     SK_PROBE(4);
     // the t < 0 chain's pivots replace the t > 0 chain's in the window
     const double* ipm = ip;
     const int* rev_m = rev;
-    if (cm.n > 0) {
+    if (cm.n > 0 && !paired) {
         uint32_t pb = 0, rbytes = 0;
         int ra0 = 0;
         ipm = pivot_window(ip, P.pivots, prow, L - cm.n, L, pb);
@@ -1256,7 +1483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
         mbar_wait(&bars[1], 0);
     }
     SK_PROBE(5);
-    solve_side(cm, ipm, rev_m, inner_m, &misc[4]);
+    if (!paired) solve_side(cm, ipm, rev_m, inner_m, &misc[4]);
     fmax_acc = fmax(fmax_acc, __hiloint2double(static_cast<int>(fmax_hi), 0));
     SK_PROBE(6);
     if (want_wsum) wsum = block_sum2(wsum, red);

@@ -44,6 +44,7 @@ struct ThetaParams {
     int regsolve;          // chain solver: 0 shared-memory walk, 1 fixed short segments, 2 SMAX=12 register walk
     int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
     int piv_stride;        // doubles per (mode, parity) pivot row
+    int pair_chains;       // theta_kernel segment solver: both chains of a parity from one solve (solve_chains_pair_fast)
     PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
     int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
     int hiocc;             // high-occupancy kernel variant (short columns: 64 registers, radices <= 8)

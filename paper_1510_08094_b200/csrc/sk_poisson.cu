@@ -327,6 +327,7 @@ struct sk_plan_s {
     double* stage_stats_h = nullptr;
     cudaEvent_t ev_stats = nullptr;
     int kseq = 0;              // lambda modes solved by the sequential recurrence (SK_KSEQ)
+    int pair_chains = 1;       // theta_kernel's segment solver pairs the chains of a parity (SK_PAIR_CHAINS=0: A/B)
     int piv_stride = 0;        // doubles per pivot-table row
     bool theta_hiocc = false;  // high-occupancy theta kernel variant (short columns)
     bool lambda_hiocc = false; // high-occupancy lambda kernel variant (short rows)
@@ -515,6 +516,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     }
     p->own_stream = true;
     if (const char* e = std::getenv("SK_KSEQ")) p->kseq = std::atoi(e);
+    if (const char* e = std::getenv("SK_PAIR_CHAINS")) p->pair_chains = std::atoi(e) != 0;
     if (const char* e = std::getenv("SK_REGSOLVE")) p->regsolve = std::atoi(e);
     p->g.M = M;
     p->g.N = N;
@@ -968,6 +970,7 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         tp.stats = p->stats;
         tp.xhalf = xhalf;
         tp.kseq = p->kseq;
+        tp.pair_chains = p->pair_chains;
         tp.regsolve = p->chain_mode;
         tp.hiocc = p->theta_hiocc ? 1 : 0;
         tp.rev_win = p->theta_q ? 0 : p->rev_win;

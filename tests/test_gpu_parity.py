@@ -431,6 +431,25 @@ def test_lambda_duo_bitwise(pkg, oracle, reference, m, n, monkeypatch):
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n", [(2048, 64), (4096, 24), (512, 48), (256, 40), (64, 32), (32, 16)])
+def test_pair_chains_matches_two_solves(pkg, oracle, reference, m, n, monkeypatch):
+    """Short even columns (C1, C2, C4: theta_kernel's segment solver) take both
+    chains of a parity from ONE solve (solve_chains_pair_fast: x- = s x+ +
+    Phi Delta, the pairing of theta_sym.cu on the unpruned transform).  On
+    rough zero-mean data (every lambda mode excited, the truncation rows
+    included) it agrees with the two separate solves (SK_PAIR_CHAINS=0) to
+    rounding and with the reference to 1e-10."""
+    f = zero_mean_noise(oracle, m, n, 3 * m + n)
+    with pkg.Plan(m, n) as plan:
+        u = plan.solve_grid(f)
+    monkeypatch.setenv("SK_PAIR_CHAINS", "0")
+    with pkg.Plan(m, n) as plan:
+        u2 = plan.solve_grid(f)
+    assert np.abs(u - u2).max() <= 1e-12 * np.abs(u2).max()
+    _, _, u_ref = ref_grid(reference, f, m)
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
 def test_bench_multi_rank_launcher():
     """bench.py --gpus 2 without a launcher re-runs itself under
     torch.distributed.run with 2 ranks (on a one-GPU box both share GPU 0:

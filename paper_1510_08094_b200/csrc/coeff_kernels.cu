@@ -43,26 +43,36 @@ __device__ __forceinline__ double lapc_diag(int i, int M) {
 }
 
 // warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0.
+// A lane owns ONE REAL COMPONENT of one column: lanes (2c, 2c+1) hold the real
+// and imaginary parts of column c (the operator is real, so the two components
+// of the complex right-hand side are independent real recurrences sharing the
+// pivots, which each lane of the pair computes for itself).  A warp's row
+// access is then one contiguous 256-byte segment of the interleaved complex
+// row, there are twice as many independent recurrences in flight, and each
+// back-substitution step carries one division instead of two.
 // Each thread's sweeps are a long dependent recurrence over M/4 rows; the
 // loads of the rows ahead (F forward, r and d' backward) do not depend on it,
-// so they are issued kPf rows ahead from a register ring (the pointers are
-// __restrict__: the stores of r and d' cannot alias the loads), which keeps
-// kPf * 16 B per thread in flight instead of one row's latency per step.
+// so they are issued a block of kPf rows ahead (the pointers are __restrict__:
+// the stores of r and d' cannot alias the loads), which keeps kPf * 8 B per
+// thread in flight instead of one row's latency per step.
 constexpr int kPf = 16;
 
 __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
-    __shared__ double2 s_rm2[32];   // r'_{-2}
-    __shared__ double s_dm2[32];    // d'_{-2}
-    __shared__ double2 s_x2[32];    // x_2
-    const int M = P.M, N = P.N, h = M / 2;
+    __shared__ double s_rm2[32];  // r'_{-2}
+    __shared__ double s_dm2[32];  // d'_{-2}
+    __shared__ double s_x2[32];   // x_2
+    const int M = P.M, N = P.N, h = M / 2, N2 = 2 * N;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int kc = blockIdx.x * 32 + lane;
+    const int kc2 = blockIdx.x * 32 + lane;  // component column: 2 kc + (0 re, 1 im)
+    const int kc = kc2 >> 1;
     const int rhs = blockIdx.y;
-    const bool live = kc < N;
+    const bool live = kc2 < N2;
+    const unsigned lmask = __ballot_sync(0xffffffffu, live);  // live lanes come in (re, im) pairs
     const size_t off = static_cast<size_t>(rhs) * M * N;
-    const double2* __restrict__ F = P.F + off;
-    double2* __restrict__ X = P.X + off;
+    const double* __restrict__ F = reinterpret_cast<const double*>(P.F + off);
+    double* __restrict__ X = reinterpret_cast<double*>(P.X + off);
     double* __restrict__ D = P.D + off;
+    const bool dwriter = (kc2 & 1) == 0;  // one lane of the pair stores d'
     const int k = kc - N / 2;
     const double negk2 = __dmul_rn(-static_cast<double>(k), static_cast<double>(k));  // -static_cast<double>(k) * k
     // chain rows (storage index i, ascending)
@@ -74,44 +84,53 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     else { i0 = h + 1; i1 = ((M - 1 - (h + 1)) / 2) * 2 + h + 1; }
     if (i1 > M - 1) i1 -= 2;
     const int nrow = (live && i0 <= i1) ? (i1 - i0) / 2 + 1 : 0;  // rows i0, i0+2, ..., i1
-    double fmx = 0.0;
+    double fmx = 0.0;  // max of this component's squares; the pair's sum below
     int bad = 0;
     // ---- forward elimination: d'_i = b_i - (a_i/d'_{i-2}) c_{i-2}; r_i = F_i - l r_{i-2}
     double dprev = 0.0;
-    double2 rprev = make_double2(0.0, 0.0);
+    double rprev = 0.0;
     if (nrow > 0) {
-        double2 ring[kPf];
+        // block prefetch: the next kPf rows are requested in one batch before the
+        // current kPf are consumed (a rolling one-row-at-a-time ring shares the
+        // few hardware scoreboards between old and young loads, so waiting for
+        // the oldest row also waits for rows requested a few steps ago)
+        double cur[kPf], nxt[kPf];
 #pragma unroll
-        for (int u = 0; u < kPf; ++u)
-            ring[u] = u < nrow ? F[static_cast<size_t>(i0 + 2 * u) * N + kc] : make_double2(0.0, 0.0);
+        for (int u = 0; u < kPf; ++u) cur[u] = u < nrow ? F[static_cast<size_t>(i0 + 2 * u) * N2 + kc2] : 0.0;
         for (int q0 = 0; q0 < nrow; q0 += kPf) {
+#pragma unroll
+            for (int u = 0; u < kPf; ++u)
+                nxt[u] = (q0 + kPf + u < nrow) ? F[static_cast<size_t>(i0 + 2 * (q0 + kPf + u)) * N2 + kc2] : 0.0;
 #pragma unroll
             for (int u = 0; u < kPf; ++u) {
                 const int q = q0 + u;
                 if (q < nrow) {
                     const int i = i0 + 2 * q;
-                    const double2 f = ring[u];
-                    if (q + kPf < nrow) ring[u] = F[static_cast<size_t>(i + 2 * kPf) * N + kc];
-                    fmx = fmax(fmx, f.x * f.x + f.y * f.y);  // squared (max|F| only scales the precondition test)
+                    const double f = cur[u];
+                    // |F|^2 = re^2 + im^2 from the lane pair (max|F| only scales the precondition test)
+                    const double f2 = f * f;
+                    fmx = fmax(fmx, f2 + __shfl_xor_sync(lmask, f2, 1));
                     const double b = __dadd_rn(lapc_diag(i, M), negk2);
                     double d = b;
-                    double2 r = f;
+                    double r = f;
                     if (q > 0) {
                         const double a = lapc_lower(i, M);
                         if (a != 0.0) {
                             if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
                             const double l = __ddiv_rn(a, dprev);
                             d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
-                            r = make_double2(__dsub_rn(f.x, __dmul_rn(l, rprev.x)), __dsub_rn(f.y, __dmul_rn(l, rprev.y)));
+                            r = __dsub_rn(f, __dmul_rn(l, rprev));
                         }
                     }
                     if (fabs(d) < 1e-300) bad += 1 << 20;
-                    X[static_cast<size_t>(i) * N + kc] = r;
-                    D[static_cast<size_t>(i) * N + kc] = d;
+                    X[static_cast<size_t>(i) * N2 + kc2] = r;
+                    if (dwriter) D[static_cast<size_t>(i) * N + kc] = d;
                     dprev = d;
                     rprev = r;
                 }
             }
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) cur[u] = nxt[u];
         }
     }
     if (w == 0 && live) {
@@ -119,39 +138,44 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
         s_dm2[lane] = dprev;
     }
     // ---- back substitution: x_i = (r_i - c_i x_{i+2}) / d'_i  (rows i1, i1-2, ..., i0)
-    double2 xnext = make_double2(0.0, 0.0);
+    // (d' of this sweep's rows: the lane's own forward values are bit-equal to
+    // the pair's stored ones, but they are gone from registers; both lanes read D)
+    __syncwarp();
+    double xnext = 0.0;
     if (nrow > 0) {
-        double2 rr[kPf];
-        double dr[kPf];
+        double rr[kPf], dr[kPf], rn[kPf], dn[kPf];
 #pragma unroll
         for (int u = 0; u < kPf; ++u) {
-            const size_t at = static_cast<size_t>(i1 - 2 * u) * N + kc;
-            rr[u] = u < nrow ? X[at] : make_double2(0.0, 0.0);
-            dr[u] = u < nrow ? D[at] : 1.0;
+            rr[u] = u < nrow ? X[static_cast<size_t>(i1 - 2 * u) * N2 + kc2] : 0.0;
+            dr[u] = u < nrow ? D[static_cast<size_t>(i1 - 2 * u) * N + kc] : 1.0;
         }
         for (int q0 = 0; q0 < nrow; q0 += kPf) {
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                const bool in = q0 + kPf + u < nrow;
+                const int i = i1 - 2 * (q0 + kPf + u);
+                rn[u] = in ? X[static_cast<size_t>(i) * N2 + kc2] : 0.0;
+                dn[u] = in ? D[static_cast<size_t>(i) * N + kc] : 1.0;
+            }
 #pragma unroll
             for (int u = 0; u < kPf; ++u) {
                 const int q = q0 + u;
                 if (q < nrow) {
                     const int i = i1 - 2 * q;
-                    const double2 r = rr[u];
-                    const double d = dr[u];
-                    if (q + kPf < nrow) {
-                        const size_t at = static_cast<size_t>(i - 2 * kPf) * N + kc;
-                        rr[u] = X[at];
-                        dr[u] = D[at];
-                    }
-                    double2 acc = r;
+                    double acc = rr[u];
                     if (i + 2 <= M - 1) {
                         const double c = lapc_upper(i, M);
-                        if (c != 0.0)
-                            acc = make_double2(__dsub_rn(acc.x, __dmul_rn(c, xnext.x)), __dsub_rn(acc.y, __dmul_rn(c, xnext.y)));
+                        if (c != 0.0) acc = __dsub_rn(acc, __dmul_rn(c, xnext));
                     }
-                    const double2 x = make_double2(__ddiv_rn(acc.x, d), __ddiv_rn(acc.y, d));
-                    X[static_cast<size_t>(i) * N + kc] = x;
+                    const double x = __ddiv_rn(acc, dr[u]);
+                    X[static_cast<size_t>(i) * N2 + kc2] = x;
                     xnext = x;
                 }
+            }
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                rr[u] = rn[u];
+                dr[u] = dn[u];
             }
         }
     }
@@ -159,42 +183,42 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     __syncthreads();
     // ---- row j = 0
     if (w == 0 && live) {
-        const double2 f0 = F[static_cast<size_t>(h) * N + kc];
-        fmx = fmax(fmx, f0.x * f0.x + f0.y * f0.y);
+        const double f0 = F[static_cast<size_t>(h) * N2 + kc2];
+        const double f02 = f0 * f0;
+        fmx = fmax(fmx, f02 + __shfl_xor_sync(lmask, f02, 1));
         const bool has_m2 = (h - 2) >= 0;
         const bool has_p2 = (h + 2) <= M - 1;
         if (k != 0) {
-            double2 r0 = f0;
+            double r0 = f0;
             if (has_m2) {  // eliminate with pivot row j = -2: f = lap[0][-2] / d'_{-2}
                 const double l = __ddiv_rn(lapc_lower(h, M), s_dm2[lane]);
-                r0 = make_double2(__dsub_rn(r0.x, __dmul_rn(l, s_rm2[lane].x)), __dsub_rn(r0.y, __dmul_rn(l, s_rm2[lane].y)));
+                r0 = __dsub_rn(r0, __dmul_rn(l, s_rm2[lane]));
             }
             if (has_p2) {
                 const double c = lapc_upper(h, M);
-                r0 = make_double2(__dsub_rn(r0.x, __dmul_rn(c, s_x2[lane].x)), __dsub_rn(r0.y, __dmul_rn(c, s_x2[lane].y)));
+                r0 = __dsub_rn(r0, __dmul_rn(c, s_x2[lane]));
             }
             const double d0 = __dadd_rn(lapc_diag(h, M), negk2);
-            X[static_cast<size_t>(h) * N + kc] = make_double2(__ddiv_rn(r0.x, d0), __ddiv_rn(r0.y, d0));
+            X[static_cast<size_t>(h) * N2 + kc2] = __ddiv_rn(r0, d0);
         }
     }
     __syncthreads();
     if (k == 0 && live && w == 0) {
         // constraint row 2 pi w^T X_0 = 0 replaces row j = 0:
         // x_0 = -(sum_{j != 0, j even} w_j x_j) / w_0, w_j = 2 / (1 - j^2)
-        double2 s = make_double2(0.0, 0.0);
+        double s = 0.0;
         for (int i = even_lo; i < M; i += 2) {
             if (i == h) continue;
             const double j = i - h;
             const double wj = 2.0 / (1.0 - j * j);
-            const double2 x = X[static_cast<size_t>(i) * N + kc];
-            s = make_double2(__dadd_rn(s.x, __dmul_rn(wj, x.x)), __dadd_rn(s.y, __dmul_rn(wj, x.y)));
+            s = __dadd_rn(s, __dmul_rn(wj, X[static_cast<size_t>(i) * N2 + kc2]));
         }
-        X[static_cast<size_t>(h) * N + kc] = make_double2(-__ddiv_rn(s.x, 2.0), -__ddiv_rn(s.y, 2.0));
+        X[static_cast<size_t>(h) * N2 + kc2] = -__ddiv_rn(s, 2.0);
     }
     // stats
     const double fm = sqrt(warp_max(live ? fmx : 0.0));
     if (lane == 0) atomic_max_nonneg(P.stats + 4 * rhs + 2, fm);
-    if (bad) atomicAdd(P.stats + 4 * rhs + 3, static_cast<double>(bad));
+    if (bad && dwriter) atomicAdd(P.stats + 4 * rhs + 3, static_cast<double>(bad));
 }
 
 // check_mean_zero (poisson.cpp:101-117): the reference computes
@@ -318,7 +342,7 @@ cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st) {
     if (P.z) {
         mean_kernel<<<P.nrhs, 256, 0, st>>>(P);
     }
-    dim3 grid((P.N + 31) / 32, P.nrhs);
+    dim3 grid((2 * P.N + 31) / 32, P.nrhs);  // one lane per real component of a column
     coeff_solve_kernel<<<grid, 128, 0, st>>>(P);
     return cudaGetLastError();
 }

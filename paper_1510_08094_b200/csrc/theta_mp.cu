@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_a_kernel(ThetaMpParams Q) {
     const ColRef cr = col_ref(P, c);
     const int lg2 = ilog2(L2);
     // fold: element (q, r2) of this block, r = r1 + L1 r2, r1 = kBlkR b + q
-#pragma unroll 4
+#pragma unroll 8
     for (int e = tid; e < kBlkR * L2; e += nthr) {
         const int q = e & (kBlkR - 1), r2 = e >> kLgR;
         const int r1 = kBlkR * b + q;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_b_kernel(ThetaMpParams Q) {
     for (int i = tid; i < L1; i += nthr) rev1[i] = __ldg(Q.f1.rev + i);
     const double2* src = Q.w1 + static_cast<size_t>(cp) * L2 * L1;
     const int lg1 = ilog2(L1);
-#pragma unroll 4
+#pragma unroll 8
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int r1 = e & (L1 - 1), q = e >> lg1;
         a[q * S1 + swz<true>(r1)] = src[static_cast<size_t>(kBlkT * b + q) * L1 + r1];
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_d_kernel(ThetaMpParams Q) {
     for (int i = tid; i < L1; i += nthr) rev1[i] = __ldg(Q.f1.rev + i);
     __syncthreads();
     const double2* src = Q.w2 + static_cast<size_t>(cp) * L;
-#pragma unroll 4
+#pragma unroll 8
     for (int e = tid; e < kBlkT * L1; e += nthr) {
         const int q = e & (kBlkT - 1), t1 = e >> kLgT;
         a[q * S1 + swz<true>(rev1[t1])] = src[static_cast<size_t>(t1) * L2 + kBlkT * b + q];  // DIT input order
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
     for (int i = tid; i < L2; i += nthr) rev2[i] = __ldg(Q.f2.rev + i);
     __syncthreads();
     const int lg2 = ilog2(L2);
-#pragma unroll 4
+#pragma unroll 8
     for (int e = tid; e < 2 * kBlkR * L2; e += nthr) {
         const int t2 = e & (L2 - 1), q = (e >> lg2) & (kBlkR - 1), par = e >> (lg2 + kLgR);
         const int p1 = kBlkR * b + q;

@@ -52,6 +52,9 @@ constexpr int kLgT = 4;    // log2 kBlkT
 // lane, rotate through the bank groups (with 8 every lane hit the same one:
 // 32-way conflicts, the shared-memory pipe was TC's bound)
 constexpr int kSeg = 9;
+#ifndef SK_TC_MINB
+#define SK_TC_MINB 2  // CTAs per SM the chain pass is compiled for (A/B: 3 spills at 80 registers)
+#endif
 constexpr int kCq = 8;     // CTAs per TC cluster (portable maximum)
 constexpr int kCthr = 256; // threads per TC CTA
 // A CTA's sequences sit L + kPad slots apart in shared memory: the tile loads
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_b_kernel(ThetaMpParams Q) {
 // ----------------------------------------------------------------- TC
 // Cluster of kCq CTAs per (column, parity); CTA h owns chain+ elements
 // [h H, h H + H) (H = kCthr kSeg) in shared memory with one neighbour either side.
-__global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, 2) theta_mp_c_kernel(ThetaMpParams Q, int relaxed_exit) {
+__global__ void __cluster_dims__(kCq, 1, 1) __launch_bounds__(kCthr, SK_TC_MINB) theta_mp_c_kernel(ThetaMpParams Q, int relaxed_exit) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const ThetaParams& P = Q.t;

@@ -334,6 +334,17 @@ def main():
             args.transport = "p2p"
         else:
             dist.init_process_group("nccl", device_id=dev)
+            if args.transport == "p2p" and cfg.nrhs == 1:
+                # the fused transposes store into the peers' buffers: every GPU
+                # pair of the job must have peer access (NVLink / NVSwitch);
+                # the answer is reduced so that all ranks take the same path
+                ok = all(torch.cuda.can_device_access_peer(local_dev, d) for d in range(min(world, ndev)) if d != local_dev)
+                t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                if t.item() == 0:
+                    if rank == 0:
+                        print("bench.py: no peer access between all GPUs; using --transport nccl", file=sys.stderr)
+                    args.transport = "nccl"
 
     from paper_1510_08094_b200.poisson import Plan
     hbm_peak, peak_kind = measured_peaks()

@@ -54,6 +54,24 @@ def test_coeff_solve_bench_workload_vs_oracle(pkg, oracle, s):
     _assert_reference_bits(X, oracle.solve(F, threads=8), s)
 
 
+def test_bench_poisson_mirror(pkg, oracle):
+    """bench_poisson (poisson.cpp:188-230) on the device: the reference's
+    sizes -> (size, reps, seconds) rows, the same RNG stream across sizes
+    (the generator is not reseeded between sizes), its size check, and the
+    problem it times solved bit-identically to the reference's solve."""
+    import paper_1510_08094_b200 as sk
+    rows = sk.bench_poisson([64, 128], reps=2)
+    assert [r.size for r in rows] == [64, 128] and all(r.reps == 2 and r.seconds > 0 for r in rows)
+    with pytest.raises(sk.size_error):
+        sk.bench_poisson([15])
+    from paper_1510_08094_b200.inputs import bench_problem
+    F = bench_problem([64, 128])  # the second problem of the stream
+    assert np.array_equal(F, oracle.bench_problem([64, 128]))
+    with pkg.Plan(128, 128) as plan:
+        X = plan.solve_coeffs(F)
+    _assert_reference_bits(X, oracle.solve(F, threads=4), 128)
+
+
 @pytest.mark.parametrize("m,n,seed", [(64, 32, 1), (32, 64, 2), (150, 40, 3), (18, 22, 4)])
 def test_coeff_solve_rectangular_vs_oracle(pkg, oracle, m, n, seed):
     F = oracle.random_mean_zero_problem(m, n, seed)

@@ -468,6 +468,21 @@ def test_pair_chains_matches_two_solves(pkg, oracle, reference, m, n, monkeypatc
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n", [(512, 256), (2048, 64), (6000, 64), (12000, 48), (64, 3000), (65536, 24), (256, 32768)])
+def test_repeated_solves_bitwise(pkg, oracle, m, n):
+    """Every kernel family of the grid path — the paired segment solver on short
+    columns, theta_sym, the multi-pass theta stage (M/2 = 32768), lambda row
+    pairs and the split lambda rows — gives the same bits on every one of 12
+    consecutive solves of rough data (a shared-memory or DSMEM race, or a
+    barrier released too early, shows up as run-to-run differences; this pool
+    has no compute-sanitizer)."""
+    f = zero_mean_noise(oracle, m, n, 7 * m + n)
+    with pkg.Plan(m, n) as plan:
+        u0 = plan.solve_grid(f).copy()
+        for _ in range(11):
+            assert np.array_equal(plan.solve_grid(f), u0)
+
+
 def test_bench_multi_rank_launcher():
     """bench.py --gpus 2 without a launcher re-runs itself under
     torch.distributed.run with 2 ranks (on a one-GPU box both share GPU 0:

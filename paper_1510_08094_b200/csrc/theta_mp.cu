@@ -51,12 +51,16 @@ constexpr int kLgT = 4;    // log2 kBlkT
 // to the CTA's staged X (16 B) and pivots (8 B), a segment apart from lane to
 // lane, rotate through the bank groups (with 8 every lane hit the same one:
 // 32-way conflicts, the shared-memory pipe was TC's bound)
-constexpr int kSeg = 9;
+#ifndef SK_TC_SEG
+#define SK_TC_SEG 9
+#define SK_TC_THR 256
+#endif
+constexpr int kSeg = SK_TC_SEG;
 #ifndef SK_TC_MINB
 #define SK_TC_MINB 2  // CTAs per SM the chain pass is compiled for (A/B: 3 spills at 80 registers)
 #endif
 constexpr int kCq = 8;     // CTAs per TC cluster (portable maximum)
-constexpr int kCthr = 256; // threads per TC CTA
+constexpr int kCthr = SK_TC_THR; // threads per TC CTA
 // A CTA's sequences sit L + kPad slots apart in shared memory: the tile loads
 // and stores of every pass walk the SEQUENCE index fastest (8 or 16
 // neighbouring lanes, the contiguous direction in HBM), and with a stride of
@@ -109,31 +113,50 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_a_kernel(ThetaMpParams Q) {
     __syncthreads();
     const double invM = 1.0 / P.g.M;
     const ColRef cr = col_ref(P, c);
-    const int lg2 = ilog2(L2);
-    // fold: element (q, r2) of this block, r = r1 + L1 r2, r1 = kBlkR b + q
-#pragma unroll 8
-    for (int e = tid; e < kBlkR * L2; e += nthr) {
-        const int q = e & (kBlkR - 1), r2 = e >> kLgR;
+    // fold: element (q, r2) of this block, r = r1 + L1 r2, r1 = kBlkR b + q.
+    // A thread keeps its q and walks r2 in steps of kThr / kBlkR, so the
+    // fold's twiddle T(r) advances by a constant factor per trip (one table
+    // lookup per thread instead of one per element: the passes are bound by
+    // the shared-memory pipe, profiles/r2_c5_mp_launches.md).
+    constexpr int kR2Step = kThr / kBlkR;
+    {
+        const int q = tid & (kBlkR - 1);
         const int r1 = kBlkR * b + q;
-        const int r = r1 + L1 * r2;
-        double2 ar = cr[r];
-        const double2 am = cr[L - r];  // a_L for r = 0
-        if (r == 0 && P.g.pole_glide) ar = cscale(ar, sgn);  // sk_internal.h GridGeom::pole_glide
-        const double2 ev = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
-        const double2 od = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), TM(r)), invM);
-        a[q * S2 + swz<true>(r2)] = ev;
-        a[(kBlkR + q) * S2 + swz<true>(r2)] = od;
+        double2 wf = TM(r1 + L1 * (tid >> kLgR));
+        const double2 Wf = TM(kR2Step * L1);  // < 2L: L2 >= 32
+#pragma unroll 8
+        for (int r2 = tid >> kLgR; r2 < L2; r2 += kR2Step) {
+            const int r = r1 + L1 * r2;
+            double2 ar = cr[r];
+            const double2 am = cr[L - r];  // a_L for r = 0
+            if (r == 0 && P.g.pole_glide) ar = cscale(ar, sgn);  // sk_internal.h GridGeom::pole_glide
+            const double2 ev = make_double2((ar.x + sgn * am.x) * invM, (ar.y + sgn * am.y) * invM);
+            const double2 od = cscale(cmul(make_double2(ar.x - sgn * am.x, ar.y - sgn * am.y), wf), invM);
+            a[q * S2 + swz<true>(r2)] = ev;
+            a[(kBlkR + q) * S2 + swz<true>(r2)] = od;
+            wf = cmul(wf, Wf);
+        }
     }
     __syncthreads();
     const int seq = tid / kGrp, g = tid - seq * kGrp;
     fft_forward<true, 8>(a + seq * S2, Q.f2, T2, g, kGrp);  // t2 at slot swz(rev2[t2])
-    // twiddle w_L^(r1 t2) = T(2 r1 t2) and the store of (par, t2, r1)
-    for (int e = tid; e < 2 * kBlkR * L2; e += nthr) {
-        const int q = e & (kBlkR - 1), t2 = (e >> kLgR) & (L2 - 1), par = e >> (kLgR + lg2);
+    // twiddle w_L^(r1 t2) = T(2 r1 t2) and the store of (par, t2, r1): both
+    // parities of a (t2, r1) share the twiddle, which advances by T(2 r1
+    // kR2Step) per trip
+    {
+        const int q = tid & (kBlkR - 1);
         const int r1 = kBlkR * b + q;
-        const double2 v = a[(par * kBlkR + q) * S2 + swz<true>(rev2[t2])];
-        const int m = 2 * r1 * t2;  // < 2 L1 L2 = 2L: no reduction
-        Q.w1[((static_cast<size_t>(c) * 2 + par) * L2 + t2) * L1 + r1] = cmul(v, TM(m));
+        double2 wt = TM(2 * r1 * (tid >> kLgR));  // 2 r1 t2 < 2 L1 L2 = 2L: no reduction
+        const double2 Wt = TM(2 * kR2Step * r1);  // < 2L: r1 < L1, L2 >= 32
+        for (int t2 = tid >> kLgR; t2 < L2; t2 += kR2Step) {
+            const int sl = swz<true>(rev2[t2]);
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+                const double2 v = a[(par * kBlkR + q) * S2 + sl];
+                Q.w1[((static_cast<size_t>(c) * 2 + par) * L2 + t2) * L1 + r1] = cmul(v, wt);
+            }
+            wt = cmul(wt, Wt);
+        }
     }
 }
 
@@ -551,11 +574,18 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_d_kernel(ThetaMpParams Q) {
     const int seq = tid / kGrp, g = tid - seq * kGrp;
     fft_inverse<true, 8>(a + seq * S1, Q.f1, T1, g, kGrp);  // natural p1
     double2* dst = Q.w1 + static_cast<size_t>(cp) * L1 * L2;
-    for (int e = tid; e < kBlkT * L1; e += nthr) {
-        const int q = e & (kBlkT - 1), p1 = e >> kLgT;
+    {
+        // w_L^-(p1 t2) = conj T(2 p1 t2): a thread keeps its t2 and walks p1 in
+        // steps of kThr / kBlkT, the twiddle advancing by T(2 t2 step) per trip
+        constexpr int kP1Step = kThr / kBlkT;
+        const int q = tid & (kBlkT - 1);
         const int t2 = kBlkT * b + q;
-        const int m = 2 * p1 * t2;  // < 2L
-        dst[static_cast<size_t>(p1) * L2 + t2] = cmulc(a[q * S1 + swz<true>(p1)], TM(m));  // w_L^-(p1 t2)
+        double2 wt = TM(2 * (tid >> kLgT) * t2);  // < 2L
+        const double2 Wt = TM(2 * kP1Step * t2);  // < 2L: t2 < L2, L1 >= 16
+        for (int p1 = tid >> kLgT; p1 < L1; p1 += kP1Step) {
+            dst[static_cast<size_t>(p1) * L2 + t2] = cmulc(a[q * S1 + swz<true>(p1)], wt);
+            wt = cmul(wt, Wt);
+        }
     }
 }
 
@@ -592,17 +622,29 @@ __global__ void __launch_bounds__(kThr, 3) theta_mp_e_kernel(ThetaMpParams Q) {
     fft_inverse<true, 8>(a + seq * S2, Q.f2, T2, g, kGrp);  // natural p2
     // v_p = Ve_p + w_M^-p Vo_p, p = p1 + L1 p2 (and p = L = Ve_0 - Vo_0 from p1 = 0)
     const ColRef cr = col_ref(P, c);
-    for (int e = tid; e < kBlkR * (L2 + 1); e += nthr) {
-        const int q = e & (kBlkR - 1), p2 = e >> kLgR;
+    {
+        // a thread keeps its p1 and walks p2; T(p) advances by T(L1 step) per trip
+        constexpr int kP2Step = kThr / kBlkR;
+        const int q = tid & (kBlkR - 1);
         const int p1 = kBlkR * b + q;
-        if (p2 == L2 && p1 != 0) continue;
-        const int p = (p2 == L2) ? L : p1 + L1 * p2;
-        const int sl = (p2 == L2) ? 0 : p2;
-        const double2 ve = a[q * S2 + swz<true>(sl)];
-        const double2 vo = a[(kBlkR + q) * S2 + swz<true>(sl)];
-        const double2 v = cadd(ve, cmulc(vo, TM(p)));
-        if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
-        else cr[p] = v;
+        double2 wp = TM(p1 + L1 * (tid >> kLgR));
+        const double2 Wp = TM(kP2Step * L1);  // < 2L: L2 >= 32
+        for (int p2 = tid >> kLgR; p2 < L2; p2 += kP2Step) {
+            const int p = p1 + L1 * p2;
+            const double2 ve = a[q * S2 + swz<true>(p2)];
+            const double2 vo = a[(kBlkR + q) * S2 + swz<true>(p2)];
+            const double2 v = cadd(ve, cmulc(vo, wp));
+            if (P.peers.n) *peer_ptr(P.peers, p, kg, p) = v;  // fused return transpose
+            else cr[p] = v;
+            wp = cmul(wp, Wp);
+        }
+        if (tid == 0 && b == 0) {  // p = L (theta = pi): Ve_0 - Vo_0, T(L) = -1
+            const double2 ve = a[swz<true>(0)];
+            const double2 vo = a[kBlkR * S2 + swz<true>(0)];
+            const double2 v = cadd(ve, cmulc(vo, TM(L)));
+            if (P.peers.n) *peer_ptr(P.peers, L, kg, L) = v;
+            else cr[L] = v;
+        }
     }
 }
 

@@ -42,6 +42,11 @@ __device__ __forceinline__ double lapc_diag(int i, int M) {
     return -__dmul_rn(__dmul_rn(j, j), 0.5);
 }
 
+// 0 / d for finite nonzero d: a zero with sign(num) xor sign(d) (IEEE 754)
+__device__ __forceinline__ double signed_zero(double num, double d) {
+    return __longlong_as_double((__double_as_longlong(num) ^ __double_as_longlong(d)) & static_cast<long long>(0x8000000000000000ULL));
+}
+
 // warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0.
 // A lane owns ONE REAL COMPONENT of one column: lanes (2c, 2c+1) hold the real
 // and imaginary parts of column c (the operator is real, so the two components
@@ -167,7 +172,11 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
                         const double c = lapc_upper(i, M);
                         if (c != 0.0) acc = __dsub_rn(acc, __dmul_rn(c, xnext));
                     }
-                    const double x = __ddiv_rn(acc, dr[u]);
+                    // a zero numerator leaves the division's fast path (its range
+                    // check reads the quotient's magnitude) for a long subroutine;
+                    // band-limited right-hand sides are mostly zeros: +-0 directly,
+                    // with the IEEE sign of 0 / d
+                    const double x = (acc == 0.0) ? signed_zero(acc, dr[u]) : __ddiv_rn(acc, dr[u]);
                     X[static_cast<size_t>(i) * N2 + kc2] = x;
                     xnext = x;
                 }

@@ -163,6 +163,15 @@ class SlabSolver:
         self.rb = slab_bounds(self.rows, world)
         self.cb = slab_bounds(self.cols, world)
         self.group = group
+        # Host-side coordination (ordering event records before waits, the
+        # precondition reduction of three host doubles) goes through a CPU
+        # (gloo) group when the job's backend is NCCL: an NCCL barrier or
+        # all-reduce is stream-ordered behind the queued stage kernels, so
+        # waiting for it on the host would drain the stream between stages.
+        self.host_group = group
+        if dist.is_initialized() and dist.get_backend(group) == "nccl":
+            ranks = dist.get_process_group_ranks(group) if group is not None else None
+            self.host_group = dist.new_group(ranks=ranks, backend="gloo")
         self.device = device if device is not None else torch.device("cpu")
         if backend is None:
             from .poisson import Plan
@@ -236,7 +245,7 @@ class SlabSolver:
     def _host_barrier(self):
         """Orders every rank's event records before the peers' waits (host
         side only: the stages keep running on the GPUs meanwhile)."""
-        self.dist.barrier(group=self.group)
+        self.dist.barrier(group=self.host_group)
 
     def close(self):
         if self.transport == "p2p":
@@ -258,12 +267,11 @@ class SlabSolver:
         if stats is None:
             return
         mre, mim, fmax = stats()
-        # NCCL reduces device tensors; gloo (CPU tests, ranks sharing one GPU) host tensors
-        rdev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
-        t = torch.tensor([mre, mim, fmax], dtype=torch.float64, device=rdev)
+        # three host doubles: reduced on the CPU group (no stream is touched)
+        t = torch.tensor([mre, mim, fmax], dtype=torch.float64)
         m = t[2:].clone()
-        dist.all_reduce(t, group=self.group)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(t, group=self.host_group)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.host_group)
         mu = complex(t[0].item(), t[1].item())
         fscale = m.item()
         if fscale != 0.0 and abs(mu) > 1e-6 * 4.0 * np.pi * fscale:

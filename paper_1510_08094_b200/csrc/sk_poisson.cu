@@ -632,6 +632,7 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     // lambda stages: one CTA per row, or a CTA pair splitting the row by parity
     // (odd first span: the digit-reversed split/pack walks spread over all banks)
     p->thr_lambda = round_threads(Ll / 8, 64, 256);
+    if (const char* e = std::getenv("SK_LAMBDA_THREADS")) p->thr_lambda = round_threads(std::atoi(e), 64, 256);  // A/B
     // short rows (<= 128 threads per CTA) run the high-occupancy lambda variant
     // (64 registers, radices <= 8, <= 6 mode pairs per thread; SK_NO_HIOCC)
     p->lambda_hiocc = p->thr_lambda <= 128 && (Ll / 2 + 1) <= 6 * p->thr_lambda && !std::getenv("SK_NO_HIOCC");

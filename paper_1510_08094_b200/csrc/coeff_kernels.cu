@@ -47,24 +47,76 @@ __device__ __forceinline__ double signed_zero(double num, double d) {
     return __longlong_as_double((__double_as_longlong(num) ^ __double_as_longlong(d)) & static_cast<long long>(0x8000000000000000ULL));
 }
 
-// warp w of the CTA: 0 even j<0, 1 odd j<0, 2 even j>0, 3 odd j>0.
-// A lane owns ONE REAL COMPONENT of one column: lanes (2c, 2c+1) hold the real
-// and imaginary parts of column c (the operator is real, so the two components
-// of the complex right-hand side are independent real recurrences sharing the
-// pivots, which each lane of the pair computes for itself).  A warp's row
-// access is then one contiguous 256-byte segment of the interleaved complex
-// row, there are twice as many independent recurrences in flight, and each
-// back-substitution step carries one division instead of two.
+// Chain rows of warp w (storage index i ascending): 0 even j<0, 1 odd j<0,
+// 2 even j>0, 3 odd j>0.
+__device__ __forceinline__ void chain_rows(int w, int M, int& i0, int& i1) {
+    const int h = M / 2;
+    const int even_lo = (h & 1) ? 1 : 0;  // i with j = i - h even
+    if (w == 0) { i0 = even_lo; i1 = h - 2; }
+    else if (w == 1) { i0 = 1 - even_lo; i1 = h - 1; }
+    else if (w == 2) { i0 = h + 2; i1 = ((M - 1 - (h + 2)) / 2) * 2 + h + 2; }
+    else { i0 = h + 1; i1 = ((M - 1 - (h + 1)) / 2) * 2 + h + 1; }
+    if (i1 > M - 1) i1 -= 2;
+}
+
+// The elimination's data-independent half, once per plan: for every column
+// and chain the pivots d'_i = b_i - l_i c_{i-2} and multipliers l_i = a_i /
+// d'_{i-2} of band_solve's forward sweep (banded.cpp:121-147), by the same
+// sequential IEEE recurrence, so that the per-solve sweeps below carry no
+// division on the forward path and read d' instead of recomputing it.
+// bad[0] counts the rows where band_solve would have swapped (|a| > |d'|) and
+// 2^20 per singular pivot.  One lane per (column, chain).
+__global__ void __launch_bounds__(128) coeff_tables_kernel(int M, int N, double* __restrict__ D, double* __restrict__ Lm,
+                                                           double* bad_out) {
+    const int h = M / 2;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int kc = blockIdx.x * 32 + lane;
+    if (kc >= N) return;
+    const int k = kc - N / 2;
+    const double negk2 = __dmul_rn(-static_cast<double>(k), static_cast<double>(k));
+    int i0, i1;
+    chain_rows(w, M, i0, i1);
+    (void)h;
+    int bad = 0;
+    double dprev = 0.0;
+    for (int i = i0, q = 0; i <= i1; i += 2, ++q) {
+        const double b = __dadd_rn(lapc_diag(i, M), negk2);
+        double d = b, l = 0.0;
+        if (q > 0) {
+            const double a = lapc_lower(i, M);
+            if (a != 0.0) {
+                if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
+                l = __ddiv_rn(a, dprev);
+                d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
+            } else {
+                bad += 1 << 20;  // a vanishing sub-diagonal inside a chain: not this operator
+            }
+        }
+        if (fabs(d) < 1e-300) bad += 1 << 20;
+        D[static_cast<size_t>(i) * N + kc] = d;
+        Lm[static_cast<size_t>(i) * N + kc] = l;
+        dprev = d;
+    }
+    if (bad) atomicAdd(bad_out, static_cast<double>(bad));
+}
+
+// K5.  A lane owns ONE REAL COMPONENT of one column: lanes (2c, 2c+1) hold the
+// real and imaginary parts of column c (the operator is real, so the two
+// components of the complex right-hand side are independent real recurrences
+// sharing the tables).  A warp's row access is one contiguous 256-byte segment
+// of the interleaved complex row, there are twice as many independent
+// recurrences in flight, and each back-substitution step carries one division.
 // Each thread's sweeps are a long dependent recurrence over M/4 rows; the
-// loads of the rows ahead (F forward, r and d' backward) do not depend on it,
-// so they are issued a block of kPf rows ahead (the pointers are __restrict__:
-// the stores of r and d' cannot alias the loads), which keeps kPf * 8 B per
-// thread in flight instead of one row's latency per step.
+// loads of the rows ahead (F and l forward, r and d' backward) do not depend
+// on it, so they are issued a block of kPf rows ahead, which keeps kPf * 16 B
+// per thread in flight instead of one row's latency per step.  (A rolling
+// one-row ring shares the few hardware scoreboards between old and young
+// loads: waiting for the oldest row also waits for rows requested a few steps
+// ago.)
 constexpr int kPf = 16;
 
 __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     __shared__ double s_rm2[32];  // r'_{-2}
-    __shared__ double s_dm2[32];  // d'_{-2}
     __shared__ double s_x2[32];   // x_2
     const int M = P.M, N = P.N, h = M / 2, N2 = 2 * N;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -76,36 +128,32 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     const size_t off = static_cast<size_t>(rhs) * M * N;
     const double* __restrict__ F = reinterpret_cast<const double*>(P.F + off);
     double* __restrict__ X = reinterpret_cast<double*>(P.X + off);
-    double* __restrict__ D = P.D + off;
-    const bool dwriter = (kc2 & 1) == 0;  // one lane of the pair stores d'
+    const double* __restrict__ D = P.D;
+    const double* __restrict__ Lm = P.Lm;
     const int k = kc - N / 2;
     const double negk2 = __dmul_rn(-static_cast<double>(k), static_cast<double>(k));  // -static_cast<double>(k) * k
-    // chain rows (storage index i, ascending)
     const int even_lo = (h & 1) ? 1 : 0;  // i with j = i - h even
     int i0, i1;
-    if (w == 0) { i0 = even_lo; i1 = h - 2; }
-    else if (w == 1) { i0 = 1 - even_lo; i1 = h - 1; }
-    else if (w == 2) { i0 = h + 2; i1 = ((M - 1 - (h + 2)) / 2) * 2 + h + 2; }
-    else { i0 = h + 1; i1 = ((M - 1 - (h + 1)) / 2) * 2 + h + 1; }
-    if (i1 > M - 1) i1 -= 2;
+    chain_rows(w, M, i0, i1);
     const int nrow = (live && i0 <= i1) ? (i1 - i0) / 2 + 1 : 0;  // rows i0, i0+2, ..., i1
-    double fmx = 0.0;  // max of this component's squares; the pair's sum below
-    int bad = 0;
-    // ---- forward elimination: d'_i = b_i - (a_i/d'_{i-2}) c_{i-2}; r_i = F_i - l r_{i-2}
-    double dprev = 0.0;
+    double fmx = 0.0;  // max of the pair's re^2 + im^2
+    // ---- forward elimination: r_i = F_i - l_i r_{i-2}
     double rprev = 0.0;
     if (nrow > 0) {
-        // block prefetch: the next kPf rows are requested in one batch before the
-        // current kPf are consumed (a rolling one-row-at-a-time ring shares the
-        // few hardware scoreboards between old and young loads, so waiting for
-        // the oldest row also waits for rows requested a few steps ago)
-        double cur[kPf], nxt[kPf];
+        double cur[kPf], nxt[kPf], lc[kPf], ln[kPf];
 #pragma unroll
-        for (int u = 0; u < kPf; ++u) cur[u] = u < nrow ? F[static_cast<size_t>(i0 + 2 * u) * N2 + kc2] : 0.0;
+        for (int u = 0; u < kPf; ++u) {
+            cur[u] = u < nrow ? F[static_cast<size_t>(i0 + 2 * u) * N2 + kc2] : 0.0;
+            lc[u] = u < nrow ? Lm[static_cast<size_t>(i0 + 2 * u) * N + kc] : 0.0;
+        }
         for (int q0 = 0; q0 < nrow; q0 += kPf) {
 #pragma unroll
-            for (int u = 0; u < kPf; ++u)
-                nxt[u] = (q0 + kPf + u < nrow) ? F[static_cast<size_t>(i0 + 2 * (q0 + kPf + u)) * N2 + kc2] : 0.0;
+            for (int u = 0; u < kPf; ++u) {
+                const bool in = q0 + kPf + u < nrow;
+                const int i = i0 + 2 * (q0 + kPf + u);
+                nxt[u] = in ? F[static_cast<size_t>(i) * N2 + kc2] : 0.0;
+                ln[u] = in ? Lm[static_cast<size_t>(i) * N + kc] : 0.0;
+            }
 #pragma unroll
             for (int u = 0; u < kPf; ++u) {
                 const int q = q0 + u;
@@ -115,37 +163,20 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
                     // |F|^2 = re^2 + im^2 from the lane pair (max|F| only scales the precondition test)
                     const double f2 = f * f;
                     fmx = fmax(fmx, f2 + __shfl_xor_sync(lmask, f2, 1));
-                    const double b = __dadd_rn(lapc_diag(i, M), negk2);
-                    double d = b;
-                    double r = f;
-                    if (q > 0) {
-                        const double a = lapc_lower(i, M);
-                        if (a != 0.0) {
-                            if (fabs(a) > fabs(dprev)) ++bad;  // band_solve would have swapped rows
-                            const double l = __ddiv_rn(a, dprev);
-                            d = __dsub_rn(b, __dmul_rn(l, lapc_upper(i - 2, M)));
-                            r = __dsub_rn(f, __dmul_rn(l, rprev));
-                        }
-                    }
-                    if (fabs(d) < 1e-300) bad += 1 << 20;
+                    const double r = (q > 0) ? __dsub_rn(f, __dmul_rn(lc[u], rprev)) : f;
                     X[static_cast<size_t>(i) * N2 + kc2] = r;
-                    if (dwriter) D[static_cast<size_t>(i) * N + kc] = d;
-                    dprev = d;
                     rprev = r;
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kPf; ++u) cur[u] = nxt[u];
+            for (int u = 0; u < kPf; ++u) {
+                cur[u] = nxt[u];
+                lc[u] = ln[u];
+            }
         }
     }
-    if (w == 0 && live) {
-        s_rm2[lane] = rprev;  // chain ends at j = -2
-        s_dm2[lane] = dprev;
-    }
+    if (w == 0 && live) s_rm2[lane] = rprev;  // chain ends at j = -2
     // ---- back substitution: x_i = (r_i - c_i x_{i+2}) / d'_i  (rows i1, i1-2, ..., i0)
-    // (d' of this sweep's rows: the lane's own forward values are bit-equal to
-    // the pair's stored ones, but they are gone from registers; both lanes read D)
-    __syncwarp();
     double xnext = 0.0;
     if (nrow > 0) {
         double rr[kPf], dr[kPf], rn[kPf], dn[kPf];
@@ -200,7 +231,7 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
         if (k != 0) {
             double r0 = f0;
             if (has_m2) {  // eliminate with pivot row j = -2: f = lap[0][-2] / d'_{-2}
-                const double l = __ddiv_rn(lapc_lower(h, M), s_dm2[lane]);
+                const double l = __ddiv_rn(lapc_lower(h, M), D[static_cast<size_t>(h - 2) * N + kc]);
                 r0 = __dsub_rn(r0, __dmul_rn(l, s_rm2[lane]));
             }
             if (has_p2) {
@@ -227,7 +258,10 @@ __global__ void __launch_bounds__(128) coeff_solve_kernel(CoeffParams P) {
     // stats
     const double fm = sqrt(warp_max(live ? fmx : 0.0));
     if (lane == 0) atomic_max_nonneg(P.stats + 4 * rhs + 2, fm);
-    if (bad && dwriter) atomicAdd(P.stats + 4 * rhs + 3, static_cast<double>(bad));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const double tb = *P.tab_bad;
+        if (tb != 0.0) atomicAdd(P.stats + 4 * rhs + 3, tb);
+    }
 }
 
 // check_mean_zero (poisson.cpp:101-117): the reference computes
@@ -344,6 +378,11 @@ __global__ void __launch_bounds__(256) msin2_kernel(int M, int N, const double2*
 cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st) {
     const long long n = static_cast<long long>(M) * N;
     msin2_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(M, N, A, F);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coeff_tables(int M, int N, double* D, double* Lm, double* bad, cudaStream_t st) {
+    coeff_tables_kernel<<<(N + 31) / 32, 128, 0, st>>>(M, N, D, Lm, bad);
     return cudaGetLastError();
 }
 

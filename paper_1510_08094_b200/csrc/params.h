@@ -97,7 +97,9 @@ struct CoeffParams {
     int M, N, nrhs;
     const double2* F;
     double2* X;
-    double* D;          // scratch pivots, M x N per rhs
+    const double* D;    // per-plan pivots d'_i, M x N (coeff_tables_kernel)
+    const double* Lm;   // per-plan multipliers l_i = a_i / d'_{i-2}, M x N (0 at a chain's first row)
+    const double* tab_bad;  // [0] pivot-order violations / singular pivots found while building the tables
     double* stats;      // per rhs: [0..1] mean, [2] max|F|, [3] pivot-order violations
     const double2* z;   // Msin^-1 Msin^-1 w (check_mean_zero), length M
 };
@@ -208,6 +210,7 @@ inline int pole_glide(int m) {
 }
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
+cudaError_t launch_coeff_tables(int M, int N, double* D, double* Lm, double* bad, cudaStream_t st);
 cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 

@@ -313,7 +313,9 @@ struct sk_plan_s {
     double2* spec = nullptr;   // nrhs * cols * rows complex
     double* stats = nullptr;   // 4 * nrhs
     double2* z = nullptr;      // mean weights, M complex
-    double* D = nullptr;       // coefficient-solve pivot scratch
+    double* D = nullptr;       // coefficient solve: per-plan pivots d' (M x N), multipliers l behind them (M x N),
+                               // then one double of table-build flags (ensure_coeff_tables)
+    bool coeff_tables = false;
     double2* hF = nullptr;     // staging for host-pointer coefficient calls
     double2* hX = nullptr;
     double* hf = nullptr;      // staging for host-pointer grid calls
@@ -386,6 +388,18 @@ namespace {
 sk_status ensure(void** p, size_t bytes) {
     if (*p) return SK_OK;
     CU(cudaMalloc(p, bytes));
+    return SK_OK;
+}
+
+// The coefficient solve's data-independent elimination tables (coeff_tables_kernel).
+sk_status ensure_coeff_tables(sk_plan_t p) {
+    if (p->coeff_tables) return SK_OK;
+    const size_t mn = static_cast<size_t>(p->M) * p->N;
+    sk_status s = ensure(reinterpret_cast<void**>(&p->D), sizeof(double) * (2 * mn + 2));
+    if (s != SK_OK) return s;
+    CU(cudaMemsetAsync(p->D + 2 * mn, 0, sizeof(double) * 2, p->stream));
+    CU(sk::launch_coeff_tables(p->M, p->N, p->D, p->D + mn, p->D + 2 * mn, p->stream));
+    p->coeff_tables = true;
     return SK_OK;
 }
 
@@ -873,9 +887,10 @@ sk_status sk_solve_coeffs(sk_plan_t p, const double* F, double* X, unsigned flag
         dF = p->hF;
         dX = p->hX;
     }
-    if ((s = ensure(reinterpret_cast<void**>(&p->D), sizeof(double) * n)) != SK_OK) return s;
+    if ((s = ensure_coeff_tables(p)) != SK_OK) return s;
     CU(cudaMemsetAsync(p->stats, 0, sizeof(double) * 4 * p->nrhs, p->stream));
-    sk::CoeffParams cp{p->M, p->N, p->nrhs, dF, dX, p->D, p->stats, p->z};
+    const size_t mn1 = static_cast<size_t>(p->M) * p->N;
+    sk::CoeffParams cp{p->M, p->N, p->nrhs, dF, dX, p->D, p->D + mn1, p->D + 2 * mn1, p->stats, p->z};
     if (p->timing) CU(cudaEventRecord(p->ev[6], p->stream));
     CU(sk::launch_coeff_solve(cp, p->stream));
     if (p->timing) CU(cudaEventRecord(p->ev[7], p->stream));
@@ -1473,7 +1488,7 @@ sk_status sk_solve_grid_exact(sk_plan_t p, const double* f, double* U, double* X
     if ((s = scratch(p, 5, sizeof(double2) * mn, &t)) != SK_OK) return s;
     if ((s = scratch(p, 6, sizeof(double2) * mn, &h)) != SK_OK) return s;
     if (!dev && (s = scratch(p, 7, sizeof(double) * np, &in)) != SK_OK) return s;
-    if ((s = ensure(reinterpret_cast<void**>(&p->D), sizeof(double) * mn * p->nrhs)) != SK_OK) return s;
+    if ((s = ensure_coeff_tables(p)) != SK_OK) return s;
     double2* G = static_cast<double2*>(g);  // doubled grid, then 2D coefficients, then X
     double2* T = static_cast<double2*>(t);  // transposed intermediates, then F
     double2* H = static_cast<double2*>(h);  // u (host calls), X staging
@@ -1491,7 +1506,7 @@ sk_status sk_solve_grid_exact(sk_plan_t p, const double* f, double* U, double* X
         if ((s = xform_pass(p, true, N, M, M, M, T, N, G)) != SK_OK) return s;          // analyze: theta columns
         CU(sk::launch_msin2(M, N, G, T, p->stream));                                    // F = Msin^2 A
         double2* dX = (dev && X) ? reinterpret_cast<double2*>(X) + r * mn : G;
-        sk::CoeffParams cp{M, N, 1, T, dX, p->D, p->stats + 4 * r, p->z};
+        sk::CoeffParams cp{M, N, 1, T, dX, p->D, p->D + mn, p->D + 2 * mn, p->stats + 4 * r, p->z};
         CU(sk::launch_coeff_solve(cp, p->stream));                                      // solve
         if (!dev && X) CU(cudaMemcpyAsync(X + 2 * r * mn, dX, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
         double2* dU = dev ? reinterpret_cast<double2*>(U) + r * mn : H;

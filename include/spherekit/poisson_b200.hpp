@@ -119,6 +119,26 @@ inline std::vector<double> solve_grid(const std::vector<double>& f, int m, int n
     return u;
 }
 
+// The reference's own grid composition on the device (sk_solve_grid_exact):
+// sample_dfs -> analyze_2d -> Msin^2 -> solve (all n lambda modes) ->
+// sample_grid.  f: physical samples as in solve_grid; returns the complex
+// doubled m x n grid the reference returns (for ANY input, under-resolved
+// data included); *X, if given, receives the solution coefficients.
+inline BMCGrid solve_grid_exact(const std::vector<double>& f, int m, int n, Matrix* X = nullptr) {
+    if (m % 2 != 0 || n % 2 != 0 || m <= 0 || n <= 0) throw size_error("solve_grid_exact: sizes must be positive and even");
+    if (static_cast<long long>(f.size()) != static_cast<long long>(m / 2 + 1) * n)
+        throw size_error("solve_grid_exact: f must hold (m/2+1) x n samples");
+    sk_plan_t p = PlanCache::instance().get(m, n);
+    BMCGrid g;
+    g.rows = m;
+    g.cols = n;
+    g.v.assign(static_cast<size_t>(m) * n, complex{});
+    if (X) *X = Matrix(m, n);
+    check(sk_solve_grid_exact(p, f.data(), reinterpret_cast<double*>(g.v.data()),
+                              X ? reinterpret_cast<double*>(X->data().data()) : nullptr, SK_HOST));
+    return g;
+}
+
 // spherekit::assemble_poisson (poisson.cpp:52-86), bit-identical F.
 inline PoissonProblem assemble_poisson(const LowRankSphereFun& f, int m, int n, AssembleReport* report = nullptr) {
     if (m % 2 != 0 || n % 2 != 0 || m <= 0 || n <= 0)

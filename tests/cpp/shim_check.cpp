@@ -5,7 +5,9 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cmath>
 #include <complex>
+#include <vector>
 
 #include "spherekit/poisson.hpp"
 #include "spherekit/poisson_b200.hpp"
@@ -61,7 +63,28 @@ int main() {
             std::printf("sample_grid round trip %.3g\n", err);
             return 1;
         }
-        std::printf("assemble / analyze_2d / sample_grid ok\n");
+        // grid solves of f = cos(theta) on 16 x 8: u = -cos(theta) / 2 (l = 1 eigenfunction)
+        {
+            const int m = 16, n = 8;
+            std::vector<double> fp(static_cast<size_t>(m / 2 + 1) * n);
+            for (int p = 0; p <= m / 2; ++p)
+                for (int q = 0; q < n; ++q) fp[static_cast<size_t>(p) * n + q] = std::cos(2.0 * 3.14159265358979323846 * p / m);
+            const std::vector<double> u = b200::solve_grid(fp, m, n);
+            Matrix Xc;
+            const BMCGrid U = b200::solve_grid_exact(fp, m, n, &Xc);
+            double e1 = 0, e2 = 0;
+            for (int p = 0; p <= m / 2; ++p)
+                for (int q = 0; q < n; ++q) {
+                    const double ue = -0.5 * std::cos(2.0 * 3.14159265358979323846 * p / m);
+                    e1 = std::max(e1, std::abs(u[static_cast<size_t>(p) * n + q] - ue));
+                    e2 = std::max(e2, std::abs(U.at((m / 2 + p) % m, q) - complex(ue, 0.0)));  // doubled row j <-> theta_j = -pi + 2 pi j/m
+                }
+            if (e1 > 1e-14 || e2 > 1e-14 || Xc.rows() != m) {
+                std::printf("grid solve mismatch %.3g %.3g\n", e1, e2);
+                return 1;
+            }
+        }
+        std::printf("assemble / analyze_2d / sample_grid / grid solves ok\n");
         return 0;
     } catch (const std::runtime_error& e) {
         std::printf("device error: %s\n", e.what());

@@ -170,6 +170,39 @@ sk_status sk_sample_grid(sk_plan_t plan, int rows, int cols, const double* X, in
                          unsigned flags);
 sk_status sk_sample_dfs(sk_plan_t plan, int m, int n, const double* phys, double* grid, unsigned flags);
 
+/* Structure-preserving Gaussian elimination on a doubled BMC grid: the
+ * building blocks of the low-rank constructor (lowrank.hpp:
+ * 73-93).  The phase-1 loop of construct (lowrank.cpp:318-415, update :384-392)
+ * runs the same arithmetic on the upper half grid.
+ *   sk_ge_pivot_search  pivot_search (lowrank.cpp:84-112): complete pivoting
+ *                       over the 2x2 blocks {(lambda* - pi, theta*), (lambda*,
+ *                       theta*)}, theta* = 2 pi t/m (t = 0..m/2 ascending),
+ *                       lambda* = lambda_k (k = n/2..n-1 ascending), first
+ *                       maximal sigma_1 = max(|a+b|, |a-b|) wins; the weights
+ *                       (m_even, m_odd) = pinv_2x2(a, b, alpha) (:60-72).
+ *                       out_i = {found, t, k}; out_d = {a, b, m_even, m_odd
+ *                       (re, im each), theta_star, lambda_star}.
+ *   sk_ge_step          ge_step (lowrank.cpp:127-162): out = grid - (1/2
+ *                       m_even ce re^T + 1/2 m_odd co ro^T) for the pivot
+ *                       piv (the 10 doubles above; the node is located as
+ *                       locate_on_grid does), bit-identical to the reference.
+ *   sk_ge_run           the elimination loop with the grid resident on the
+ *                       device: max|grid| -> while it exceeds tau and steps <
+ *                       max_steps: pivot search, update (in place), max|grid|.
+ *                       resid[0] = max before the first step, resid[s + 1]
+ *                       after step s; piv_i (2 ints) / piv_d (10 doubles) per
+ *                       step as above.  The caller keeps construct's policy
+ *                       (plateau bookkeeping, rank limits) on the host.
+ * grid / out: m x n complex, row-major (BMCGrid, sphere_domain.hpp:43-58);
+ * host or device pointers by flags.  Errors: SK_ERR_SIZE (odd or non-positive
+ * sizes), SK_ERR_ARGUMENT (a pivot that is not a grid node: index_error). */
+sk_status sk_ge_pivot_search(sk_plan_t plan, int m, int n, const double* grid, double alpha, int out_i[3],
+                             double out_d[10], unsigned flags);
+sk_status sk_ge_step(sk_plan_t plan, int m, int n, const double* grid, const double piv[10], double* out,
+                     unsigned flags);
+sk_status sk_ge_run(sk_plan_t plan, int m, int n, double* grid, double alpha, double tau, int max_steps, int* nsteps,
+                    int* piv_i, double* piv_d, double* resid, unsigned flags);
+
 /* Seeded spherical-harmonic input generator (untimed helper):
  * phys = sum_{l=1..L} sum_{|m|<=l} coeffs[l*l+l+m] Y_l^m on the plan's
  * physical grid, Y as in the reference tests (helpers.hpp:18-27).

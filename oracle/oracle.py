@@ -125,6 +125,29 @@ class _Lib:
         self._call("analyze_2d", _I(m), _I(n), _ptr(grid), _ptr(X))
         return X
 
+    # ---- structure-preserving GE on a doubled grid (lowrank.hpp:73-93)
+    def pivot_search(self, grid, alpha=0.01):
+        """(t, k, a, b, m_even, m_odd, theta_star, lambda_star) or None."""
+        m, n = grid.shape
+        oi = (ctypes.c_int * 3)()
+        od = np.zeros(10)
+        self._call("pivot_search", _I(m), _I(n), _ptr(np.ascontiguousarray(grid, np.complex128)),
+                   ctypes.c_double(alpha), oi, _ptr(od))
+        if not oi[0]:
+            return None
+        c = od[:8].view(np.complex128)
+        return (int(oi[1]), int(oi[2]), complex(c[0]), complex(c[1]), complex(c[2]), complex(c[3]), float(od[8]),
+                float(od[9]))
+
+    def ge_step(self, grid, piv):
+        """piv as returned by pivot_search."""
+        m, n = grid.shape
+        t, k, a, b, me, mo, th, lam = piv
+        pd = np.array([a.real, a.imag, b.real, b.imag, me.real, me.imag, mo.real, mo.imag, th, lam])
+        out = np.zeros((m, n), np.complex128)
+        self._call("ge_step", _I(m), _I(n), _ptr(np.ascontiguousarray(grid, np.complex128)), _ptr(pd), _ptr(out))
+        return out
+
     def sample_grid(self, X, m_out, n_out):
         r, c = X.shape
         g = np.zeros((m_out, n_out), np.complex128)

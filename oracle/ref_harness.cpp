@@ -724,4 +724,45 @@ int ref_time_stock_sample(int m, int n, int kc0, int ncols, int j0, int nrows, i
     });
 }
 
+// lowrank.cpp:84-112  pivot_search (complete pivoting over theta* in [0, pi],
+// lambda* in [0, pi)).  out_i: found, t (theta* = 2 pi t / m), k (lambda index);
+// out_d: a, b, m_even, m_odd (re, im each), theta_star, lambda_star.
+int ref_pivot_search(int m, int n, const double* grid, double alpha, int* out_i, double* out_d) {
+    return guarded([&] {
+        BMCGrid g(m, n);
+        std::memcpy(g.v.data(), grid, sizeof(complex) * static_cast<size_t>(m) * n);
+        const auto p = pivot_search(g, alpha);
+        out_i[0] = p.has_value() ? 1 : 0;
+        out_i[1] = out_i[2] = -1;
+        for (int i = 0; i < 10; ++i) out_d[i] = 0.0;
+        if (!p) return;
+        out_i[1] = static_cast<int>(std::lround(p->theta_star / (kTwoPi / m)));
+        out_i[2] = static_cast<int>(std::lround((p->lambda_star + kPi) / (kTwoPi / n))) % n;
+        const complex v[4] = {p->a, p->b, p->m_even, p->m_odd};
+        for (int i = 0; i < 4; ++i) {
+            out_d[2 * i] = v[i].real();
+            out_d[2 * i + 1] = v[i].imag();
+        }
+        out_d[8] = p->theta_star;
+        out_d[9] = p->lambda_star;
+    });
+}
+
+// lowrank.cpp:127-162  ge_step; piv = a, b, m_even, m_odd, theta_star, lambda_star (as above)
+int ref_ge_step(int m, int n, const double* grid, const double* piv, double* out) {
+    return guarded([&] {
+        BMCGrid g(m, n);
+        std::memcpy(g.v.data(), grid, sizeof(complex) * static_cast<size_t>(m) * n);
+        PivotBlock p;
+        p.a = complex(piv[0], piv[1]);
+        p.b = complex(piv[2], piv[3]);
+        p.m_even = complex(piv[4], piv[5]);
+        p.m_odd = complex(piv[6], piv[7]);
+        p.theta_star = piv[8];
+        p.lambda_star = piv[9];
+        const BMCGrid r = ge_step(g, p);
+        std::memcpy(out, r.v.data(), sizeof(complex) * static_cast<size_t>(m) * n);
+    });
+}
+
 }  // extern "C"

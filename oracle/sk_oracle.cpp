@@ -643,8 +643,107 @@ int sko_synthesize_1d(int n, const double* c, int n_out, double* g) {
     });
 }
 
+// ---- structure-preserving GE on a doubled BMC grid (lowrank.hpp:73-93; the
+// phase-1 loop of construct, lowrank.cpp:318-415, runs the same update on the
+// upper half grid)
+
+// lowrank.cpp:60-72  pinv_2x2: spectral form of the eps-pseudoinverse of [a b; b a]
+static void pinv_2x2(cplx a, cplx b, double alpha, cplx& me, cplx& mo) {
+    const cplx s = a + b, d = a - b;
+    const double sp = std::abs(s), dp = std::abs(d);
+    if (sp == 0.0 && dp == 0.0) throw std::runtime_error("pinv_2x2: zero pivot matrix");
+    me = mo = cplx{};
+    if (dp == 0.0) { me = 1.0 / s; return; }
+    if (sp == 0.0) { mo = 1.0 / d; return; }
+    if (dp < alpha * sp) { me = 1.0 / s; return; }
+    if (sp < alpha * dp) { mo = 1.0 / d; return; }
+    me = 1.0 / s;
+    mo = 1.0 / d;
+}
+
+// lowrank.cpp:84-112  pivot_search: theta* = 2 pi t / m, t = 0..m/2 ascending
+// (grid rows m/2 .. m-1, then row 0 for theta* = pi), lambda index k = n/2 ..
+// n-1 ascending; sigma_1 = max(|a + b|, |a - b|) of the pair (k - n/2, k);
+// strict '>' keeps the first maximal block.
+static bool ge_pivot_search(int m, int n, const cplx* g, double alpha, int& bt, int& bk, cplx* v4) {
+    double best = 0;
+    bt = bk = -1;
+    for (int t = 0; t <= m / 2; ++t) {
+        const int j = (m / 2 + t) % m;
+        for (int k = n / 2; k < n; ++k) {
+            const cplx a = g[static_cast<size_t>(j) * n + k - n / 2], b = g[static_cast<size_t>(j) * n + k];
+            const double s1 = std::max(std::abs(a + b), std::abs(a - b));
+            if (s1 > best) {
+                best = s1;
+                bt = t;
+                bk = k;
+            }
+        }
+    }
+    if (best == 0.0) return false;
+    const int j = (m / 2 + bt) % m;
+    v4[0] = g[static_cast<size_t>(j) * n + bk - n / 2];
+    v4[1] = g[static_cast<size_t>(j) * n + bk];
+    pinv_2x2(v4[0], v4[1], alpha, v4[2], v4[3]);
+    return true;
+}
+
+// lowrank.cpp:127-162  ge_step at the grid node (js, ks): js = row of theta*,
+// ks = column of lambda*; jm = row of -theta*, km = column of lambda* - pi.
+static void ge_step(int m, int n, const cplx* g, int js, int ks, cplx me, cplx mo, cplx* out) {
+    const int jm = (m - js) % m, km = (ks + n / 2) % n;
+    std::vector<cplx> ce(m), co(m), re(n), ro(n);
+    for (int j = 0; j < m; ++j) {
+        const cplx cm = g[static_cast<size_t>(j) * n + km], cp = g[static_cast<size_t>(j) * n + ks];
+        ce[j] = cm + cp;
+        co[j] = cm - cp;
+    }
+    for (int k = 0; k < n; ++k) {
+        const cplx rp = g[static_cast<size_t>(js) * n + k], rm = g[static_cast<size_t>(jm) * n + k];
+        re[k] = rp + rm;
+        ro[k] = rp - rm;
+    }
+    const cplx de = 0.5 * me, dodd = 0.5 * mo;
+    const bool has_e = me != cplx{}, has_o = mo != cplx{};
+    for (int j = 0; j < m; ++j)
+        for (int k = 0; k < n; ++k) {
+            cplx upd{};
+            if (has_e) upd += de * ce[j] * re[k];
+            if (has_o) upd += dodd * co[j] * ro[k];
+            out[static_cast<size_t>(j) * n + k] = g[static_cast<size_t>(j) * n + k] - upd;
+        }
+}
+
 int sko_analyze_2d(int m, int n, const double* grid, double* X) {
     return guarded([&] { analyze_2d(m, n, as_c(grid), as_c(X)); });
+}
+int sko_pivot_search(int m, int n, const double* grid, double alpha, int* out_i, double* out_d) {
+    return guarded([&] {
+        int bt, bk;
+        cplx v4[4] = {};
+        const bool found = ge_pivot_search(m, n, as_c(grid), alpha, bt, bk, v4);
+        out_i[0] = found ? 1 : 0;
+        out_i[1] = found ? bt : -1;
+        out_i[2] = found ? bk : -1;
+        for (int i = 0; i < 10; ++i) out_d[i] = 0.0;
+        if (!found) return;
+        for (int i = 0; i < 4; ++i) {
+            out_d[2 * i] = v4[i].real();
+            out_d[2 * i + 1] = v4[i].imag();
+        }
+        const double twopi = 6.283185307179586476925286766559;
+        out_d[8] = twopi * bt / m;                                // lowrank.cpp:106
+        out_d[9] = -3.14159265358979323846 + twopi * bk / n;      // BMCGrid::lambda, sphere_domain.hpp:55
+    });
+}
+int sko_ge_step(int m, int n, const double* grid, const double* piv, double* out) {
+    return guarded([&] {
+        const double twopi = 6.283185307179586476925286766559, pi = 3.14159265358979323846;
+        // locate_on_grid (lowrank.cpp:116-123)
+        const long js = std::lround((piv[8] + pi) / (twopi / m)), ks = std::lround((piv[9] + pi) / (twopi / n));
+        ge_step(m, n, as_c(grid), static_cast<int>(((js % m) + m) % m), static_cast<int>(((ks % n) + n) % n),
+                cplx(piv[4], piv[5]), cplx(piv[6], piv[7]), reinterpret_cast<cplx*>(out));
+    });
 }
 
 int sko_sample_grid(int rows, int cols, const double* X, int m_out, int n_out, double* grid) {

@@ -5,8 +5,9 @@ include/sk_poisson.h); this package is the host-side mirror of the
 reference's spherekit Poisson interface (poisson.hpp) on top of it.
 """
 from .poisson import (  # noqa: F401
-    AssembleReport, BenchRow, DeviceError, LowRankSphereFun, Plan, PoissonProblem, PoissonSolution, ResidualReport,
-    UnsupportedError, analyze_2d, assemble_poisson, bench_poisson, integration_weights, precondition_error, residual,
+    AssembleReport, BenchRow, DeviceError, LowRankSphereFun, PivotBlock, Plan, PoissonProblem, PoissonSolution, ResidualReport,
+    UnsupportedError, analyze_2d, assemble_poisson, bench_poisson, ge_step, integration_weights, pivot_search,
+    precondition_error, residual,
     sample_dfs, sample_grid, size_error, solve, solve_grid, solve_grid_exact, structure_error, coefficients_from_half,
     rhs_coefficients)
 

@@ -33,7 +33,7 @@ EXPORTS = [
     "sk_stage_lambda_fwd_peer", "sk_stage_theta_peer", "sk_device_alloc", "sk_device_free", "sk_ipc_handle",
     "sk_ipc_open", "sk_ipc_close", "sk_assemble", "sk_analyze_2d", "sk_sample_grid", "sk_sample_dfs",
     "sk_solve_grid_exact", "sk_ipc_event_create", "sk_ipc_event_open", "sk_event_destroy", "sk_event_record",
-    "sk_stream_wait_event", "sk_stage_stats",
+    "sk_stream_wait_event", "sk_stage_stats", "sk_ge_pivot_search", "sk_ge_step", "sk_ge_run",
 ]
 
 
@@ -120,6 +120,9 @@ def load() -> ctypes.CDLL:
         "sk_event_record": (I, [P, P]),
         "sk_stream_wait_event": (I, [P, P]),
         "sk_stage_stats": (I, [P, D]),
+        "sk_ge_pivot_search": (I, [P, I, I, P, ctypes.c_double, IP, D, U]),
+        "sk_ge_step": (I, [P, I, I, P, D, P, U]),
+        "sk_ge_run": (I, [P, I, I, P, ctypes.c_double, ctypes.c_double, I, IP, IP, D, D, U]),
         "sk_last_error": (ctypes.c_char_p, []),
         "sk_version": (ctypes.c_char_p, []),
     }

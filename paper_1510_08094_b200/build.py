@@ -27,6 +27,7 @@ UNITS = [
     ("lambda_duo.cu", []),
     ("coeff_kernels.cu", ["--fmad=false"]),
     ("assemble_kernels.cu", ["--fmad=false"]),
+    ("ge_kernels.cu", ["--fmad=false"]),
     ("transforms.cu", []),
     ("sk_poisson.cu", []),
 ]

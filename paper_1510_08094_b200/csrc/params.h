@@ -211,6 +211,15 @@ inline int pole_glide(int m) {
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st);
 cudaError_t launch_coeff_solve(const CoeffParams& P, cudaStream_t st);
 cudaError_t launch_coeff_tables(int M, int N, double* D, double* Lm, double* bad, cudaStream_t st);
+// structure-preserving GE on a doubled grid (ge_kernels.cu).  scratch: ge_scratch_bytes(m, n) device bytes;
+// doubles [0..5] of it receive the search result (sigma_1, candidate index t (n/2) + k - n/2 or -1, a, b),
+// double [8] the max |residual| of a step / of launch_ge_maxabs.
+constexpr int kGeParts = 2048;
+size_t ge_scratch_bytes(int m, int n);
+cudaError_t launch_ge_search(int m, int n, const double2* g, void* scratch, cudaStream_t st);
+cudaError_t launch_ge_step(int m, int n, const double2* g, int js, int ks, double2 de, double2 dodd, int has_e, int has_o,
+                           double2* out, void* scratch, bool want_max, cudaStream_t st);
+cudaError_t launch_ge_maxabs(int m, int n, const double2* g, void* scratch, cudaStream_t st);
 cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 

@@ -1397,6 +1397,163 @@ sk_status sk_assemble(sk_plan_t p, int K, int mf, int nf, const double* d, const
     return SK_OK;
 }
 
+// ---- structure-preserving GE on a doubled grid (ge_kernels.cu)
+namespace {
+
+using cplx = std::complex<double>;
+
+// lowrank.cpp:60-72 (host: std::complex division as the reference's compiler emits it)
+bool pinv_2x2_host(cplx a, cplx b, double alpha, cplx& me, cplx& mo) {
+    const cplx s = a + b, d = a - b;
+    const double sp = std::abs(s), dp = std::abs(d);
+    me = mo = cplx{};
+    if (sp == 0.0 && dp == 0.0) return false;
+    if (dp == 0.0) { me = 1.0 / s; return true; }
+    if (sp == 0.0) { mo = 1.0 / d; return true; }
+    if (dp < alpha * sp) { me = 1.0 / s; return true; }
+    if (sp < alpha * dp) { mo = 1.0 / d; return true; }
+    me = 1.0 / s;
+    mo = 1.0 / d;
+    return true;
+}
+
+constexpr double kPiRef = 3.141592653589793238462643383279502884;  // types.hpp:12-13
+constexpr double kTwoPiRef = 2.0 * kPiRef;
+
+sk_status ge_check_sizes(int m, int n) {
+    if (m <= 0 || n <= 0 || (m & 1) || (n & 1)) return fail(SK_ERR_SIZE, "BMCGrid: sample counts must be positive and even");
+    return SK_OK;
+}
+
+// search on the device grid g; fills out_i / out_d (host); returns found
+sk_status ge_search_dev(sk_plan_t p, int m, int n, const double2* g, void* scr, double alpha, int out_i[3],
+                        double out_d[10]) {
+    CU(sk::launch_ge_search(m, n, g, scr, p->stream));
+    double h[6];
+    CU(cudaMemcpyAsync(h, scr, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int i = 0; i < 10; ++i) out_d[i] = 0.0;
+    out_i[0] = 0;
+    out_i[1] = out_i[2] = -1;
+    if (h[1] < 0.0 || !(h[0] > 0.0)) return SK_OK;  // best == 0: no pivot (lowrank.cpp:103)
+    const long long c = static_cast<long long>(h[1]);
+    const int t = static_cast<int>(c / (n / 2)), k = static_cast<int>(c % (n / 2)) + n / 2;
+    const cplx a(h[2], h[3]), b(h[4], h[5]);
+    cplx me, mo;
+    if (!pinv_2x2_host(a, b, alpha, me, mo)) return fail(SK_ERR_SINGULAR, "pinv_2x2: zero pivot matrix");
+    out_i[0] = 1;
+    out_i[1] = t;
+    out_i[2] = k;
+    const cplx v[4] = {a, b, me, mo};
+    for (int i = 0; i < 4; ++i) {
+        out_d[2 * i] = v[i].real();
+        out_d[2 * i + 1] = v[i].imag();
+    }
+    out_d[8] = kTwoPiRef * t / m;             // lowrank.cpp:106
+    out_d[9] = -kPiRef + kTwoPiRef * k / n;   // BMCGrid::lambda, sphere_domain.hpp:55
+    return SK_OK;
+}
+
+// locate_on_grid (lowrank.cpp:116-123)
+sk_status ge_locate(double x, double step, int count, int* idx) {
+    const double t = (x + kPiRef) / step;
+    const long i = std::lround(t);
+    if (std::abs(t - static_cast<double>(i)) > 1e-9) return fail(SK_ERR_ARGUMENT, "ge_step: pivot coordinate is not a grid node");
+    *idx = static_cast<int>(((i % count) + count) % count);
+    return SK_OK;
+}
+
+sk_status ge_step_dev(sk_plan_t p, int m, int n, const double2* g, const double piv[10], double2* out, void* scr,
+                      bool want_max) {
+    int js = 0, ks = 0;
+    sk_status s = ge_locate(piv[8], kTwoPiRef / m, m, &js);
+    if (s != SK_OK) return s;
+    if ((s = ge_locate(piv[9], kTwoPiRef / n, n, &ks)) != SK_OK) return s;
+    const cplx me(piv[4], piv[5]), mo(piv[6], piv[7]);
+    const cplx de = 0.5 * me, dodd = 0.5 * mo;  // lowrank.cpp:147-148
+    CU(sk::launch_ge_step(m, n, g, js, ks, make_double2(de.real(), de.imag()), make_double2(dodd.real(), dodd.imag()),
+                          me != cplx{} ? 1 : 0, mo != cplx{} ? 1 : 0, out, scr, want_max, p->stream));
+    return SK_OK;
+}
+
+}  // namespace
+
+sk_status sk_ge_pivot_search(sk_plan_t p, int m, int n, const double* grid, double alpha, int out_i[3], double out_d[10],
+                             unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!grid || !out_i || !out_d) return fail(SK_ERR_ARGUMENT, "null argument");
+    if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
+    const void* g = nullptr;
+    void* scr = nullptr;
+    if ((s = stage_in(p, grid, sizeof(double2) * m * static_cast<size_t>(n), flags, 0, &g)) != SK_OK) return s;
+    if ((s = scratch(p, 2, sk::ge_scratch_bytes(m, n), &scr)) != SK_OK) return s;
+    p->last_launches = 2;
+    return ge_search_dev(p, m, n, static_cast<const double2*>(g), scr, alpha, out_i, out_d);
+}
+
+sk_status sk_ge_step(sk_plan_t p, int m, int n, const double* grid, const double piv[10], double* out, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!grid || !piv || !out) return fail(SK_ERR_ARGUMENT, "null argument");
+    if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
+    const size_t bytes = sizeof(double2) * m * static_cast<size_t>(n);
+    const void* g = nullptr;
+    void *scr = nullptr, *o = out;
+    if ((s = stage_in(p, grid, bytes, flags, 0, &g)) != SK_OK) return s;
+    if ((s = scratch(p, 2, sk::ge_scratch_bytes(m, n), &scr)) != SK_OK) return s;
+    if (!(flags & SK_DEVICE) && (s = scratch(p, 1, bytes, &o)) != SK_OK) return s;
+    if ((s = ge_step_dev(p, m, n, static_cast<const double2*>(g), piv, static_cast<double2*>(o), scr, false)) != SK_OK)
+        return s;
+    p->last_launches = 2;
+    if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(out, o, bytes, cudaMemcpyDeviceToHost, p->stream));
+    if (!((flags & SK_ASYNC) && (flags & SK_DEVICE))) CU(cudaStreamSynchronize(p->stream));
+    return SK_OK;
+}
+
+sk_status sk_ge_run(sk_plan_t p, int m, int n, double* grid, double alpha, double tau, int max_steps, int* nsteps,
+                    int* piv_i, double* piv_d, double* resid, unsigned flags) {
+    sk_status s = check_plan(p);
+    if (s != SK_OK) return s;
+    if (!grid || !nsteps || !piv_i || !piv_d || !resid || max_steps < 0) return fail(SK_ERR_ARGUMENT, "bad argument");
+    if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
+    const size_t bytes = sizeof(double2) * m * static_cast<size_t>(n);
+    void *g = grid, *scr = nullptr;
+    if (!(flags & SK_DEVICE)) {
+        if ((s = scratch(p, 0, bytes, &g)) != SK_OK) return s;
+        CU(cudaMemcpyAsync(g, grid, bytes, cudaMemcpyHostToDevice, p->stream));
+    }
+    if ((s = scratch(p, 2, sk::ge_scratch_bytes(m, n), &scr)) != SK_OK) return s;
+    double2* gd = static_cast<double2*>(g);
+    double* mx = static_cast<double*>(scr) + 8;
+    auto read_max = [&](double* v) -> sk_status {
+        CU(cudaMemcpyAsync(v, mx, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        return SK_OK;
+    };
+    CU(sk::launch_ge_maxabs(m, n, gd, scr, p->stream));
+    if ((s = read_max(&resid[0])) != SK_OK) return s;
+    int step = 0;
+    p->last_launches = 1;
+    while (step < max_steps && resid[step] > tau) {
+        int oi[3];
+        if ((s = ge_search_dev(p, m, n, gd, scr, alpha, oi, piv_d + 10 * step)) != SK_OK) return s;
+        if (!oi[0]) break;  // the residual is exactly zero on the pivot set
+        piv_i[2 * step] = oi[1];
+        piv_i[2 * step + 1] = oi[2];
+        if ((s = ge_step_dev(p, m, n, gd, piv_d + 10 * step, gd, scr, true)) != SK_OK) return s;
+        if ((s = read_max(&resid[step + 1])) != SK_OK) return s;
+        p->last_launches += 4;
+        ++step;
+    }
+    *nsteps = step;
+    if (!(flags & SK_DEVICE)) {
+        CU(cudaMemcpyAsync(grid, g, bytes, cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+    }
+    return SK_OK;
+}
+
 sk_status sk_analyze_2d(sk_plan_t p, int m, int n, const double* grid, double* X, unsigned flags) {
     sk_status s = check_plan(p);
     if (s != SK_OK) return s;

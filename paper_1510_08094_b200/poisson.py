@@ -362,6 +362,57 @@ class Plan:
         _lib.check(self.lib.sk_sample_dfs(self._h, m, n, _ptr(phys), _ptr(grid), _lib.SK_DEVICE if dev else _lib.SK_HOST))
         return grid
 
+    # -- structure-preserving GE on a doubled grid (lowrank.hpp:73-93)
+    def pivot_search(self, grid, alpha: float = 0.01):
+        """pivot_search (lowrank.cpp:84-112) of an m x n complex doubled grid:
+        a PivotBlock, or None where the grid vanishes on the pivot set."""
+        dev = _is_device(grid)
+        m, n = (int(x) for x in grid.shape[-2:])
+        if not dev:
+            grid = np.ascontiguousarray(grid, dtype=np.complex128)
+        self._follow_torch(grid)
+        oi = (ctypes.c_int * 3)()
+        od = (ctypes.c_double * 10)()
+        _lib.check(self.lib.sk_ge_pivot_search(self._h, m, n, _ptr(grid), float(alpha), oi, od,
+                                               _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return PivotBlock._from(oi, od) if oi[0] else None
+
+    def ge_step(self, grid, p: "PivotBlock", out=None):
+        """ge_step (lowrank.cpp:127-162): grid minus the rank-<=2 update of
+        pivot p, bit-identical to the reference."""
+        dev = _is_device(grid)
+        m, n = (int(x) for x in grid.shape[-2:])
+        if dev:
+            import torch
+            out = torch.empty_like(grid) if out is None else out
+        else:
+            grid = np.ascontiguousarray(grid, dtype=np.complex128)
+            out = np.empty((m, n), np.complex128) if out is None else out
+        self._follow_torch(grid)
+        pd = (ctypes.c_double * 10)(*p._doubles())
+        _lib.check(self.lib.sk_ge_step(self._h, m, n, _ptr(grid), pd, _ptr(out), _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        return out
+
+    def ge_run(self, grid, tau: float, alpha: float = 0.01, max_steps: int = 1024):
+        """The elimination loop with the grid resident on the device (in place
+        for device tensors; host arrays are copied in and back): returns
+        (pivots, resid) with resid[0] = max|grid| before the first step and
+        resid[s + 1] after step s."""
+        dev = _is_device(grid)
+        m, n = (int(x) for x in grid.shape[-2:])
+        if not dev and not (isinstance(grid, np.ndarray) and grid.dtype == np.complex128 and grid.flags.c_contiguous):
+            raise size_error("ge_run: a C-contiguous complex128 array is updated in place")
+        self._follow_torch(grid)
+        ns = ctypes.c_int(0)
+        pi = (ctypes.c_int * (2 * max_steps))()
+        pd = (ctypes.c_double * (10 * max_steps))()
+        rs = (ctypes.c_double * (max_steps + 1))()
+        _lib.check(self.lib.sk_ge_run(self._h, m, n, _ptr(grid), float(alpha), float(tau), int(max_steps), ctypes.byref(ns),
+                                      pi, pd, rs, _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        k = ns.value
+        piv = [PivotBlock._from((1, pi[2 * i], pi[2 * i + 1]), pd[10 * i: 10 * i + 10]) for i in range(k)]
+        return piv, [rs[i] for i in range(k + 1)]
+
     def _check_shape(self, a, tail):
         shp = tuple(a.shape)
         if shp[-2:] != tuple(tail):
@@ -512,6 +563,33 @@ def bench_poisson(sizes, reps: Optional[int] = None):
     return rows
 
 
+@dataclasses.dataclass
+class PivotBlock:
+    """One 2x2 GE pivot (lowrank.hpp:19-26): (lambda_star, theta_star) pairs
+    with (lambda_star - pi, -theta_star); a, b the grid values at the pair,
+    (m_even, m_odd) the spectral form of the eps-pseudoinverse of [a b; b a].
+    t, k: the node indices (theta_star = 2 pi t/m, lambda_star = lambda_k)."""
+    lambda_star: float
+    theta_star: float
+    a: complex
+    b: complex
+    m_even: complex
+    m_odd: complex
+    t: int = -1
+    k: int = -1
+
+    @classmethod
+    def _from(cls, oi, od):
+        c = [complex(od[2 * i], od[2 * i + 1]) for i in range(4)]
+        return cls(float(od[9]), float(od[8]), c[0], c[1], c[2], c[3], int(oi[1]), int(oi[2]))
+
+    def _doubles(self):
+        v = []
+        for z in (self.a, self.b, self.m_even, self.m_odd):
+            v += [z.real, z.imag]
+        return v + [self.theta_star, self.lambda_star]
+
+
 # ------------------------------------------------- assemble / Fourier layer
 @dataclasses.dataclass
 class LowRankSphereFun:
@@ -562,6 +640,16 @@ def sample_grid(X, m: int, n: int) -> np.ndarray:
     """spherekit::sample_grid (fourier.cpp:190-209): coefficients -> m x n
     grid values, zero-padding or truncating the modes."""
     return _xplan().sample_grid(X, m, n)
+
+
+def pivot_search(grid, alpha: float = 0.01):
+    """spherekit::pivot_search (lowrank.hpp:89)."""
+    return _xplan().pivot_search(grid, alpha)
+
+
+def ge_step(grid, p: PivotBlock) -> np.ndarray:
+    """spherekit::ge_step (lowrank.hpp:93)."""
+    return _xplan().ge_step(grid, p)
 
 
 def sample_dfs(phys, m: Optional[int] = None) -> np.ndarray:

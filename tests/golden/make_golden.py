@@ -35,7 +35,7 @@ def main(only=None):
     R = Reference()
     O = Oracle()
     if only:
-        {"lowrank": lowrank_fixtures, "transforms": transform_fixtures}[only](R)
+        {"lowrank": lowrank_fixtures, "transforms": transform_fixtures, "ge": ge_fixtures}[only](R)
         return
 
     # test_poisson.cpp:53-67 — l = 1 eigenfunction cos(theta), 64 x 64
@@ -109,6 +109,7 @@ def main(only=None):
 
     lowrank_fixtures(R)
     transform_fixtures(R)
+    ge_fixtures(R)
 
 
 def lowrank_fixtures(R):
@@ -143,6 +144,77 @@ def transform_fixtures(R):
     for m, n in [(8, 6), (20, 16)]:
         phys = rng.standard_normal((m // 2 + 1, n))
         save(f"dfs_double_{m}x{n}", phys=phys, grid=R.sample_dfs_phys(phys, m))
+
+
+def ge_grids():
+    """Doubled BMC grids for the GE building blocks, after the reference's
+    own test constructions (test_lowrank.cpp:68-190, acceptance_main.cpp:
+    262-285): a rank-1 product, symmetrised trigonometric sums, cos(theta)
+    (pivot ties on the pole rows), and seeded exact-rank BMC functions with
+    complex coefficients."""
+    def grid(m, n, fn):
+        th = -np.pi + 2 * np.pi * np.arange(m) / m
+        la = -np.pi + 2 * np.pi * np.arange(n) / n
+        T, L = np.meshgrid(th, la, indexing="ij")
+        return np.asarray(fn(T, L), dtype=np.complex128)
+
+    def bmc(g):  # g(-theta, lambda + pi) = g(theta, lambda), written as the reference's tests do
+        m, n = g.shape
+        out = g.copy()
+        for j in range(m):
+            for k in range(n):
+                out[(m - j) % m, (k + n // 2) % n] = out[j, k]
+        return out
+
+    def rand_rank(m, n, K, seed):
+        r = np.random.default_rng(seed)
+
+        def f(T, L):
+            acc = 0
+            for _ in range(K):
+                p = int(r.integers(0, 2))
+                a = int(r.integers(1, 6))
+                b = 2 * int(r.integers(0, 4)) + p
+                c = r.normal() + 1j * r.normal()
+                acc = acc + c * (np.cos(a * T) if p == 0 else np.sin(a * T)) * np.exp(1j * b * L)
+            return acc
+        return bmc(grid(m, n, f))
+
+    return {
+        "rank1_32x32": grid(32, 32, lambda T, L: (np.cos(2 * T) + 2.0) * (np.sin(2 * L) + 0.4)),
+        "sym_32x48": bmc(grid(32, 48, lambda T, L: np.cos(2 * T) * np.cos(2 * L) + np.sin(T) * np.sin(L)
+                              + 0.3 * np.sin(2 * T) * np.sin(3 * L))),
+        "sym4_32x32": bmc(grid(32, 32, lambda T, L: np.cos(2 * T) * np.cos(2 * L) + np.sin(T) * np.sin(L)
+                               + 0.25 * np.sin(2 * T) * np.sin(4 * L) + 0.4)),
+        "cos_theta_16x16": grid(16, 16, lambda T, L: np.cos(T) + 0 * L),
+        "rand6_32x32": rand_rank(32, 32, 6, 515),
+        "rand12_64x96": rand_rank(64, 96, 12, 7),
+    }
+
+
+def ge_fixtures(R):
+    """pivot_search (lowrank.cpp:84-112) and ge_step (:127-162) of the
+    reference, stepped until the residual is at rounding level (at most 10
+    steps): per step the pivot (t, k, a, b, m_even, m_odd, theta*, lambda*)
+    and, for the first two steps and the last, the updated grid."""
+    for name, g in ge_grids().items():
+        arrs = {"grid": g}
+        cur, scale = g, np.abs(g).max()
+        piv_i, piv_d, keep = [], [], []
+        for step in range(10):
+            p = R.pivot_search(cur)
+            if p is None:
+                break
+            t, k, a, b, me, mo, th, lam = p
+            piv_i.append([t, k])
+            piv_d.append([a.real, a.imag, b.real, b.imag, me.real, me.imag, mo.real, mo.imag, th, lam])
+            cur = R.ge_step(cur, p)
+            if step < 2:
+                arrs[f"after_{step}"] = cur
+            if np.abs(cur).max() < 1e-13 * scale:
+                break
+        arrs.update(piv_i=np.array(piv_i, np.int64), piv_d=np.array(piv_d), final=cur)
+        save(f"ge_{name}", **arrs)
 
 
 if __name__ == "__main__":

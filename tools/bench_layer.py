@@ -144,6 +144,35 @@ def main():
                "dof_per_s": M * N / 2 / (best * 1e-3)}
         out.append(rec)
         plan.close()
+    # GE building blocks (lowrank.hpp:73-93) on a doubled grid resident on the device:
+    # one step = pivot search (reads the upper half: 16 (m/2+1) n bytes) + cross + update
+    # (reads and writes the grid: 32 m n bytes, max|.| fused); CPU reference on a smaller grid
+    xp = Plan(8, 4)
+    for m, n in [(4096, 4096), (2048, 2048)]:
+        grid0 = crand(m, n)
+        jm = (m - torch.arange(m, device=dev)) % m
+        km = (torch.arange(n, device=dev) + n // 2) % n
+        grid0 = 0.5 * (grid0 + grid0[jm][:, km])  # BMC-symmetric noise (full rank: every step does work)
+        grid = grid0.clone()
+        out_g = torch.empty_like(grid)
+        p = xp.pivot_search(grid)
+        bs, ms_ = timed(xp, lambda: xp.pivot_search(grid))
+        bu, mu_ = timed(xp, lambda: xp.ge_step(grid, p, out_g))
+        steps = 16
+        t0 = time.perf_counter()
+        piv, resid = xp.ge_run(grid, tau=0.0, max_steps=steps)
+        torch.cuda.synchronize()
+        run_ms = 1e3 * (time.perf_counter() - t0) / max(len(piv), 1)
+        by = 16.0 * (m // 2 + 1) * n + 32.0 * m * n
+        rec = {"op": "ge_step (pivot_search + update)", "m": m, "n": n, "search_ms": bs, "update_ms": bu,
+               "run_ms_per_step": run_ms, "steps": len(piv), "achieved_gbs": by / (bs + bu) / 1e6, "peak_gbs": pk,
+               "frac": by / (bs + bu) / 1e6 / pk, "update_gbs": 32.0 * m * n / bu / 1e6}
+        if R is not None and m * n <= 1 << 22:
+            gn = grid0.cpu().numpy()
+            pr = R.pivot_search(gn)
+            rec["cpu_reference_ms"] = 1e3 * (cpu_time(lambda: R.pivot_search(gn)) + cpu_time(lambda: R.ge_step(gn, pr)))
+        out.append(rec)
+    xp.close()
     for r in out:
         print(json.dumps(r))
 

@@ -30,6 +30,7 @@
 #include <string>
 #include <thread>
 #include <tuple>
+#include <optional>
 #include <vector>
 
 #include "sk_poisson.h"
@@ -206,6 +207,36 @@ inline BMCGrid sample_dfs(const std::vector<double>& phys, int m, int n) {
     BMCGrid g = make_grid(m, n);
     check(sk_sample_dfs(transform_plan(), m, n, phys.data(), reinterpret_cast<double*>(g.v.data()), SK_HOST));
     return g;
+}
+
+// spherekit::pivot_search (lowrank.hpp:89, lowrank.cpp:84-112)
+inline std::optional<PivotBlock> pivot_search(const BMCGrid& residual, double alpha = 0.01) {
+    int oi[3];
+    double od[10];
+    check(sk_ge_pivot_search(transform_plan(), residual.rows, residual.cols,
+                             reinterpret_cast<const double*>(residual.v.data()), alpha, oi, od, SK_HOST));
+    if (!oi[0]) return std::nullopt;
+    PivotBlock p;
+    p.a = complex(od[0], od[1]);
+    p.b = complex(od[2], od[3]);
+    p.m_even = complex(od[4], od[5]);
+    p.m_odd = complex(od[6], od[7]);
+    p.theta_star = od[8];
+    p.lambda_star = od[9];
+    return p;
+}
+
+// spherekit::ge_step (lowrank.hpp:93, lowrank.cpp:127-162), bit-identical
+inline BMCGrid ge_step(const BMCGrid& residual, const PivotBlock& p) {
+    const double piv[10] = {p.a.real(),     p.a.imag(),     p.b.real(),   p.b.imag(),   p.m_even.real(),
+                            p.m_even.imag(), p.m_odd.real(), p.m_odd.imag(), p.theta_star, p.lambda_star};
+    BMCGrid out = make_grid(residual.rows, residual.cols);
+    const sk_status s = sk_ge_step(transform_plan(), residual.rows, residual.cols,
+                                   reinterpret_cast<const double*>(residual.v.data()), piv,
+                                   reinterpret_cast<double*>(out.v.data()), SK_HOST);
+    if (s == SK_ERR_ARGUMENT) throw index_error(sk_last_error());  // a pivot that is not a grid node
+    check(s);
+    return out;
 }
 
 }  // namespace b200

@@ -84,7 +84,35 @@ int main() {
                 return 1;
             }
         }
-        std::printf("assemble / analyze_2d / sample_grid / grid solves ok\n");
+        // pivot_search + ge_step annihilate a rank-1 BMC function (test_lowrank.cpp:87-96)
+        {
+            BMCGrid r1 = b200::make_grid(32, 32);
+            for (int j = 0; j < 32; ++j)
+                for (int k = 0; k < 32; ++k)
+                    r1.at(j, k) = (std::cos(2 * r1.theta(j)) + 2.0) * (std::sin(2 * r1.lambda(k)) + 0.4);
+            const auto p = b200::pivot_search(r1);
+            if (!p) {
+                std::printf("no pivot\n");
+                return 1;
+            }
+            const BMCGrid z = b200::ge_step(r1, *p);
+            double mx = 0, sc = 0;
+            for (size_t i = 0; i < z.v.size(); ++i) {
+                mx = std::max(mx, std::abs(z.v[i]));
+                sc = std::max(sc, std::abs(r1.v[i]));
+            }
+            bool threw = false;
+            try {
+                b200::ge_step(r1, PivotBlock{0.123, 0.456, 1.0, 0.5, 1.0, 1.0});
+            } catch (const index_error&) {
+                threw = true;
+            }
+            if (mx > 1e-14 * sc || !threw) {
+                std::printf("ge mismatch %.3g %d\n", mx / sc, int(threw));
+                return 1;
+            }
+        }
+        std::printf("assemble / analyze_2d / sample_grid / grid solves / ge ok\n");
         return 0;
     } catch (const std::runtime_error& e) {
         std::printf("device error: %s\n", e.what());

@@ -39,4 +39,4 @@ def test_cpp_shim_on_device():
         pytest.skip("tests/cpp/_build/shim_check was not built (needs the reference headers)")
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "assemble / analyze_2d / sample_grid / grid solves ok" in r.stdout
+    assert "assemble / analyze_2d / sample_grid / grid solves / ge ok" in r.stdout

@@ -127,30 +127,46 @@ __global__ void __launch_bounds__(256) ge_cross_kernel(int m, int n, const doubl
     }
 }
 
-// out = g - upd over the whole grid; mx (may be null) receives max |out|
+// out = g - upd over the whole grid; mx (may be null) receives max |out|.
+// One grid row per blockIdx.y trip (its column factors loaded once), four
+// independent entries per thread and trip.
 __global__ void __launch_bounds__(256) ge_update_kernel(int m, int n, const double2* g,  // g may be out (in place)
                                                         const double2* __restrict__ dce, const double2* __restrict__ dco,
                                                         const double2* __restrict__ re, const double2* __restrict__ ro,
                                                         int has_e, int has_o, double2* out, double* mx) {
     __shared__ double red[64];
-    const long long total = static_cast<long long>(m) * n;
     double lm = 0.0;
-    for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(idx / n), k = static_cast<int>(idx - static_cast<long long>(j) * n);
-        double2 upd = make_double2(0.0, 0.0);
-        if (has_e) {
-            const double2 t = cmul_ref(dce[j], re[k]);
-            upd = make_double2(upd.x + t.x, upd.y + t.y);
+    constexpr int kU = 4;
+    for (int j = blockIdx.y; j < m; j += gridDim.y) {
+        const double2 ce = dce[j], co = dco[j];
+        const double2* gr = g + static_cast<size_t>(j) * n;
+        double2* orow = out + static_cast<size_t>(j) * n;
+        for (int k0 = blockIdx.x * blockDim.x * kU + threadIdx.x; k0 < n; k0 += gridDim.x * blockDim.x * kU) {
+            double2 v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int k = k0 + u * blockDim.x;
+                v[u] = k < n ? gr[k] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int k = k0 + u * blockDim.x;
+                if (k < n) {
+                    double2 upd = make_double2(0.0, 0.0);
+                    if (has_e) {
+                        const double2 t = cmul_ref(ce, re[k]);
+                        upd = make_double2(upd.x + t.x, upd.y + t.y);
+                    }
+                    if (has_o) {
+                        const double2 t = cmul_ref(co, ro[k]);
+                        upd = make_double2(upd.x + t.x, upd.y + t.y);
+                    }
+                    const double2 r = make_double2(v[u].x - upd.x, v[u].y - upd.y);
+                    orow[k] = r;
+                    if (mx) lm = fmax(lm, hypot(r.x, r.y));
+                }
+            }
         }
-        if (has_o) {
-            const double2 t = cmul_ref(dco[j], ro[k]);
-            upd = make_double2(upd.x + t.x, upd.y + t.y);
-        }
-        const double2 v = g[idx];
-        const double2 r = make_double2(v.x - upd.x, v.y - upd.y);
-        out[idx] = r;
-        if (mx) lm = fmax(lm, hypot(r.x, r.y));
     }
     if (mx) {
         lm = block_max(lm, red);
@@ -199,8 +215,9 @@ cudaError_t launch_ge_step(int m, int n, const double2* g, int js, int ks, doubl
     const int mn = m > n ? m : n;
     ge_cross_kernel<<<(mn + 255) / 256, 256, 0, st>>>(m, n, g, js, ks, de, dodd, dce, dco, re, ro);
     if (want_max) cudaMemsetAsync(mx, 0, sizeof(double), st);
-    ge_update_kernel<<<ge_blocks(static_cast<long long>(m) * n), 256, 0, st>>>(m, n, g, dce, dco, re, ro, has_e, has_o, out,
-                                                                              want_max ? mx : nullptr);
+    const int bx = (n + 1023) / 1024;
+    const int by = m < 65535 / 1 ? (m < 2048 ? m : 2048) : 2048;
+    ge_update_kernel<<<dim3(bx, by), 256, 0, st>>>(m, n, g, dce, dco, re, ro, has_e, has_o, out, want_max ? mx : nullptr);
     return cudaGetLastError();
 }
 

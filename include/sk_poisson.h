@@ -70,6 +70,7 @@ typedef struct sk_plan_s* sk_plan_t;
 /* flags for data arguments */
 #define SK_HOST 0u     /* pointers are host memory (copies inside the call)   */
 #define SK_DEVICE 1u   /* pointers are device memory on the plan's device    */
+#define SK_GE_HALF 8u  /* sk_ge_*: the grid is the (m/2+1) x n upper half (below)    */
 #define SK_ASYNC 2u    /* do not synchronise before returning.  Device
                           pointers: work is queued on the plan stream.  Host
                           pointers (sk_solve_grid): the solve is pipelined —
@@ -194,7 +195,12 @@ sk_status sk_sample_dfs(sk_plan_t plan, int m, int n, const double* phys, double
  *                       step as above.  The caller keeps construct's policy
  *                       (plateau bookkeeping, rank limits) on the host.
  * grid / out: m x n complex, row-major (BMCGrid, sphere_domain.hpp:43-58);
- * host or device pointers by flags.  Errors: SK_ERR_SIZE (odd or non-positive
+ * host or device pointers by flags.  With SK_GE_HALF the arrays hold only the
+ * upper half grid, (m/2+1) x n with row i <-> theta_i = 2 pi i/m, exactly as
+ * construct's phase 1 keeps it (lowrank.cpp:246-252: the lower half is implied
+ * by the glide symmetry; the row of -theta* is the pivot row shifted by pi in
+ * lambda, :370-378) - half the bytes per step, the same pivots and the same
+ * bits on the stored rows for BMC-symmetric data.  Errors: SK_ERR_SIZE (odd or non-positive
  * sizes), SK_ERR_ARGUMENT (a pivot that is not a grid node: index_error). */
 sk_status sk_ge_pivot_search(sk_plan_t plan, int m, int n, const double* grid, double alpha, int out_i[3],
                              double out_d[10], unsigned flags);

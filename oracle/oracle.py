@@ -177,6 +177,21 @@ class Oracle(_Lib):
     def __init__(self, path=ORACLE_SO):
         super().__init__(path)
 
+    def ge_half_step(self, e, alpha=0.01):
+        """One phase-1 step (lowrank.cpp:345-392) on the (g/2+1) x g upper half
+        grid: ((bi, bk, a, b, m_even, m_odd), updated e) or None."""
+        h, g = e.shape
+        assert h == g // 2 + 1
+        oi = (ctypes.c_int * 3)()
+        od = np.zeros(8)
+        out = np.zeros((h, g), np.complex128)
+        self._call("ge_half_step", _I(g), _ptr(np.ascontiguousarray(e, np.complex128)), ctypes.c_double(alpha), oi,
+                   _ptr(od), _ptr(out))
+        if not oi[0]:
+            return None
+        c = od.view(np.complex128)
+        return (int(oi[1]), int(oi[2]), complex(c[0]), complex(c[1]), complex(c[2]), complex(c[3])), out
+
     def build_lap(self, m):
         lap = np.zeros((m, 5))
         self._call("build_lap", _I(m), _ptr(lap))

@@ -717,6 +717,75 @@ static void ge_step(int m, int n, const cplx* g, int js, int ks, cplx me, cplx m
 int sko_analyze_2d(int m, int n, const double* grid, double* X) {
     return guarded([&] { analyze_2d(m, n, as_c(grid), as_c(X)); });
 }
+// construct's phase-1 loop body on the upper half grid e[h x g], h = g/2 + 1,
+// row i <-> theta_i = 2 pi i / g (lowrank.cpp:345-392): complete pivoting
+// over i ascending, k = g/2 .. g-1 ascending (:345-360), the pivot cross with
+// the row of -theta* taken as the pivot row shifted by pi in lambda
+// (:362-380), and the update (:381-392).
+static bool ge_pivot_search_half(int g, const cplx* e, double alpha, int& bi, int& bk, cplx* v4) {
+    const int h = g / 2 + 1;
+    double best = 0;
+    bi = bk = -1;
+    for (int i = 0; i < h; ++i) {
+        const size_t row = static_cast<size_t>(i) * g;
+        for (int k = g / 2; k < g; ++k) {
+            const cplx a = e[row + k - g / 2], b = e[row + k];
+            const double s1 = std::max(std::abs(a + b), std::abs(a - b));
+            if (s1 > best) {
+                best = s1;
+                bi = i;
+                bk = k;
+            }
+        }
+    }
+    if (best == 0.0) return false;
+    v4[0] = e[static_cast<size_t>(bi) * g + bk - g / 2];
+    v4[1] = e[static_cast<size_t>(bi) * g + bk];
+    pinv_2x2(v4[0], v4[1], alpha, v4[2], v4[3]);
+    return true;
+}
+static void ge_step_half(int g, const cplx* e, int bi, int bk, cplx me, cplx mo, cplx* out) {
+    const int h = g / 2 + 1;
+    std::vector<cplx> ce(h), co(h), re(g), ro(g);
+    for (int i = 0; i < h; ++i) {
+        const cplx cm = e[static_cast<size_t>(i) * g + bk - g / 2], cp = e[static_cast<size_t>(i) * g + bk];
+        ce[i] = cm + cp;
+        co[i] = cm - cp;
+    }
+    const size_t row = static_cast<size_t>(bi) * g;
+    for (int k = 0; k < g; ++k) {
+        const cplx rp = e[row + k], rm = e[row + (k + g / 2) % g];
+        re[k] = rp + rm;
+        ro[k] = rp - rm;
+    }
+    const cplx de = 0.5 * me, dodd = 0.5 * mo;
+    const bool has_e = me != cplx{}, has_o = mo != cplx{};
+    for (int i = 0; i < h; ++i)
+        for (int k = 0; k < g; ++k) {
+            cplx upd{};
+            if (has_e) upd += de * ce[i] * re[k];
+            if (has_o) upd += dodd * co[i] * ro[k];
+            out[static_cast<size_t>(i) * g + k] = e[static_cast<size_t>(i) * g + k] - upd;
+        }
+}
+// one phase-1 step on the half grid e ((g/2+1) x g): out_i = found, bi, bk; out_d = a, b, m_even, m_odd
+int sko_ge_half_step(int g, const double* e, double alpha, int* out_i, double* out_d, double* out) {
+    return guarded([&] {
+        int bi, bk;
+        cplx v4[4] = {};
+        const bool found = ge_pivot_search_half(g, as_c(e), alpha, bi, bk, v4);
+        out_i[0] = found ? 1 : 0;
+        out_i[1] = found ? bi : -1;
+        out_i[2] = found ? bk : -1;
+        for (int i = 0; i < 8; ++i) out_d[i] = 0.0;
+        if (!found) return;
+        for (int i = 0; i < 4; ++i) {
+            out_d[2 * i] = v4[i].real();
+            out_d[2 * i + 1] = v4[i].imag();
+        }
+        ge_step_half(g, as_c(e), bi, bk, v4[2], v4[3], reinterpret_cast<cplx*>(out));
+    });
+}
 int sko_pivot_search(int m, int n, const double* grid, double alpha, int* out_i, double* out_d) {
     return guarded([&] {
         int bt, bk;

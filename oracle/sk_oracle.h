@@ -51,6 +51,8 @@ int sko_analyze_2d(int m, int n, const double* grid, double* X);
 // lowrank.cpp:84-112 / :127-162 (out_i: found, t, k; out_d / piv: a, b, m_even, m_odd, theta_star, lambda_star)
 int sko_pivot_search(int m, int n, const double* grid, double alpha, int* out_i, double* out_d);
 int sko_ge_step(int m, int n, const double* grid, const double* piv, double* out);
+// lowrank.cpp:345-392: one phase-1 step (search + update) on the (g/2+1) x g upper half grid
+int sko_ge_half_step(int g, const double* e, double alpha, int* out_i, double* out_d, double* out);
 int sko_sample_grid(int rows, int cols, const double* X, int m_out, int n_out, double* grid);
 
 // sphere_domain.cpp:19-26, :46-52 applied to physical samples (index map a3)

@@ -24,6 +24,7 @@ SK_ERR_NCCL = 7
 SK_HOST = 0
 SK_DEVICE = 1
 SK_ASYNC = 2
+SK_GE_HALF = 8
 
 # Every symbol declared in include/sk_poisson.h (checked by tests/test_abi.py).
 EXPORTS = [

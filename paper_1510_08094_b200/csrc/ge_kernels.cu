@@ -65,7 +65,9 @@ __device__ __forceinline__ Cand block_best(Cand v, Cand* red) {
 }  // namespace
 
 // part[blockIdx.x] = best candidate of this block's share
-__global__ void __launch_bounds__(256) ge_search_kernel(int m, int n, const double2* __restrict__ g, Cand* part) {
+// half: g holds only the upper half grid, row i <-> theta_i = 2 pi i / m (i = 0..m/2), as construct's phase 1
+// keeps it (lowrank.cpp:246-252); else the doubled grid (row of theta* = 2 pi t / m is (m/2 + t) mod m)
+__global__ void __launch_bounds__(256) ge_search_kernel(int m, int n, int half, const double2* __restrict__ g, Cand* part) {
     __shared__ Cand red[8];
     const int hn = n / 2;
     const long long total = static_cast<long long>(m / 2 + 1) * hn;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(256) ge_search_kernel(int m, int n, const doub
     for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < total;
          c += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int t = static_cast<int>(c / hn), kk = static_cast<int>(c - static_cast<long long>(t) * hn);
-        const int j = (m / 2 + t) % m;
+        const int j = half ? t : (m / 2 + t) % m;
         const double2 a = g[static_cast<size_t>(j) * n + kk], b = g[static_cast<size_t>(j) * n + kk + hn];
         const double sp = hypot(a.x + b.x, a.y + b.y), sm = hypot(a.x - b.x, a.y - b.y);
         const double s1 = (sp < sm) ? sm : sp;  // std::max
@@ -84,8 +86,8 @@ __global__ void __launch_bounds__(256) ge_search_kernel(int m, int n, const doub
 }
 
 // out[0] = sigma_1, out[1] = candidate index (as double, -1: none), out[2..5] = a, b
-__global__ void __launch_bounds__(256) ge_search_final_kernel(int m, int n, const double2* __restrict__ g, const Cand* part,
-                                                              int nparts, double* out) {
+__global__ void __launch_bounds__(256) ge_search_final_kernel(int m, int n, int half, const double2* __restrict__ g,
+                                                              const Cand* part, int nparts, double* out) {
     __shared__ Cand red[8];
     Cand best{0.0, -1};
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) best = better(best, part[i]);
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(256) ge_search_final_kernel(int m, int n, cons
         if (best.c >= 0) {
             const int hn = n / 2;
             const int t = static_cast<int>(best.c / hn), kk = static_cast<int>(best.c - static_cast<long long>(t) * hn);
-            const int j = (m / 2 + t) % m;
+            const int j = half ? t : (m / 2 + t) % m;
             a = g[static_cast<size_t>(j) * n + kk];
             b = g[static_cast<size_t>(j) * n + kk + hn];
         }
@@ -110,18 +112,22 @@ __global__ void __launch_bounds__(256) ge_search_final_kernel(int m, int n, cons
 
 // The pivot cross of the PRE-update residual: dce[j] = de (g[j][km] + g[j][ks]),
 // dco[j] = dodd (g[j][km] - g[j][ks]), re[k] = g[js][k] + g[jm][k], ro[k] = g[js][k] - g[jm][k]
-__global__ void __launch_bounds__(256) ge_cross_kernel(int m, int n, const double2* __restrict__ g, int js, int ks,
-                                                       double2 de, double2 dodd, double2* dce, double2* dco, double2* re,
-                                                       double2* ro) {
+// over the `rows` stored rows.  Half grid (lowrank.cpp:362-380): the row of
+// -theta* is the pivot row itself shifted by pi in lambda (glide symmetry),
+// re[k] = e[bi][k] + e[bi][(k + n/2) mod n].
+__global__ void __launch_bounds__(256) ge_cross_kernel(int rows, int n, int half, const double2* __restrict__ g, int js, int jm,
+                                                       int ks, double2 de, double2 dodd, double2* dce, double2* dco,
+                                                       double2* re, double2* ro) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int jm = (m - js) % m, km = (ks + n / 2) % n;
-    if (i < m) {
+    const int km = (ks + n / 2) % n;
+    if (i < rows) {
         const double2 cm = g[static_cast<size_t>(i) * n + km], cp = g[static_cast<size_t>(i) * n + ks];
         dce[i] = cmul_ref(de, make_double2(cm.x + cp.x, cm.y + cp.y));
         dco[i] = cmul_ref(dodd, make_double2(cm.x - cp.x, cm.y - cp.y));
     }
     if (i < n) {
-        const double2 rp = g[static_cast<size_t>(js) * n + i], rm = g[static_cast<size_t>(jm) * n + i];
+        const double2 rp = g[static_cast<size_t>(js) * n + i];
+        const double2 rm = half ? g[static_cast<size_t>(js) * n + (i + n / 2) % n] : g[static_cast<size_t>(jm) * n + i];
         re[i] = make_double2(rp.x + rm.x, rp.y + rm.y);
         ro[i] = make_double2(rp.x - rm.x, rp.y - rm.y);
     }
@@ -198,33 +204,36 @@ static int ge_blocks(long long work) {
     return static_cast<int>(b);
 }
 
-cudaError_t launch_ge_search(int m, int n, const double2* g, void* scratch, cudaStream_t st) {
+cudaError_t launch_ge_search(int m, int n, bool half, const double2* g, void* scratch, cudaStream_t st) {
     double* res = static_cast<double*>(scratch);
     Cand* part = reinterpret_cast<Cand*>(static_cast<char*>(scratch) + 128);
     const int nb = ge_blocks(static_cast<long long>(m / 2 + 1) * (n / 2));
-    ge_search_kernel<<<nb, 256, 0, st>>>(m, n, g, part);
-    ge_search_final_kernel<<<1, 256, 0, st>>>(m, n, g, part, nb, res);
+    ge_search_kernel<<<nb, 256, 0, st>>>(m, n, half ? 1 : 0, g, part);
+    ge_search_final_kernel<<<1, 256, 0, st>>>(m, n, half ? 1 : 0, g, part, nb, res);
     return cudaGetLastError();
 }
 
-cudaError_t launch_ge_step(int m, int n, const double2* g, int js, int ks, double2 de, double2 dodd, int has_e, int has_o,
-                           double2* out, void* scratch, bool want_max, cudaStream_t st) {
+// (js, ks): the pivot node; full grid: js the doubled row of theta*; half grid: js = t
+cudaError_t launch_ge_step(int m, int n, bool half, const double2* g, int js, int ks, double2 de, double2 dodd, int has_e,
+                           int has_o, double2* out, void* scratch, bool want_max, cudaStream_t st) {
     double* mx = static_cast<double*>(scratch) + 8;
     double2* cross = reinterpret_cast<double2*>(static_cast<char*>(scratch) + 128 + sizeof(Cand) * kGeParts);
     double2 *dce = cross, *dco = cross + m, *re = cross + 2 * m, *ro = cross + 2 * m + n;
-    const int mn = m > n ? m : n;
-    ge_cross_kernel<<<(mn + 255) / 256, 256, 0, st>>>(m, n, g, js, ks, de, dodd, dce, dco, re, ro);
+    const int rows = half ? m / 2 + 1 : m;
+    const int jm = half ? js : (m - js) % m;
+    const int mn = rows > n ? rows : n;
+    ge_cross_kernel<<<(mn + 255) / 256, 256, 0, st>>>(rows, n, half ? 1 : 0, g, js, jm, ks, de, dodd, dce, dco, re, ro);
     if (want_max) cudaMemsetAsync(mx, 0, sizeof(double), st);
     const int bx = (n + 1023) / 1024;
-    const int by = m < 65535 / 1 ? (m < 2048 ? m : 2048) : 2048;
-    ge_update_kernel<<<dim3(bx, by), 256, 0, st>>>(m, n, g, dce, dco, re, ro, has_e, has_o, out, want_max ? mx : nullptr);
+    const int by = rows < 2048 ? rows : 2048;
+    ge_update_kernel<<<dim3(bx, by), 256, 0, st>>>(rows, n, g, dce, dco, re, ro, has_e, has_o, out, want_max ? mx : nullptr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_ge_maxabs(int m, int n, const double2* g, void* scratch, cudaStream_t st) {
+cudaError_t launch_ge_maxabs(long long total, const double2* g, void* scratch, cudaStream_t st) {
     double* mx = static_cast<double*>(scratch) + 8;
     cudaMemsetAsync(mx, 0, sizeof(double), st);
-    ge_maxabs_kernel<<<ge_blocks(static_cast<long long>(m) * n), 256, 0, st>>>(static_cast<long long>(m) * n, g, mx);
+    ge_maxabs_kernel<<<ge_blocks(total), 256, 0, st>>>(total, g, mx);
     return cudaGetLastError();
 }
 

@@ -216,10 +216,11 @@ cudaError_t launch_coeff_tables(int M, int N, double* D, double* Lm, double* bad
 // double [8] the max |residual| of a step / of launch_ge_maxabs.
 constexpr int kGeParts = 2048;
 size_t ge_scratch_bytes(int m, int n);
-cudaError_t launch_ge_search(int m, int n, const double2* g, void* scratch, cudaStream_t st);
-cudaError_t launch_ge_step(int m, int n, const double2* g, int js, int ks, double2 de, double2 dodd, int has_e, int has_o,
-                           double2* out, void* scratch, bool want_max, cudaStream_t st);
-cudaError_t launch_ge_maxabs(int m, int n, const double2* g, void* scratch, cudaStream_t st);
+// half: g holds the (m/2+1) x n upper half grid (row i <-> theta_i = 2 pi i/m), as construct's phase 1 keeps it
+cudaError_t launch_ge_search(int m, int n, bool half, const double2* g, void* scratch, cudaStream_t st);
+cudaError_t launch_ge_step(int m, int n, bool half, const double2* g, int js, int ks, double2 de, double2 dodd, int has_e,
+                           int has_o, double2* out, void* scratch, bool want_max, cudaStream_t st);
+cudaError_t launch_ge_maxabs(long long total, const double2* g, void* scratch, cudaStream_t st);
 cudaError_t launch_msin2(int M, int N, const double2* A, double2* F, cudaStream_t st);
 cudaError_t launch_residual(const ResidualParams& P, cudaStream_t st);
 

@@ -1426,9 +1426,9 @@ sk_status ge_check_sizes(int m, int n) {
 }
 
 // search on the device grid g; fills out_i / out_d (host); returns found
-sk_status ge_search_dev(sk_plan_t p, int m, int n, const double2* g, void* scr, double alpha, int out_i[3],
+sk_status ge_search_dev(sk_plan_t p, int m, int n, bool half, const double2* g, void* scr, double alpha, int out_i[3],
                         double out_d[10]) {
-    CU(sk::launch_ge_search(m, n, g, scr, p->stream));
+    CU(sk::launch_ge_search(m, n, half, g, scr, p->stream));
     double h[6];
     CU(cudaMemcpyAsync(h, scr, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
@@ -1463,15 +1463,19 @@ sk_status ge_locate(double x, double step, int count, int* idx) {
     return SK_OK;
 }
 
-sk_status ge_step_dev(sk_plan_t p, int m, int n, const double2* g, const double piv[10], double2* out, void* scr,
-                      bool want_max) {
+sk_status ge_step_dev(sk_plan_t p, int m, int n, bool half, const double2* g, const double piv[10], double2* out,
+                      void* scr, bool want_max) {
     int js = 0, ks = 0;
     sk_status s = ge_locate(piv[8], kTwoPiRef / m, m, &js);
     if (s != SK_OK) return s;
     if ((s = ge_locate(piv[9], kTwoPiRef / n, n, &ks)) != SK_OK) return s;
+    if (half) {  // stored row i <-> theta_i = 2 pi i / m: the doubled row m/2 + i (theta* = pi is doubled row 0)
+        js = (js + m - m / 2) % m;
+        if (js > m / 2) return fail(SK_ERR_ARGUMENT, "ge_step: theta* lies outside [0, pi]");
+    }
     const cplx me(piv[4], piv[5]), mo(piv[6], piv[7]);
     const cplx de = 0.5 * me, dodd = 0.5 * mo;  // lowrank.cpp:147-148
-    CU(sk::launch_ge_step(m, n, g, js, ks, make_double2(de.real(), de.imag()), make_double2(dodd.real(), dodd.imag()),
+    CU(sk::launch_ge_step(m, n, half, g, js, ks, make_double2(de.real(), de.imag()), make_double2(dodd.real(), dodd.imag()),
                           me != cplx{} ? 1 : 0, mo != cplx{} ? 1 : 0, out, scr, want_max, p->stream));
     return SK_OK;
 }
@@ -1484,12 +1488,14 @@ sk_status sk_ge_pivot_search(sk_plan_t p, int m, int n, const double* grid, doub
     if (s != SK_OK) return s;
     if (!grid || !out_i || !out_d) return fail(SK_ERR_ARGUMENT, "null argument");
     if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
+    const bool half = (flags & SK_GE_HALF) != 0;
     const void* g = nullptr;
     void* scr = nullptr;
-    if ((s = stage_in(p, grid, sizeof(double2) * m * static_cast<size_t>(n), flags, 0, &g)) != SK_OK) return s;
+    if ((s = stage_in(p, grid, sizeof(double2) * (half ? m / 2 + 1 : m) * static_cast<size_t>(n), flags, 0, &g)) != SK_OK)
+        return s;
     if ((s = scratch(p, 2, sk::ge_scratch_bytes(m, n), &scr)) != SK_OK) return s;
     p->last_launches = 2;
-    return ge_search_dev(p, m, n, static_cast<const double2*>(g), scr, alpha, out_i, out_d);
+    return ge_search_dev(p, m, n, half, static_cast<const double2*>(g), scr, alpha, out_i, out_d);
 }
 
 sk_status sk_ge_step(sk_plan_t p, int m, int n, const double* grid, const double piv[10], double* out, unsigned flags) {
@@ -1497,13 +1503,14 @@ sk_status sk_ge_step(sk_plan_t p, int m, int n, const double* grid, const double
     if (s != SK_OK) return s;
     if (!grid || !piv || !out) return fail(SK_ERR_ARGUMENT, "null argument");
     if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
-    const size_t bytes = sizeof(double2) * m * static_cast<size_t>(n);
+    const bool half = (flags & SK_GE_HALF) != 0;
+    const size_t bytes = sizeof(double2) * (half ? m / 2 + 1 : m) * static_cast<size_t>(n);
     const void* g = nullptr;
     void *scr = nullptr, *o = out;
     if ((s = stage_in(p, grid, bytes, flags, 0, &g)) != SK_OK) return s;
     if ((s = scratch(p, 2, sk::ge_scratch_bytes(m, n), &scr)) != SK_OK) return s;
     if (!(flags & SK_DEVICE) && (s = scratch(p, 1, bytes, &o)) != SK_OK) return s;
-    if ((s = ge_step_dev(p, m, n, static_cast<const double2*>(g), piv, static_cast<double2*>(o), scr, false)) != SK_OK)
+    if ((s = ge_step_dev(p, m, n, half, static_cast<const double2*>(g), piv, static_cast<double2*>(o), scr, false)) != SK_OK)
         return s;
     p->last_launches = 2;
     if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(out, o, bytes, cudaMemcpyDeviceToHost, p->stream));
@@ -1517,7 +1524,9 @@ sk_status sk_ge_run(sk_plan_t p, int m, int n, double* grid, double alpha, doubl
     if (s != SK_OK) return s;
     if (!grid || !nsteps || !piv_i || !piv_d || !resid || max_steps < 0) return fail(SK_ERR_ARGUMENT, "bad argument");
     if ((s = ge_check_sizes(m, n)) != SK_OK) return s;
-    const size_t bytes = sizeof(double2) * m * static_cast<size_t>(n);
+    const bool half = (flags & SK_GE_HALF) != 0;
+    const long long rows = half ? m / 2 + 1 : m;
+    const size_t bytes = sizeof(double2) * rows * static_cast<size_t>(n);
     void *g = grid, *scr = nullptr;
     if (!(flags & SK_DEVICE)) {
         if ((s = scratch(p, 0, bytes, &g)) != SK_OK) return s;
@@ -1531,17 +1540,17 @@ sk_status sk_ge_run(sk_plan_t p, int m, int n, double* grid, double alpha, doubl
         CU(cudaStreamSynchronize(p->stream));
         return SK_OK;
     };
-    CU(sk::launch_ge_maxabs(m, n, gd, scr, p->stream));
+    CU(sk::launch_ge_maxabs(rows * n, gd, scr, p->stream));
     if ((s = read_max(&resid[0])) != SK_OK) return s;
     int step = 0;
     p->last_launches = 1;
     while (step < max_steps && resid[step] > tau) {
         int oi[3];
-        if ((s = ge_search_dev(p, m, n, gd, scr, alpha, oi, piv_d + 10 * step)) != SK_OK) return s;
+        if ((s = ge_search_dev(p, m, n, half, gd, scr, alpha, oi, piv_d + 10 * step)) != SK_OK) return s;
         if (!oi[0]) break;  // the residual is exactly zero on the pivot set
         piv_i[2 * step] = oi[1];
         piv_i[2 * step + 1] = oi[2];
-        if ((s = ge_step_dev(p, m, n, gd, piv_d + 10 * step, gd, scr, true)) != SK_OK) return s;
+        if ((s = ge_step_dev(p, m, n, half, gd, piv_d + 10 * step, gd, scr, true)) != SK_OK) return s;
         if ((s = read_max(&resid[step + 1])) != SK_OK) return s;
         p->last_launches += 4;
         ++step;

@@ -363,43 +363,50 @@ class Plan:
         return grid
 
     # -- structure-preserving GE on a doubled grid (lowrank.hpp:73-93)
-    def pivot_search(self, grid, alpha: float = 0.01):
+    def pivot_search(self, grid, alpha: float = 0.01, half: bool = False):
         """pivot_search (lowrank.cpp:84-112) of an m x n complex doubled grid:
-        a PivotBlock, or None where the grid vanishes on the pivot set."""
+        a PivotBlock, or None where the grid vanishes on the pivot set.
+        half: grid is the (m/2+1) x n upper half, row i <-> theta_i = 2 pi i/m,
+        as construct's phase 1 keeps it (lowrank.cpp:246-252)."""
         dev = _is_device(grid)
         m, n = (int(x) for x in grid.shape[-2:])
+        m = 2 * (m - 1) if half else m
         if not dev:
             grid = np.ascontiguousarray(grid, dtype=np.complex128)
         self._follow_torch(grid)
         oi = (ctypes.c_int * 3)()
         od = (ctypes.c_double * 10)()
         _lib.check(self.lib.sk_ge_pivot_search(self._h, m, n, _ptr(grid), float(alpha), oi, od,
-                                               _lib.SK_DEVICE if dev else _lib.SK_HOST))
+                                               (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (_lib.SK_GE_HALF if half else 0)))
         return PivotBlock._from(oi, od) if oi[0] else None
 
-    def ge_step(self, grid, p: "PivotBlock", out=None):
+    def ge_step(self, grid, p: "PivotBlock", out=None, half: bool = False):
         """ge_step (lowrank.cpp:127-162): grid minus the rank-<=2 update of
-        pivot p, bit-identical to the reference."""
+        pivot p, bit-identical to the reference (half: as in pivot_search;
+        the phase-1 update lowrank.cpp:362-392)."""
         dev = _is_device(grid)
-        m, n = (int(x) for x in grid.shape[-2:])
+        rows, n = (int(x) for x in grid.shape[-2:])
+        m = 2 * (rows - 1) if half else rows
         if dev:
             import torch
             out = torch.empty_like(grid) if out is None else out
         else:
             grid = np.ascontiguousarray(grid, dtype=np.complex128)
-            out = np.empty((m, n), np.complex128) if out is None else out
+            out = np.empty((rows, n), np.complex128) if out is None else out
         self._follow_torch(grid)
         pd = (ctypes.c_double * 10)(*p._doubles())
-        _lib.check(self.lib.sk_ge_step(self._h, m, n, _ptr(grid), pd, _ptr(out), _lib.SK_DEVICE if dev else _lib.SK_HOST))
+        _lib.check(self.lib.sk_ge_step(self._h, m, n, _ptr(grid), pd, _ptr(out),
+                                       (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (_lib.SK_GE_HALF if half else 0)))
         return out
 
-    def ge_run(self, grid, tau: float, alpha: float = 0.01, max_steps: int = 1024):
+    def ge_run(self, grid, tau: float, alpha: float = 0.01, max_steps: int = 1024, half: bool = False):
         """The elimination loop with the grid resident on the device (in place
         for device tensors; host arrays are copied in and back): returns
         (pivots, resid) with resid[0] = max|grid| before the first step and
         resid[s + 1] after step s."""
         dev = _is_device(grid)
         m, n = (int(x) for x in grid.shape[-2:])
+        m = 2 * (m - 1) if half else m
         if not dev and not (isinstance(grid, np.ndarray) and grid.dtype == np.complex128 and grid.flags.c_contiguous):
             raise size_error("ge_run: a C-contiguous complex128 array is updated in place")
         self._follow_torch(grid)
@@ -408,7 +415,7 @@ class Plan:
         pd = (ctypes.c_double * (10 * max_steps))()
         rs = (ctypes.c_double * (max_steps + 1))()
         _lib.check(self.lib.sk_ge_run(self._h, m, n, _ptr(grid), float(alpha), float(tau), int(max_steps), ctypes.byref(ns),
-                                      pi, pd, rs, _lib.SK_DEVICE if dev else _lib.SK_HOST))
+                                      pi, pd, rs, (_lib.SK_DEVICE if dev else _lib.SK_HOST) | (_lib.SK_GE_HALF if half else 0)))
         k = ns.value
         piv = [PivotBlock._from((1, pi[2 * i], pi[2 * i + 1]), pd[10 * i: 10 * i + 10]) for i in range(k)]
         return piv, [rs[i] for i in range(k + 1)]

@@ -311,3 +311,33 @@ def test_ge_errors(pkg):
         bad = pkg.PivotBlock(0.456, 0.123, p.a, p.b, p.m_even, p.m_odd)  # not a grid node (test_lowrank.cpp:127)
         with pytest.raises(ValueError):
             plan.ge_step(g, bad)
+
+
+@pytest.mark.parametrize("name", ["ge_rand6_32x32", "ge_sym4_32x32", "ge_sym_32x48", "ge_rand12_64x96"])
+def test_ge_half_grid_mode(pkg, oracle, name):
+    """SK_GE_HALF: the elimination on the (m/2+1) x n upper half grid, as
+    construct's phase 1 keeps it (lowrank.cpp:246-252, :345-392): the same
+    pivots as on the doubled grid and, on the stored rows, the same bits as
+    the reference's ge_step (golden) and as the oracle's phase-1 step."""
+    g = golden(name)
+    grid = g["grid"]
+    m, n = grid.shape
+    up = lambda a: np.ascontiguousarray(np.concatenate([a[m // 2:], a[:1]]))  # noqa: E731
+    half = up(grid)
+    with pkg.Plan(8, 8) as plan:
+        cur = half
+        for s, (pi, pd) in enumerate(zip(g["piv_i"], g["piv_d"])):
+            p = plan.pivot_search(cur, half=True)
+            assert (p.t, p.k) == (int(pi[0]), int(pi[1])) and np.array_equal(_piv_doubles(p), pd)
+            nxt = plan.ge_step(cur, p, half=True)
+            if m == n:
+                _, oh = oracle.ge_half_step(cur)
+                assert _bits_equal(nxt, oh)
+            if f"after_{s}" in g.files:
+                assert _bits_equal(nxt, up(g[f"after_{s}"]))
+            cur = nxt
+        assert _bits_equal(cur, up(g["final"]))
+        run = half.copy()
+        piv, resid = plan.ge_run(run, tau=1e-13 * np.abs(grid).max(), max_steps=10, half=True)
+        assert [(p.t, p.k) for p in piv] == [tuple(int(v) for v in r) for r in g["piv_i"]]
+        assert _bits_equal(run, up(g["final"]))

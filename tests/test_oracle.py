@@ -203,3 +203,25 @@ def test_oracle_ge_vs_reference_random(oracle, reference):
             assert _bits_equal(nxt, reference.ge_step(cur, pr))
             cur = nxt
     assert oracle.pivot_search(np.zeros((16, 16), complex)) is None
+
+
+@pytest.mark.parametrize("name", ["ge_rand6_32x32", "ge_sym4_32x32"])  # exactly BMC-symmetric fixtures
+def test_oracle_phase1_half_step_equals_reference_full_step(oracle, name):
+    """construct's phase-1 loop body on the upper half grid (lowrank.cpp:
+    345-392; internal to the reference) restated: on BMC-symmetric data it
+    picks the pivots of the reference's public pivot_search and leaves, on
+    the stored rows, exactly the bits of the reference's ge_step on the
+    doubled grid (the golden fixtures hold both)."""
+    g = golden(name)
+    grid = g["grid"]
+    m = grid.shape[0]
+    half = np.concatenate([grid[m // 2:], grid[:1]])  # theta_i = 2 pi i/m, i = 0..m/2 (theta = pi is doubled row 0)
+    for s, (pi, pd) in enumerate(zip(g["piv_i"], g["piv_d"])):
+        (bi, bk, a, b, me, mo), half = oracle.ge_half_step(half)
+        assert (bi, bk) == (int(pi[0]), int(pi[1]))
+        assert np.array_equal(np.array([a.real, a.imag, b.real, b.imag, me.real, me.imag, mo.real, mo.imag]), pd[:8])
+        if f"after_{s}" in g.files:
+            full = g[f"after_{s}"]
+            assert _bits_equal(half, np.concatenate([full[m // 2:], full[:1]]))
+    full = g["final"]
+    assert _bits_equal(half, np.concatenate([full[m // 2:], full[:1]]))

@@ -101,8 +101,10 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
         // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
         const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
         const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-        const double2 Xk = cadd(A, cmul(T(k), B));
-        const double2 Xm = cadd(conjd(A), cmul(T(km), conjd(B)));
+        // T(L - k) = -conj T(k) (2L-th roots): X_{L-k} = conj(A) + T(L-k) conj(B) = conj(A - T(k) B)
+        const double2 Pk = cmul(T(k), B);
+        const double2 Xk = cadd(A, Pk);
+        const double2 Xm = conjd(csub(A, Pk));
         const double2 vk = cscale(Xk, (k & 1) ? -invN : invN);
         const double2 vm = cscale(Xm, (km & 1) ? -invN : invN);
         if (P.peers.n) {  // fused transpose: store into the theta rank's receive buffer over NVLink
@@ -161,8 +163,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
                 const double2 zp = a[s_rev[km == L ? 0 : km]];
                 const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
                 const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-                vk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
-                vm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+                const double2 Pk = cmul(T(k), B);  // T(L - k) = -conj T(k): X_{L-k} = conj(A - T(k) B)
+                vk[u] = cscale(cadd(A, Pk), (k & 1) ? -invN : invN);
+                vm[u] = cscale(conjd(csub(A, Pk)), (km & 1) ? -invN : invN);
             }
         }
         __syncthreads();
@@ -255,8 +258,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 2) lambda_fwd_q
                 const double2 zp = a[s_rev[km == L ? 0 : km]];
                 const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
                 const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-                vk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
-                vm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+                const double2 Pk = cmul(T(k), B);  // T(L - k) = -conj T(k): X_{L-k} = conj(A - T(k) B)
+                vk[u] = cscale(cadd(A, Pk), (k & 1) ? -invN : invN);
+                vm[u] = cscale(conjd(csub(A, Pk)), (km & 1) ? -invN : invN);
             }
         }
         __syncthreads();
@@ -336,14 +340,11 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParam
             }
             // Z_k = E_k + i O_k, E_k = V_k + conj V_{L-k}, O_k = (V_k - conj V_{L-k}) conj(T(k))
             {
+                // conj T(L - k) = -T(k): E_{L-k} = conj E_k, O_{L-k} = conj O_k, one twiddle product for both
                 const double2 E = make_double2(v.x + w.x, v.y - w.y);
                 const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
                 zk[u] = make_double2(E.x - O.y, E.y + O.x);
-            }
-            {
-                const double2 E = make_double2(w.x + v.x, w.y - v.y);
-                const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-                zm[u] = make_double2(E.x - O.y, E.y + O.x);
+                zm[u] = make_double2(E.x + O.y, O.x - E.y);
             }
         }
     }
@@ -428,14 +429,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
                     w.y = 0.0;
                 }
                 {
+                    // conj T(L - k) = -T(k): E_{L-k} = conj E_k, O_{L-k} = conj O_k, one twiddle product for both
                     const double2 E = make_double2(v.x + w.x, v.y - w.y);
                     const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
                     zk[u] = make_double2(E.x - O.y, E.y + O.x);
-                }
-                {
-                    const double2 E = make_double2(w.x + v.x, w.y - v.y);
-                    const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-                    zm[u] = make_double2(E.x - O.y, E.y + O.x);
+                    zm[u] = make_double2(E.x + O.y, O.x - E.y);
                 }
             }
         }

@@ -74,8 +74,9 @@ __global__ void __launch_bounds__(512, 1) lambda_fwd_duo_kernel(LambdaParams P) 
             // A = (Z_k + conj Z_{L-k}) / 2,  B = -i (Z_k - conj Z_{L-k}) / 2
             const double2 A = make_double2(0.5 * (z.x + zp.x), 0.5 * (z.y - zp.y));
             const double2 B = make_double2(0.5 * (z.y + zp.y), -0.5 * (z.x - zp.x));
-            vk[u] = cscale(cadd(A, cmul(T(k), B)), (k & 1) ? -invN : invN);
-            vm[u] = cscale(cadd(conjd(A), cmul(T(km), conjd(B))), (km & 1) ? -invN : invN);
+            const double2 Pk = cmul(T(k), B);  // T(L - k) = -conj T(k): X_{L-k} = conj(A - T(k) B)
+            vk[u] = cscale(cadd(A, Pk), (k & 1) ? -invN : invN);
+            vm[u] = cscale(conjd(csub(A, Pk)), (km & 1) ? -invN : invN);
         }
     }
     __syncthreads();
@@ -143,14 +144,11 @@ __global__ void __launch_bounds__(512, 1) lambda_inv_duo_kernel(LambdaParams P, 
             }
             // Z_k = E_k + i O_k, E_k = V_k + conj V_{L-k}, O_k = (V_k - conj V_{L-k}) conj(T(k))
             {
+                // conj T(L - k) = -T(k): E_{L-k} = conj E_k, O_{L-k} = conj O_k, one twiddle product for both
                 const double2 E = make_double2(v.x + w.x, v.y - w.y);
                 const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), T(k));
                 zk[u] = make_double2(E.x - O.y, E.y + O.x);
-            }
-            {
-                const double2 E = make_double2(w.x + v.x, w.y - v.y);
-                const double2 O = cmulc(make_double2(w.x - v.x, w.y + v.y), T(km));
-                zm[u] = make_double2(E.x - O.y, E.y + O.x);
+                zm[u] = make_double2(E.x + O.y, O.x - E.y);
             }
         }
     }

@@ -39,9 +39,19 @@ __device__ unsigned long long g_phase[4096][24];
         __syncthreads();                                                    \
         if (threadIdx.x == 0 && blockIdx.x < 4096) g_phase[blockIdx.x][i] = clock64(); \
     } while (0)
+// phase probes of the lambda kernels (their own table: they run before / after the theta stage)
+__device__ unsigned long long g_phase_l[2][4096][8];
+#define SK_PROBE_LAM(w, i)                                                         \
+    do {                                                                           \
+        __syncthreads();                                                           \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) g_phase_l[w][blockIdx.x][i] = clock64(); \
+    } while (0)
 #else
 #define SK_PROBE(i) \
     do {            \
+    } while (0)
+#define SK_PROBE_LAM(w, i) \
+    do {                   \
     } while (0)
 #endif
 
@@ -139,6 +149,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
     const int c = static_cast<int>(cluster.block_rank());
     const int row = blockIdx.x;
     const bool live = row < P.rows_local;  // CTA-uniform
+    SK_PROBE_LAM(0, 0);
     if (live && tid == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -151,7 +162,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
     __syncthreads();
     if (live) {
         mbar_wait(bar, 0);
+        SK_PROBE_LAM(0, 1);
         fft_forward<false, 25>(a, P.fd, T, tid, nthr);
+        SK_PROBE_LAM(0, 2);
         const double invN = 1.0 / P.g.N;
         double2 vk[kLamPairs], vm[kLamPairs];
 #pragma unroll
@@ -178,7 +191,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
             }
         }
     }
+    SK_PROBE_LAM(0, 3);
     cluster.sync();
+    SK_PROBE_LAM(0, 4);
     const double2* other = cluster.map_shared_rank(a, c ^ 1);
     const int r0 = row & ~1;
     const int nk = L + 1;
@@ -205,7 +220,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) lambda_fwd_p
             if (i < tot && sub < sub_hi) P.spec[static_cast<size_t>(k) * P.rows_local + r0 + sub] = v[u];
         }
     }
+    SK_PROBE_LAM(0, 5);
     cluster_exit_barrier(relaxed_exit);
+    SK_PROBE_LAM(0, 6);
 }
 
 // Row groups of G = 4 (p .. p+3) on a 4-CTA cluster (single RHS, unswizzled
@@ -310,6 +327,7 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParam
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int row = blockIdx.x % P.rows_local;
     const int rhs = blockIdx.x / P.rows_local;
+    SK_PROBE_LAM(1, 0);
     if (tid == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -324,6 +342,7 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParam
     const Tw T{s_hi, s_lo, P.fd.shift, (1 << P.fd.shift) - 1};
     __syncthreads();
     mbar_wait(bar, 0);
+    SK_PROBE_LAM(1, 1);
     double2 zk[kPairs], zm[kPairs];
 #pragma unroll
     for (int u = 0; u < kPairs; ++u) {
@@ -359,9 +378,12 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_inv_kernel(LambdaParam
         }
     }
     __syncthreads();
+    SK_PROBE_LAM(1, 2);
     fft_inverse<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);
+    SK_PROBE_LAM(1, 3);
     double2* dst = reinterpret_cast<double2*>(P.u + rhs * P.out_rhs_stride + static_cast<long long>(row) * P.g.N);
     for (int j = tid; j < L; j += nthr) dst[j] = a[swz<SWZ>(j)];
+    SK_PROBE_LAM(1, 4);
 }
 
 // Inverse on row pairs (p, p+1), the mirror image of lambda_fwd_pair_kernel

@@ -495,6 +495,10 @@ namespace sk { extern __device__ unsigned long long g_phase[4096][24]; }
 extern "C" int sk_debug_phases(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, sk::g_phase, sizeof(unsigned long long) * 4096 * 24) == cudaSuccess ? 0 : 1;
 }
+namespace sk { extern __device__ unsigned long long g_phase_l[2][4096][8]; }
+extern "C" int sk_debug_phases_lambda(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, sk::g_phase_l, sizeof(unsigned long long) * 2 * 4096 * 8) == cudaSuccess ? 0 : 1;
+}
 #endif
 
 extern "C" {

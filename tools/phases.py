@@ -43,3 +43,21 @@ if (sub > 0).all():
     dd = np.diff(np.concatenate([base, sub], axis=1), axis=1)
     for i, nm in enumerate(sn):
         print(f"    chain+ {nm:18s} {dd[:, i].mean():8.0f} cyc")
+
+# lambda kernels (their own probe table)
+lb = (ctypes.c_ulonglong * (2 * 4096 * 8))()
+if hasattr(_lib.load(), "sk_debug_phases_lambda") and _lib.load().sk_debug_phases_lambda(lb) == 0:
+    la = np.frombuffer(lb, dtype=np.uint64).reshape(2, 4096, 8).astype(np.int64)
+    nr = min(4096, cfg.M // 2 + 1)
+    for w, (title, nm) in enumerate([("lambda_fwd (row pairs)", ["barrier init + tables + row TMA wait", "forward FFT",
+                                                               "real split -> natural order", "cluster barrier",
+                                                               "paired stores (half remote)", "exit barrier"]),
+                                     ("lambda_inv", ["tables + mode gather (TMA) wait", "C2R pack", "inverse FFT",
+                                                     "row store"])]):
+        t = la[w, :nr, :len(nm) + 1]
+        if (t > 0).all():
+            d = np.diff(t, axis=1)
+            tot = d.sum(axis=1).mean()
+            print(f"{title}: mean cycles per CTA {tot:.0f}")
+            for i, n_ in enumerate(nm):
+                print(f"  {n_:38s} {d[:, i].mean():9.0f} cyc  {100 * d[:, i].mean() / tot:5.1f}%")

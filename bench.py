@@ -549,6 +549,24 @@ def main():
         nb = f.numel() * 8
         e2e = {"value": dofs_step / (ms_e2e * 1e-3), "unit": "DOF/s", "h2d_bytes_per_step": nb,
                "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e}
+        # the interconnect's share: the same bytes in and out at once on two
+        # streams, no solve (what a fully overlapped pipeline could reach)
+        try:
+            s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            dsrc = torch.empty_like(f)
+            torch.cuda.synchronize()
+            reps = 3
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                with torch.cuda.stream(s_in):
+                    f.copy_(fh, non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    uh.copy_(dsrc, non_blocking=True)
+            torch.cuda.synchronize()
+            e2e["copies_only_ms"] = 1e3 * (time.perf_counter() - t0) / reps
+            del dsrc
+        except RuntimeError:
+            pass
 
     # ---- CPU baseline (rank 0, N = 1, bounded sample: 2 of the 16 stock blocks)
     cpu = None

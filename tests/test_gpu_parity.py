@@ -182,6 +182,42 @@ def test_grid_solve_rough_data_vs_reference(pkg, oracle, reference, m, n):
     assert np.abs(u - u_herm).max() <= 1e-10 * np.abs(u_herm).max()
 
 
+_SWEEP = [(16, 16), (24, 20), (100, 30), (200, 24), (300, 20), (600, 28), (1024, 24), (1200, 16), (2000, 20),
+          (3000, 16), (4096, 16), (5000, 12), (8192, 12), (9000, 8), (14000, 8), (20000, 8), (24, 600), (40, 1200),
+          (32, 4096), (24, 5000), (16, 10000), (36, 18), (84, 42), (500, 250), (1470, 14), (14, 1470)]
+
+
+@pytest.mark.parametrize("m,n", _SWEEP)
+def test_grid_size_sweep_vs_reference(pkg, oracle, reference, m, n):
+    """Rough zero-mean data across the plan's kernel-selection boundaries
+    (segment / register / shared-memory chain solvers, high-occupancy and
+    swizzled variants, theta_sym, row-pair lambda kernels, radices 3 / 5 / 7)
+    against the reference's own composition (oracle/_ref), the comparands of
+    test_grid_solve_rough_data_vs_reference.  Half lengths with a prime factor
+    > 7 belong to sk_solve_grid_exact (tests/test_gpu_exact.py)."""
+    f = zero_mean_noise(oracle, m, n, m + 3 * n)
+    X_ref, _, u_herm = ref_grid(reference, f, m)
+    with pkg.Plan(m, n) as plan:
+        u, Xh = plan.solve_grid(f, coeffs=True)
+    assert np.abs(Xh[: n // 2] - X_ref[:, n // 2:].T).max() <= 1e-10 * np.abs(X_ref).max()
+    assert np.abs(u - u_herm).max() <= 1e-10 * np.abs(u_herm).max()
+
+
+@pytest.mark.parametrize("m,n", [(44, 26), (1204, 22), (26, 1204)])
+def test_grid_unsupported_lengths_fail_loudly(pkg, oracle, m, n):
+    """Half lengths with a prime factor > 7 are outside the real grid path
+    (DESIGN section 7): it reports SK_ERR_UNSUPPORTED instead of computing
+    anything, and the same data go through sk_solve_grid_exact."""
+    from paper_1510_08094_b200._lib import UnsupportedError
+    f = zero_mean_noise(oracle, m, n, 5)
+    with pytest.raises(UnsupportedError):
+        with pkg.Plan(m, n) as plan:
+            plan.solve_grid(f)
+    with pkg.Plan(m, n) as plan:
+        U = plan.solve_grid_exact(f)
+    assert np.isfinite(U).all()
+
+
 def test_grid_precondition_error(pkg):
     m, n = 32, 16
     f = np.ones((m // 2 + 1, n))

@@ -553,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
     const int c = static_cast<int>(cluster.block_rank());
     const int L = P.fd.L, Lh = L / 2;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* tN_hi = a + ((Lh + 7) & ~7);  // whole 8-slot swizzle blocks
+    double2* tN_hi = a + PS.aslots;
     double2* tN_lo = tN_hi + P.fd.nhi;
     double2* th_hi = tN_lo + P.fd.nlo;
     double2* th_lo = th_hi + fh.nhi;
@@ -622,7 +622,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_fwd_s
 // Inverse: CTA c gathers the modes k = c (mod 2) (and their partners L - k),
 // forms Z_k, runs the length-L/2 inverse transform of its class and the pair
 // recombines z_j = W0_j + w_L^j W1_j through DSMEM (CTA c writes half the row).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_split_kernel(LambdaSplitParams PS, int relaxed_exit) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    lambda_inv_split_kernel(LambdaSplitParams PS, int relaxed_exit, const __grid_constant__ CUtensorMap map0,
+                            const __grid_constant__ CUtensorMap map1) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const LambdaParams& P = PS.l;
     const FftDesc& fh = PS.fh;
@@ -630,22 +632,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) lambda_inv_s
     const int c = static_cast<int>(cluster.block_rank());
     const int L = P.fd.L, Lh = L / 2;
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* tN_hi = a + ((Lh + 7) & ~7);  // whole 8-slot swizzle blocks
+    double2* tN_hi = a + PS.aslots;
     double2* tN_lo = tN_hi + P.fd.nhi;
     double2* th_hi = tN_lo + P.fd.nlo;
     double2* th_lo = th_hi + fh.nhi;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(th_lo + fh.nlo);
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int rowi = blockIdx.x / 2;
     const int row = rowi % P.rows_local;
     const int rhs = rowi / P.rows_local;
+    const int* revh = fh.rev;
+    const int mcount = (L / 2 - c) / 2 + 1;  // pairs (k, L - k), k = 2m + c <= L/2
+    if (PS.tma) {
+        // this CTA's modes k = 2m + c, m = 0 .. (L - c)/2, gathered by the copy
+        // engine through the per-parity tensor map (mode stride 2) into slots
+        // m in natural order; out-of-range modes of the last box are zero-filled
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const int nbox = PS.aslots / kSplitBox;
+            mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * kSplitBox * 16);
+            const CUtensorMap* mp = c == 0 ? &map0 : &map1;
+            for (int b = 0; b < nbox; ++b) tma_load_3d(a + b * kSplitBox, mp, 2 * row, b * kSplitBox, rhs, bar);
+        }
+    }
     const Tw TN = load_tw(P.fd, tN_hi, tN_lo, tid, nthr);
     SK_PROBE_L(19);
     const Tw TH = load_tw(fh, th_hi, th_lo, tid, nthr);
     __syncthreads();
     SK_PROBE_L(20);
+    if (PS.tma) {
+        // every pair through registers (the packed values land in swizzled
+        // digit-reversed slots of the same buffer); the table indices are
+        // fetched while the gather is in flight
+        double2 zk[kSplitPairs], zm[kSplitPairs];
+        int rk[kSplitPairs], rm[kSplitPairs];
+#pragma unroll
+        for (int u = 0; u < kSplitPairs; ++u) {
+            const int m = min(tid + u * nthr, mcount - 1);
+            rk[u] = __ldg(revh + m);
+            rm[u] = __ldg(revh + min((L - 2 * m - 2 * c) / 2, Lh - 1));  // partner L - k = 2 m' + c
+        }
+        mbar_wait(bar, 0);
+#pragma unroll
+        for (int u = 0; u < kSplitPairs; ++u) {
+            const int m = tid + u * nthr;
+            if (m < mcount) {
+                const int k = 2 * m + c;
+                const int km = L - k;
+                double2 v = a[m];
+                double2 w = a[(km - c) / 2];
+                if (k & 1) v = make_double2(-v.x, -v.y);
+                if (km & 1) w = make_double2(-w.x, -w.y);
+                if (k == 0) {  // DC and Nyquist of a real signal are real
+                    v.y = 0.0;
+                    w.y = 0.0;
+                }
+                // conj TN(L - k) = -TN(k): E_{L-k} = conj E_k, O_{L-k} = conj O_k, one twiddle product for both
+                const double2 E = make_double2(v.x + w.x, v.y - w.y);
+                const double2 O = cmulc(make_double2(v.x - w.x, v.y + w.y), TN(k));
+                zk[u] = make_double2(E.x - O.y, E.y + O.x);
+                zm[u] = make_double2(E.x + O.y, O.x - E.y);
+            }
+        }
+        __syncthreads();  // every gathered mode has been read
+#pragma unroll
+        for (int u = 0; u < kSplitPairs; ++u) {
+            const int m = tid + u * nthr;
+            if (m < mcount) {
+                const int k = 2 * m + c;
+                a[swz<true>(rk[u])] = zk[u];
+                if (k != 0 && L - k != k) a[swz<true>(rm[u])] = zm[u];
+            }
+        }
+    }
     const double2* in = P.spec + rhs * P.in_rhs_stride;
-    const int* revh = fh.rev;
-    for (int m = tid; 2 * m + c <= L / 2; m += nthr) {
+    for (int m = PS.tma ? mcount : tid; 2 * m + c <= L / 2; m += nthr) {
         const int k = 2 * m + c;
         const int km = L - k;
         double2 v = __ldg(in + static_cast<size_t>(k) * P.rows_local + row);
@@ -714,9 +776,11 @@ cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st) {
+// map0 / map1: the spectrum's even / odd modes (make_spec_map with mode step 2), read when P.tma
+cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, const CUtensorMap& map0, const CUtensorMap& map1, int nthr,
+                                    size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(lambda_inv_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    lambda_inv_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P, exit_relaxed());
+    lambda_inv_split_kernel<<<2 * P.l.rows_local * P.l.nrhs, nthr, smem, st>>>(P, exit_relaxed(), map0, map1);
     return cudaGetLastError();
 }
 

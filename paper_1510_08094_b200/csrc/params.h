@@ -132,21 +132,29 @@ struct ThetaMpParams {
 size_t theta_mp_smem_bytes(int which, int L1, int L2, int nhi1, int nlo1, int nhi2, int nlo2, int nhiM, int nloM);
 int theta_mp_chain_cap();
 cudaError_t launch_theta_mp(const ThetaMpParams& Q, cudaStream_t st);
+constexpr int kSplitBox = 256;   // modes per gather box of the split inverse lambda kernel
+constexpr int kSplitPairs = 9;   // mode pairs (k, L - k) per thread it holds in registers (512 threads)
 struct LambdaSplitParams {
     LambdaParams l;
     FftDesc fh;
+    int aslots;  // data slots ahead of the tables: L/2 rounded up to swizzle blocks, or whole gather boxes
+    int tma;     // inverse: gather the modes through the per-parity tensor maps
 };
 inline size_t theta_large_smem_bytes(int Lq, int nhiM, int nloM, int nhiq, int nloq) {
     return static_cast<size_t>((Lq + 7) & ~7) * 16 + static_cast<size_t>(nhiM + nloM + nhiq + nloq) * 16 +
            static_cast<size_t>((Lq + 4 + 1) & ~1) * 8 + 32 * 32 + 2 * 32 + 16 * 16 + 64 * 8 + 4 * 8;
 }
-inline size_t lambda_split_smem_bytes(int Lh, int nhiN, int nloN, int nhih, int nloh) {
-    return static_cast<size_t>((Lh + 7) & ~7) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16;
+inline int lambda_split_slots(int Lh, bool tma) {
+    return tma ? (Lh / kSplitBox + 1) * kSplitBox : ((Lh + 7) & ~7);  // (Lh + 1 modes of the even class)
+}
+inline size_t lambda_split_smem_bytes(int Lh, int nhiN, int nloN, int nhih, int nloh, bool tma = false) {
+    return static_cast<size_t>(lambda_split_slots(Lh, tma)) * 16 + static_cast<size_t>(nhiN + nloN + nhih + nloh) * 16 + 16;
 }
 cudaError_t launch_theta_large(const ThetaLargeParams& P, const CUtensorMap& cmap, int Q, int nthr, size_t smem,
                                cudaStream_t st);
 cudaError_t launch_lambda_fwd_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
-cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_lambda_inv_split(const LambdaSplitParams& P, const CUtensorMap& map0, const CUtensorMap& map1, int nthr,
+                                    size_t smem, cudaStream_t st);
 
 // Complex slots of the theta kernel's data buffer: the raw column (L+1)
 // and whole 8-slot blocks for the swizzled layout.

@@ -165,7 +165,10 @@ void free_fft(DevFft& f) {
 // Tensor map over a mode-major spectrum [rhs][k][p] (complex, rows p
 // contiguous) as a 3-D float64 tensor {2*rows, cols, nrhs}; one box is one
 // row's slice of 256 consecutive modes (box_rows = 2: rows p, p+1 together).
-sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs, int box_rows = 1) {
+// step > 1: the modes first, first + step, ... (count of them) of a spectrum
+// whose right-hand sides are rows * cols entries apart
+sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs, int box_rows = 1, int step = 1,
+                        int first = 0, int count = 0) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -175,11 +178,12 @@ sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nr
             return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled is not available");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * rows), static_cast<cuuint64_t>(cols),
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * rows), static_cast<cuuint64_t>(step > 1 ? count : cols),
                                 static_cast<cuuint64_t>(nrhs)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rows) * 16, static_cast<cuuint64_t>(rows) * cols * 16};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rows) * 16 * step, static_cast<cuuint64_t>(rows) * cols * 16};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * box_rows), 256, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    base = static_cast<char*>(base) + static_cast<size_t>(first) * rows * 16;
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -308,6 +312,7 @@ struct sk_plan_s {
     DevFft ftq, flh;           // local transforms of the cluster-split kernels
     int theta_q = 0;           // 0: CTA-pair theta kernel; Q: 2Q-CTA cluster kernel
     int lambda_split = 0;      // lambda rows split over a CTA pair
+    int lambda_split_tma = 0;  // ... whose inverse gathers its modes through per-parity tensor maps
     int thr_theta = 0, thr_lambda = 0;
     size_t smem_theta = 0, smem_lambda = 0;
     double2* spec = nullptr;   // nrhs * cols * rows complex
@@ -674,8 +679,14 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
                 p->grid_ok = false;
                 p->grid_why = "lambda length " + std::to_string(Ll) + " cannot be split over a CTA pair";
             } else {
+                // the inverse gathers through tensor maps when every thread can hold its
+                // mode pairs in registers and whole gather boxes fit (SK_SPLIT_TMA=0: A/B)
+                const bool want_tma = !std::getenv("SK_SPLIT_TMA") || std::atoi(std::getenv("SK_SPLIT_TMA")) != 0;
+                p->lambda_split_tma = want_tma && Ll / 4 + 1 <= sk::kSplitPairs * 512 &&
+                                      sk::lambda_split_smem_bytes(Ll / 2, p->fl.d.nhi, p->fl.d.nlo, p->flh.d.nhi,
+                                                                  p->flh.d.nlo, true) <= cap;
                 p->smem_lambda = sk::lambda_split_smem_bytes(Ll / 2, p->fl.d.nhi, p->fl.d.nlo, p->flh.d.nhi,
-                                                             p->flh.d.nlo);
+                                                             p->flh.d.nlo, p->lambda_split_tma != 0);
                 if (p->smem_lambda > cap) {
                     p->grid_ok = false;
                     p->grid_why = "lambda length " + std::to_string(Ll) + " exceeds the CTA-pair shared-memory limit";
@@ -961,7 +972,9 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         if (peers) lp.peers = *peers;
         if (p->timing) CU(cudaEventRecord(p->ev[0], p->stream));
         if (p->lambda_split) {
-            sk::LambdaSplitParams sp{lp, p->flh.d};
+            // (measured and not kept at C5: boxed TMA stores of the modes, 12.4 vs 11.8 ms; row pairs on
+            // 4-CTA clusters for 32-byte stores, 12.4 vs 11.3 ms)
+            sk::LambdaSplitParams sp{lp, p->flh.d, sk::lambda_split_slots(p->fl.d.L / 2, p->lambda_split_tma != 0), 0};
             CU(sk::launch_lambda_fwd_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
         } else if (p->lambda_duo && !peers && sk::lambda_duo_ok(lp, p->thr_lambda)) {
             CU(sk::launch_lambda_fwd_duo(lp, p->thr_lambda, p->stream));
@@ -1056,8 +1069,16 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         lp.peers = sk::PeerMap{};
         if (p->timing) CU(cudaEventRecord(p->ev[4], p->stream));
         if (p->lambda_split) {
-            sk::LambdaSplitParams sp{lp, p->flh.d};
-            CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+            sk::LambdaSplitParams sp{lp, p->flh.d, sk::lambda_split_slots(p->fl.d.L / 2, p->lambda_split_tma != 0),
+                                     p->lambda_split_tma};
+            CUtensorMap m0{}, m1{};
+            if (p->lambda_split_tma) {
+                const int Lh = p->fl.d.L / 2;
+                sk_status ms = make_spec_map(&m0, spec, rows_local, p->g.cols, lp.nrhs, 1, 2, 0, Lh + 1);
+                if (ms == SK_OK) ms = make_spec_map(&m1, spec, rows_local, p->g.cols, lp.nrhs, 1, 2, 1, Lh);
+                if (ms != SK_OK) return ms;
+            }
+            CU(sk::launch_lambda_inv_split(sp, m0, m1, p->thr_lambda, p->smem_lambda, p->stream));
         } else if (p->lambda_duo && sk::lambda_duo_ok(lp, p->thr_lambda)) {
             CUtensorMap map;
             sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs, 2);
@@ -1213,8 +1234,15 @@ sk_status sk_shgen(sk_plan_t p, int L, const double* coeffs_dev, double* phys_de
     lp.spec = p->spec;
     lp.u = phys_dev;
     if (p->lambda_split) {
-        sk::LambdaSplitParams sp{lp, p->flh.d};
-        CU(sk::launch_lambda_inv_split(sp, p->thr_lambda, p->smem_lambda, p->stream));
+        sk::LambdaSplitParams sp{lp, p->flh.d, sk::lambda_split_slots(p->fl.d.L / 2, p->lambda_split_tma != 0),
+                                 p->lambda_split_tma};
+        CUtensorMap m0{}, m1{};
+        if (p->lambda_split_tma) {
+            const int Lh = p->fl.d.L / 2;
+            if ((s = make_spec_map(&m0, p->spec, p->g.rows, p->g.cols, 1, 1, 2, 0, Lh + 1)) != SK_OK) return s;
+            if ((s = make_spec_map(&m1, p->spec, p->g.rows, p->g.cols, 1, 1, 2, 1, Lh)) != SK_OK) return s;
+        }
+        CU(sk::launch_lambda_inv_split(sp, m0, m1, p->thr_lambda, p->smem_lambda, p->stream));
     } else {
         CUtensorMap map;
         if ((s = make_spec_map(&map, p->spec, p->g.rows, p->g.cols, 1)) != SK_OK) return s;

@@ -341,6 +341,23 @@ def test_grid_split_kernels_rough_data(pkg, oracle, reference, m, n):
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
 
 
+@pytest.mark.parametrize("m,n,tma", [(64, 32768, "1"), (64, 32768, "0"), (30, 32768, "1"), (18, 36864, "1"),
+                                     (18, 36864, "0"), (16, 20480, "1")])
+def test_lambda_split_gather_paths(pkg, oracle, reference, m, n, tma, monkeypatch):
+    """Rows split over a CTA pair (N/2 beyond one CTA's shared memory): the
+    inverse gathers each CTA's modes (k = c mod 2) through per-parity tensor
+    maps (default when a thread's mode pairs fit its registers), or with
+    per-thread loads (SK_SPLIT_TMA=0, and lengths beyond that limit); rough
+    data against the reference's composition, odd row counts included."""
+    monkeypatch.setenv("SK_SPLIT_TMA", tma)
+    f = zero_mean_noise(oracle, m, n, m + n)
+    X_ref, _, u_ref = ref_grid(reference, f, m)
+    with pkg.Plan(m, n) as plan:
+        u, Xh = plan.solve_grid(f, coeffs=True)
+    assert np.abs(Xh[: n // 2] - X_ref[:, n // 2:].T).max() <= 1e-10 * np.abs(X_ref).max()
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
 @pytest.mark.parametrize("m,n,theta_hi,lambda_hi", [(2048, 1024, True, True), (4096, 2048, True, True),
                                                      (20000, 10000, False, False), (512, 256, True, True)])
 def test_plan_kernel_variants(pkg, m, n, theta_hi, lambda_hi):

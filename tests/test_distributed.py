@@ -170,13 +170,16 @@ def _p2p_worker(rank, world, port, M, N, L, q):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,M,N,L", [(2, 512, 256, 40), (3, 240, 200, 30), (2, 64, 3000, 12),
-                                           (2, 6000, 64, 20), (3, 12000, 48, 16), (2, 32768, 48, 12)])  # theta_sym, multi-pass theta
+                                           (2, 6000, 64, 20), (3, 12000, 48, 16), (2, 32768, 48, 12),
+                                           (2, 48, 32768, 12), (3, 30, 32768, 10)])  # theta_sym, multi-pass theta, split lambda rows
 def test_p2p_fused_transposes_bitwise(world, M, N, L):
     """The fused peer-store slab solve equals the single-GPU grid solve bit
     for bit (the theta stage is slab-invariant); 64 x 3000 runs the forward
     lambda stage on 4-CTA clusters with 64-byte peer stores, 6000 / 12000 x
-    N the theta_sym kernel and 32768 x 48 the multi-pass theta stage with
-    peer stores (the kernels of C3 and C5 on several GPUs)."""
+    N the theta_sym kernel, 32768 x 48 the multi-pass theta stage with peer
+    stores and M x 32768 the lambda rows split over CTA pairs (peer stores
+    forward, the per-parity TMA gather on the rank's own rows inverse): the
+    kernels of C3 and C5 on several GPUs."""
     import torch
     if not torch.cuda.is_available():
         pytest.fail("no CUDA device")

@@ -73,6 +73,8 @@ struct XformParams {
     double2* dst;
     int swizzle;           // XOR-swizzled shared-memory slots (first FFT span even)
     int hiocc;             // high-occupancy variant (<= 256 threads: 64 registers, radices <= 8)
+    int gather;            // sequences are the COLUMNS of src (TMA gather), outputs contiguous rows of ld_out
+    int aslots;            // data slots ahead of the tables (xform_slots)
     // Bluestein (chirp-z) for lengths with a prime factor > 7 (xform_blue_kernel):
     // nb = the DFT length (0: plain transform of length fd.L); fd is then the
     // convolution FFT of length Lb >= 2 nb - 1, chirp[j] = exp(-i pi j^2 / nb),
@@ -204,8 +206,13 @@ cudaError_t launch_lambda_fwd_duo(const LambdaParams& P, int nthr, cudaStream_t 
 cudaError_t launch_lambda_inv_duo(const LambdaParams& P, const CUtensorMap& map, int nthr, cudaStream_t st);
 cudaError_t launch_shgen(const ShgenParams& P, cudaStream_t st);
 cudaError_t launch_assemble(const AssembleParams& P, cudaStream_t st);
-size_t xform_smem_bytes(int n, int nhi, int nlo);
-cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st);
+constexpr int kXformBox = 256;    // elements per gather box
+constexpr int kXformStage = 20;   // gathered elements a thread re-slots through registers (512-thread variant)
+constexpr int kXformStageHi = 8;  // ... of the 64-register variant (<= 256 threads, n <= 2048)
+int xform_slots(int n, int n_src);
+size_t xform_smem_bytes(int n, int nhi, int nlo, int n_src = 0);
+cudaError_t launch_xform(const XformParams& P, const CUtensorMap& map, bool analyze, int nrows, int nthr, size_t smem,
+                         cudaStream_t st);
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st);
 // theta_{m/2} = -pi + 2 pi (m/2) / m evaluated exactly as the reference does
 // (sphere_domain.hpp:54, types.hpp:12-13) is negative: the reference's

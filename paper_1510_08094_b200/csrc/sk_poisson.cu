@@ -1362,29 +1362,74 @@ sk_status xform_blue(sk_plan_t p, int n, const sk_plan_s::BlueFft** out) {
 // One pass: nrows sequences of the input (row stride ld_in) -> transform of
 // length n -> transposed store (output stride ld_out).  Lengths with a prime
 // factor > 7 go through Bluestein (xform_blue_kernel).
+// gather: the sequences are the nrows COLUMNS of the row-major input (n_in
+// rows of ld_in entries), gathered by the copy engine, and each result is
+// stored as the contiguous row dst[r * ld_out ..] (xform_gather_ok).
 sk_status xform_pass(sk_plan_t p, bool analyze, int nrows, int n, int n_in, long long ld_in, const double2* src,
-                     long long ld_out, double2* dst) {
+                     long long ld_out, double2* dst, bool gather = false) {
+    CUtensorMap map{};
     if (!smooth7(n)) {
+        if (gather) return fail(SK_ERR_UNSUPPORTED, "internal: gathered Bluestein pass");
         const sk_plan_s::BlueFft* b = nullptr;
         sk_status s = xform_blue(p, n, &b);
         if (s != SK_OK) return s;
         const int Lb = b->f.d.L;
         sk::XformParams xp{b->f.d, n_in, ld_in, ld_out, src, dst, (b->f.d.nst > 0 && b->f.d.span[0] % 2 == 0) ? 1 : 0,
-                           0, n, b->chirp, analyze ? b->bhat_a : b->bhat_s};
-        CU(sk::launch_xform(xp, analyze, nrows, xform_threads(Lb), sk::xform_smem_bytes(Lb, b->f.d.nhi, b->f.d.nlo),
+                           0, 0, (Lb + 7) & ~7, n, b->chirp, analyze ? b->bhat_a : b->bhat_s};
+        CU(sk::launch_xform(xp, map, analyze, nrows, xform_threads(Lb), sk::xform_smem_bytes(Lb, b->f.d.nhi, b->f.d.nlo),
                             p->stream));
         return SK_OK;
     }
     const DevFft* f = nullptr;
     sk_status s = xform_fft(p, n, &f);
     if (s != SK_OK) return s;
-    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0, 0, 0,
-                       nullptr, nullptr};
+    const int n_src = gather ? (analyze ? n : n_in) : 0;
+    sk::XformParams xp{f->d, n_in, ld_in, ld_out, src, dst, (f->d.nst > 0 && f->d.span[0] % 2 == 0) ? 1 : 0, 0,
+                       gather ? 1 : 0, sk::xform_slots(n, n_src), 0, nullptr, nullptr};
     xp.hiocc = xform_threads(n) <= 256 ? 1 : 0;
     for (int st = 0; st < f->d.nst; ++st)
         if (f->d.R[st] > 8) xp.hiocc = 0;  // the variant only instantiates radices <= 8
-    CU(sk::launch_xform(xp, analyze, nrows, xform_threads(n), sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo), p->stream));
+    if (gather) {
+        s = make_spec_map(&map, const_cast<double2*>(src), static_cast<int>(ld_in), n_src, 1);
+        if (s != SK_OK) return s;
+    }
+    CU(sk::launch_xform(xp, map, analyze, nrows, xform_threads(n), sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo, n_src),
+                        p->stream));
     return SK_OK;
+}
+
+// Can a pass of output length n over n_in inputs run in gather mode: a plain
+// (2, 3, 5, 7)-smooth transform whose thread count re-slots the gathered
+// column through kXformStage registers and whose boxes fit shared memory.
+bool xform_gather_ok(sk_plan_t p, bool analyze, int n, int n_in) {
+    static const bool off = std::getenv("SK_XFORM_GATHER") && std::atoi(std::getenv("SK_XFORM_GATHER")) == 0;
+    if (off || !smooth7(n) || n_in <= 0) return false;
+    const DevFft* f = nullptr;
+    if (xform_fft(p, n, &f) != SK_OK) return false;
+    const int n_src = analyze ? n : n_in;
+    bool hi = xform_threads(n) <= 256;
+    for (int st = 0; st < f->d.nst; ++st)
+        if (f->d.R[st] > 8) hi = false;
+    const bool swz = f->d.nst > 0 && f->d.span[0] % 2 == 0;
+    const bool staged = !analyze || swz;  // (unswizzled analysis transforms the gathered column where it lands)
+    const int stage = hi ? sk::kXformStageHi : sk::kXformStage;
+    return (!staged || std::max(n, n_src) <= stage * xform_threads(n)) &&
+           sk::xform_smem_bytes(n, f->d.nhi, f->d.nlo, n_src) <= 227 * 1024;
+}
+
+// The separable 2-D transform of a rows x cols row-major input into an
+// m_out x n_out row-major output through the cols x m_out intermediate T
+// (gather passes: theta direction first, every store contiguous), or through
+// the n_out x rows intermediate of the transposed-store passes.
+sk_status xform_2d(sk_plan_t p, bool analyze, int rows, int cols, int m_out, int n_out, const double2* src, double2* T,
+                   double2* dst) {
+    sk_status s;
+    if (xform_gather_ok(p, analyze, m_out, rows) && xform_gather_ok(p, analyze, n_out, cols)) {
+        if ((s = xform_pass(p, analyze, cols, m_out, rows, cols, src, m_out, T, true)) != SK_OK) return s;   // theta
+        return xform_pass(p, analyze, m_out, n_out, cols, m_out, T, n_out, dst, true);                     // lambda
+    }
+    if ((s = xform_pass(p, analyze, rows, n_out, cols, cols, src, rows, T)) != SK_OK) return s;  // lambda, transposed
+    return xform_pass(p, analyze, n_out, m_out, rows, rows, T, n_out, dst);                     // theta, transposed
 }
 
 }  // namespace
@@ -1607,8 +1652,7 @@ sk_status sk_analyze_2d(sk_plan_t p, int m, int n, const double* grid, double* X
     if ((s = scratch(p, 1, sizeof(double2) * mn * ((flags & SK_DEVICE) ? 1 : 2), &t)) != SK_OK) return s;
     double2* T = static_cast<double2*>(t);  // lambda-analysed rows, transposed: n x m
     double2* out = (flags & SK_DEVICE) ? reinterpret_cast<double2*>(X) : T + mn;
-    if ((s = xform_pass(p, true, m, n, n, n, g, m, T)) != SK_OK) return s;    // rows j: lambda direction
-    if ((s = xform_pass(p, true, n, m, m, m, T, n, out)) != SK_OK) return s;  // columns kc: theta direction
+    if ((s = xform_2d(p, true, m, n, m, n, g, T, out)) != SK_OK) return s;
     p->last_launches = 2;
     if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(X, out, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
     if (!(flags & SK_ASYNC) || !(flags & SK_DEVICE)) CU(cudaStreamSynchronize(p->stream));
@@ -1626,7 +1670,7 @@ sk_status sk_sample_grid(sk_plan_t p, int rows, int cols, const double* X, int m
     const size_t nx = static_cast<size_t>(rows) * cols, ng = static_cast<size_t>(m_out) * n_out;
     const double2* x = nullptr;
     if ((s = stage_in(p, X, sizeof(double2) * nx, flags, 0, reinterpret_cast<const void**>(&x))) != SK_OK) return s;
-    const size_t nt = static_cast<size_t>(rows) * n_out;
+    const size_t nt = std::max(static_cast<size_t>(rows) * n_out, static_cast<size_t>(cols) * m_out);
     void* t = nullptr;
     if ((s = scratch(p, 1, sizeof(double2) * (nt + ((flags & SK_DEVICE) ? 0 : ng)), &t)) != SK_OK) return s;
     double2* T = static_cast<double2*>(t);  // lambda-synthesised rows, transposed: n_out x rows
@@ -1634,8 +1678,7 @@ sk_status sk_sample_grid(sk_plan_t p, int rows, int cols, const double* X, int m
     if (rows == 0) {
         CU(cudaMemsetAsync(out, 0, sizeof(double2) * ng, p->stream));
     } else {
-        if ((s = xform_pass(p, false, rows, n_out, cols, cols, x, rows, T)) != SK_OK) return s;      // lambda
-        if ((s = xform_pass(p, false, n_out, m_out, rows, rows, T, n_out, out)) != SK_OK) return s;  // theta
+        if ((s = xform_2d(p, false, rows, cols, m_out, n_out, x, T, out)) != SK_OK) return s;
     }
     p->last_launches = 2;
     if (!(flags & SK_DEVICE)) CU(cudaMemcpyAsync(grid, out, sizeof(double2) * ng, cudaMemcpyDeviceToHost, p->stream));
@@ -1700,16 +1743,14 @@ sk_status sk_solve_grid_exact(sk_plan_t p, const double* f, double* U, double* X
             df = static_cast<const double*>(in);
         }
         CU(sk::launch_dfs_double(M, N, df, G, p->stream));                            // sample_dfs
-        if ((s = xform_pass(p, true, M, N, N, N, G, M, T)) != SK_OK) return s;          // analyze: lambda rows
-        if ((s = xform_pass(p, true, N, M, M, M, T, N, G)) != SK_OK) return s;          // analyze: theta columns
+        if ((s = xform_2d(p, true, M, N, M, N, G, T, G)) != SK_OK) return s;            // analyze_2d
         CU(sk::launch_msin2(M, N, G, T, p->stream));                                    // F = Msin^2 A
         double2* dX = (dev && X) ? reinterpret_cast<double2*>(X) + r * mn : G;
         sk::CoeffParams cp{M, N, 1, T, dX, p->D, p->D + mn, p->D + 2 * mn, p->stats + 4 * r, p->z};
         CU(sk::launch_coeff_solve(cp, p->stream));                                      // solve
         if (!dev && X) CU(cudaMemcpyAsync(X + 2 * r * mn, dX, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
         double2* dU = dev ? reinterpret_cast<double2*>(U) + r * mn : H;
-        if ((s = xform_pass(p, false, M, N, N, N, dX, M, T)) != SK_OK) return s;        // sample_grid: lambda
-        if ((s = xform_pass(p, false, N, M, M, M, T, N, dU)) != SK_OK) return s;        // sample_grid: theta
+        if ((s = xform_2d(p, false, M, N, M, N, dX, T, dU)) != SK_OK) return s;         // sample_grid
         if (!dev) CU(cudaMemcpyAsync(U + 2 * r * mn, dU, sizeof(double2) * mn, cudaMemcpyDeviceToHost, p->stream));
         p->last_launches += 9;
     }

@@ -19,6 +19,7 @@
 #include "fft_dev.cuh"
 #include "params.h"
 #include "sk_internal.h"
+#include "tma.cuh"
 
 namespace sk {
 
@@ -30,15 +31,87 @@ namespace sk {
 // lengths, where the butterflies of a stage otherwise share one bank).
 // HI: high-occupancy variant for short transforms (<= 256 threads, radices <= 8).
 template <bool ANALYZE, bool SWZ, bool HI>
-__global__ void __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) xform_kernel(XformParams P) {
+__global__ void __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1)
+    xform_kernel(XformParams P, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int n = P.fd.L;  // transform length (n for ANALYZE, n_out for SYNTH)
     double2* a = reinterpret_cast<double2*>(smem_raw);
-    double2* s_hi = a + ((n + 7) & ~7);  // whole 8-slot swizzle blocks
+    double2* s_hi = a + P.aslots;  // whole 8-slot swizzle blocks (gather: whole boxes)
     double2* s_lo = s_hi + P.fd.nhi;
     int* s_rev = reinterpret_cast<int*>(s_lo + P.fd.nlo);
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int r = blockIdx.x;
+    if (P.gather) {
+        // Sequence r is COLUMN r of the row-major input (element j at
+        // src[j ld_in + r]): the copy engine gathers it as boxes of 256
+        // elements through the tensor map, and the result leaves as one
+        // contiguous row dst[r ld_out ..].  The transposition sits on the load
+        // side: gathered 16-byte loads run several times faster here than
+        // per-thread 16-byte stores one row apart.
+        uint64_t* bar = reinterpret_cast<uint64_t*>(s_rev + ((n + 3) & ~3));
+        const int n_src = ANALYZE ? n : P.n_in;
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const int nbox = (n_src + kXformBox - 1) / kXformBox;
+            mbar_expect_tx(bar, static_cast<uint32_t>(nbox) * kXformBox * 16);
+            for (int b = 0; b < nbox; ++b) tma_load_3d(a + b * kXformBox, &tmap, 2 * r, b * kXformBox, 0, bar);
+        }
+        const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
+        for (int i = tid; i < n; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
+        __syncthreads();
+        mbar_wait(bar, 0);
+        double2* out = P.dst + static_cast<long long>(r) * P.ld_out;
+        constexpr int kStage = HI ? kXformStageHi : kXformStage;
+        double2 v[kStage];
+        if constexpr (ANALYZE) {
+            if constexpr (SWZ) {  // natural slots -> swizzled slots through registers
+#pragma unroll
+                for (int u = 0; u < kStage; ++u) {
+                    const int j = tid + u * nthr;
+                    if (j < n) v[u] = a[j];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < kStage; ++u) {
+                    const int j = tid + u * nthr;
+                    if (j < n) a[swz<SWZ>(j)] = v[u];
+                }
+                __syncthreads();
+            }
+            fft_forward<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);  // X_t at a[swz(rev[t])]
+            const double inv = 1.0 / n;
+            for (int kp = tid; kp < n; kp += nthr) {
+                const int k = kp - n / 2;
+                const int t = k < 0 ? k + n : k;
+                const double s = (k % 2 == 0) ? inv : -inv;
+                const double2 x = a[swz<SWZ>(s_rev[t])];
+                out[kp] = make_double2(s * x.x, s * x.y);
+            }
+        } else {
+            const int lo = max(-P.n_in / 2, -n / 2), hi = min(P.n_in / 2, n / 2);
+#pragma unroll
+            for (int u = 0; u < kStage; ++u) {
+                const int k = lo + tid + u * nthr;
+                if (k < hi) v[u] = a[k + P.n_in / 2];
+            }
+            __syncthreads();
+            for (int j = tid; j < n; j += nthr) a[swz<SWZ>(j)] = make_double2(0.0, 0.0);
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < kStage; ++u) {
+                const int k = lo + tid + u * nthr;
+                if (k < hi) {
+                    const int t = k < 0 ? k + n : k;
+                    a[swz<SWZ>(s_rev[t])] = (k % 2 == 0) ? v[u] : make_double2(-v[u].x, -v[u].y);  // DIT input: digit-reversed
+                }
+            }
+            __syncthreads();
+            fft_inverse<SWZ, HI ? 8 : 25>(a, P.fd, T, tid, nthr);  // natural order
+            for (int j = tid; j < n; j += nthr) out[j] = a[swz<SWZ>(j)];
+        }
+        return;
+    }
     const double2* src = P.src + static_cast<long long>(r) * P.ld_in;
     const Tw T = load_tw(P.fd, s_hi, s_lo, tid, nthr);
     for (int i = tid; i < n; i += nthr) s_rev[i] = __ldg(P.fd.rev + i);
@@ -194,21 +267,30 @@ __global__ void dfs_double_kernel(int m, int n, const double* phys, double2* gri
     grid[idx] = make_double2(v, 0.0);
 }
 
-size_t xform_smem_bytes(int n, int nhi, int nlo) {
-    return static_cast<size_t>((n + 7) & ~7) * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>(n) * 4;
+// n_src > 0: gather mode, the data slots hold whole boxes of the n_src-element input column
+int xform_slots(int n, int n_src) {
+    const int s = (n + 7) & ~7;
+    return n_src > 0 ? max(s, (n_src + kXformBox - 1) / kXformBox * kXformBox) : s;
+}
+size_t xform_smem_bytes(int n, int nhi, int nlo, int n_src) {
+    return static_cast<size_t>(xform_slots(n, n_src)) * 16 + static_cast<size_t>(nhi + nlo) * 16 +
+           static_cast<size_t>((n + 3) & ~3) * 4 + 16;
 }
 
 template <bool ANALYZE, bool SWZ, bool HI>
-static cudaError_t launch_xform_t(const XformParams& P, int nrows, int nthr, size_t smem, cudaStream_t st) {
+static cudaError_t launch_xform_t(const XformParams& P, const CUtensorMap& map, int nrows, int nthr, size_t smem,
+                                  cudaStream_t st) {
     static std::atomic<unsigned long long> attr{0};
     configure_on_device(attr, [] {
         cudaFuncSetAttribute(xform_kernel<ANALYZE, SWZ, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
-    xform_kernel<ANALYZE, SWZ, HI><<<nrows, nthr, smem, st>>>(P);
+    xform_kernel<ANALYZE, SWZ, HI><<<nrows, nthr, smem, st>>>(P, map);
     return cudaGetLastError();
 }
 
-cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr, size_t smem, cudaStream_t st) {
+// map: the input as a column-gather tensor map (make_spec_map), read when P.gather
+cudaError_t launch_xform(const XformParams& P, const CUtensorMap& map, bool analyze, int nrows, int nthr, size_t smem,
+                         cudaStream_t st) {
     if (nrows <= 0) return cudaSuccess;
     if (P.nb) {
         if (analyze) return P.swizzle ? launch_blue_t<true, true>(P, nrows, nthr, smem, st)
@@ -218,15 +300,15 @@ cudaError_t launch_xform(const XformParams& P, bool analyze, int nrows, int nthr
     }
     const bool hi = P.hiocc && nthr <= 256;
     if (analyze) {
-        if (hi) return P.swizzle ? launch_xform_t<true, true, true>(P, nrows, nthr, smem, st)
-                                 : launch_xform_t<true, false, true>(P, nrows, nthr, smem, st);
-        return P.swizzle ? launch_xform_t<true, true, false>(P, nrows, nthr, smem, st)
-                         : launch_xform_t<true, false, false>(P, nrows, nthr, smem, st);
+        if (hi) return P.swizzle ? launch_xform_t<true, true, true>(P, map, nrows, nthr, smem, st)
+                                 : launch_xform_t<true, false, true>(P, map, nrows, nthr, smem, st);
+        return P.swizzle ? launch_xform_t<true, true, false>(P, map, nrows, nthr, smem, st)
+                         : launch_xform_t<true, false, false>(P, map, nrows, nthr, smem, st);
     }
-    if (hi) return P.swizzle ? launch_xform_t<false, true, true>(P, nrows, nthr, smem, st)
-                             : launch_xform_t<false, false, true>(P, nrows, nthr, smem, st);
-    return P.swizzle ? launch_xform_t<false, true, false>(P, nrows, nthr, smem, st)
-                     : launch_xform_t<false, false, false>(P, nrows, nthr, smem, st);
+    if (hi) return P.swizzle ? launch_xform_t<false, true, true>(P, map, nrows, nthr, smem, st)
+                             : launch_xform_t<false, false, true>(P, map, nrows, nthr, smem, st);
+    return P.swizzle ? launch_xform_t<false, true, false>(P, map, nrows, nthr, smem, st)
+                     : launch_xform_t<false, false, false>(P, map, nrows, nthr, smem, st);
 }
 
 cudaError_t launch_dfs_double(int m, int n, const double* phys, double2* grid, cudaStream_t st) {

@@ -120,6 +120,43 @@ def test_transforms_vs_oracle_and_round_trip(pkg, oracle, m, n):
     assert _rel(pkg.sample_grid(X, m, n), g) <= 1e-13
 
 
+@pytest.mark.parametrize("m,n,gather", [(64, 10000, "1"), (10000, 48, "1"), (96, 8192, "1"), (8192, 64, "1"),
+                                        (48, 9000, "1"), (1000, 700, "0"), (96, 8192, "0"), (6, 10, "0")])
+def test_transforms_gather_and_transposed_passes(pkg, oracle, m, n, gather, monkeypatch):
+    """The two pass structures of the 2-D transforms: columns gathered by the
+    copy engine with contiguous stores (default when both lengths are plain
+    smooth transforms whose columns fit the register staging: 20 elements per
+    thread, unswizzled analysis unstaged) and row loads with transposed stores
+    (SK_XFORM_GATHER=0, Bluestein lengths); against the
+    oracle, zero-padded / truncated synthesis and the round trip."""
+    import subprocess, sys, json, os, textwrap
+    # the switch is read once per process: run the case in a child
+    code = textwrap.dedent(f"""
+        import sys, json
+        import numpy as np
+        sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+        import paper_1510_08094_b200 as pkg
+        from oracle.oracle import Oracle
+        o = Oracle()
+        m, n = {m}, {n}
+        rng = np.random.default_rng(m + n)
+        g = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+        rel = lambda a, b: float(np.abs(a - b).max() / np.abs(b).max())
+        X = pkg.analyze_2d(g)
+        out = dict(analyze=rel(X, o.analyze_2d(g)), round_trip=rel(pkg.sample_grid(X, m, n), g))
+        mo = 2 * m if m <= 4000 else m // 2
+        no = n // 2 if n % 4 == 0 else n
+        out["resample"] = rel(pkg.sample_grid(X, mo, no), o.sample_grid(X, mo, no))
+        print(json.dumps(out))
+    """)
+    env = dict(os.environ, SK_XFORM_GATHER=gather)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["analyze"] <= 1e-14, out
+    assert out["round_trip"] <= 1e-13 and out["resample"] <= 1e-13, out
+
+
 def test_transforms_device_tensors(pkg):
     import torch
     rng = np.random.default_rng(3)

@@ -120,6 +120,12 @@ __global__ void __launch_bounds__(256, HI ? 4 : 2) lambda_fwd_kernel(LambdaParam
         if (P.peers.n) {  // fused transpose: store into the theta rank's receive buffer over NVLink
             *peer_ptr(P.peers, k, k, row) = vk;
             if (km != k) *peer_ptr(P.peers, km, km, row) = vm;
+        } else if (P.pair & 8) {
+            // row-major spectrum R[rhs][p][k]: the row's modes are contiguous, adjacent lanes write
+            // adjacent modes (k ascending, L - k descending); the theta stage gathers its columns
+            double2* rr = P.spec + (static_cast<size_t>(rhs) * P.rows_local + row) * (L + 1);
+            rr[k] = vk;
+            if (km != k) rr[km] = vm;
         } else {
             out[static_cast<size_t>(k) * P.rows_local + row] = vk;
             if (km != k) out[static_cast<size_t>(km) * P.rows_local + row] = vm;
@@ -1281,7 +1287,9 @@ __device__ void solve_chain_seq(double2* a, const int* rev, const double* ip, co
 // <= 8): 64 registers per thread, so twice the CTAs per SM hide the latency of
 // a transform that gives each thread only one or two butterflies per stage.
 template <bool SWZ, int CH, bool HI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1) theta_kernel(ThetaParams P, int relaxed_exit) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ? 4 : 1)
+    theta_kernel(ThetaParams P, int relaxed_exit, const __grid_constant__ CUtensorMap cmap,
+                 const __grid_constant__ CUtensorMap cmap_tail) {
     constexpr int kFold = HI ? kFoldMaxHi : kFoldMax;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -1331,12 +1339,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HI ? 256 : 512, HI ?
         int ra0 = 0;
         uint32_t rbytes = 0;
         if (P.rev_win) rev_window(rw, cp.tau0, cp.tau0 + cp.n, ra0, rbytes);
+        if (P.gather) bytes = static_cast<uint32_t>(P.gather_nbox * 256 + P.gather_tail) * 16;
         mbar_expect_tx(&bars[0], bytes + pb + rbytes);
         if (rbytes) bulk_g2s_chunked(rw, P.fd.rev + ra0, rbytes, &bars[0]);
-        for (int s = 0; s < P.sl.P; ++s) {
-            const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
-            if (r1 > r0)
-                bulk_g2s_chunked(a + r0, colbase + theta_addr(P.sl, P.ncols, kl, r0), (r1 - r0) * 16, &bars[0]);
+        if (P.gather) {
+            // column kl of the row-major spectrum R[rhs][p][k] (lambda_fwd_kernel's contiguous rows):
+            // gather_nbox boxes of 256 rows and a tail box (a multiple of 8 rows: 128-byte destinations),
+            // 16 bytes per row, through the two tensor maps; rows past M/2 are zero-filled
+            for (int b = 0; b < P.gather_nbox; ++b) tma_load_3d(a + b * 256, &cmap, 2 * kl, b * 256, rhs, &bars[0]);
+            if (P.gather_tail)
+                tma_load_3d(a + P.gather_nbox * 256, &cmap_tail, 2 * kl, P.gather_nbox * 256, rhs, &bars[0]);
+        } else {
+            for (int s = 0; s < P.sl.P; ++s) {
+                const int r0 = P.sl.row_b[s], r1 = P.sl.row_b[s + 1];
+                if (r1 > r0)
+                    bulk_g2s_chunked(a + r0, colbase + theta_addr(P.sl, P.ncols, kl, r0), (r1 - r0) * 16, &bars[0]);
+            }
         }
         const size_t a0 = (prow + cp.tau0) & ~static_cast<size_t>(1);
         if (pb) bulk_g2s_chunked(ip, P.pivots + a0, pb, &bars[0]);
@@ -1646,6 +1664,13 @@ bool lambda_quad_ok(const LambdaParams& P, int nthr) {
     return !P.swizzle && !P.hiocc && P.nrhs == 1 && nthr <= 256 && P.fd.L / 2 + 1 <= kLamPairs * nthr;
 }
 cudaError_t launch_lambda_fwd(const LambdaParams& P, const CUtensorMap& map, int nthr, size_t smem, cudaStream_t st) {
+    if (P.pair & 8) {  // row-major spectrum: the per-row kernel, contiguous stores
+        if (P.hiocc)
+            return P.swizzle ? launch_lambda_fwd_t<true, true>(P, map, nthr, smem, st)
+                             : launch_lambda_fwd_t<false, true>(P, map, nthr, smem, st);
+        return P.swizzle ? launch_lambda_fwd_t<true, false>(P, map, nthr, smem, st)
+                         : launch_lambda_fwd_t<false, false>(P, map, nthr, smem, st);
+    }
     if ((P.pair & 4) && lambda_quad_ok(P, nthr)) {
         static std::atomic<unsigned long long> attr{0};
         configure_on_device(attr, [] {
@@ -1699,28 +1724,31 @@ cudaError_t launch_lambda_inv(const LambdaParams& P, const CUtensorMap& map, int
 }
 
 template <bool SWZ, int CH, bool HI = false>
-static cudaError_t launch_theta_t(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
+static cudaError_t launch_theta_t(const ThetaParams& P, const CUtensorMap& cmap, const CUtensorMap& ctail, int nthr,
+                                  size_t smem, cudaStream_t st) {
     static std::atomic<unsigned long long> attr{0};
     configure_on_device(attr, [] {
         cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(theta_kernel<SWZ, CH, HI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
-    theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P, exit_relaxed());
+    theta_kernel<SWZ, CH, HI><<<2 * P.ncols * P.nrhs, nthr, smem, st>>>(P, exit_relaxed(), cmap, ctail);
     return cudaGetLastError();
 }
 
-cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st) {
+// cmap / ctail: the row-major spectrum as column-gather tensor maps (boxes of 256 rows / the tail box; read when P.gather)
+cudaError_t launch_theta(const ThetaParams& P, const CUtensorMap& cmap, const CUtensorMap& ctail, int nthr, size_t smem,
+                         cudaStream_t st) {
     const int ch = P.regsolve;  // chain solver chosen by the plan
     if (P.hiocc && ch == 1 && nthr <= 256)  // short columns (plan: radices <= 8, fixed-segment chains)
-        return P.swizzle ? launch_theta_t<true, 1, true>(P, nthr, smem, st) : launch_theta_t<false, 1, true>(P, nthr, smem, st);
+        return P.swizzle ? launch_theta_t<true, 1, true>(P, cmap, ctail, nthr, smem, st) : launch_theta_t<false, 1, true>(P, cmap, ctail, nthr, smem, st);
     if (P.swizzle) {
-        if (ch == 2) return launch_theta_t<true, 2>(P, nthr, smem, st);
-        if (ch == 1) return launch_theta_t<true, 1>(P, nthr, smem, st);
-        return launch_theta_t<true, 0>(P, nthr, smem, st);
+        if (ch == 2) return launch_theta_t<true, 2>(P, cmap, ctail, nthr, smem, st);
+        if (ch == 1) return launch_theta_t<true, 1>(P, cmap, ctail, nthr, smem, st);
+        return launch_theta_t<true, 0>(P, cmap, ctail, nthr, smem, st);
     }
-    if (ch == 2) return launch_theta_t<false, 2>(P, nthr, smem, st);
-    if (ch == 1) return launch_theta_t<false, 1>(P, nthr, smem, st);
-    return launch_theta_t<false, 0>(P, nthr, smem, st);
+    if (ch == 2) return launch_theta_t<false, 2>(P, cmap, ctail, nthr, smem, st);
+    if (ch == 1) return launch_theta_t<false, 1>(P, cmap, ctail, nthr, smem, st);
+    return launch_theta_t<false, 0>(P, cmap, ctail, nthr, smem, st);
 }
 
 cudaError_t launch_pivot_table(int L, int k0, int ncols, double* ipt, int stride, cudaStream_t st) {

@@ -26,6 +26,7 @@ struct LambdaParams {
     int hiocc;          // high-occupancy kernel variant (short rows: 64 registers, radices <= 8)
     int pair;           // bit 0 fwd, bit 1 inv: row pairs on CTA pairs, 32-byte (p, p+1) segments (lambda_pair_ok decides);
                         // bit 2 fwd: row quads on 4-CTA clusters, 64-byte (p .. p+3) segments (lambda_quad_ok)
+                        // bit 3 fwd: spec is the row-major spectrum R[rhs][p][k], contiguous row stores (K1)
 };
 
 struct ThetaParams {
@@ -45,6 +46,9 @@ struct ThetaParams {
     int swizzle;           // XOR-swizzled data slots (plans whose first FFT span is even)
     int piv_stride;        // doubles per (mode, parity) pivot row
     int pair_chains;       // theta_kernel segment solver: both chains of a parity from one solve (solve_chains_pair_fast)
+    int gather;            // theta_kernel: the raw column is gathered from the row-major spectrum R[rhs][p][k]
+    int gather_nbox;       // ... as gather_nbox tensor-map boxes of 256 rows
+    int gather_tail;       // ... and one tail box of gather_tail rows (a multiple of 8; together theta_data_slots)
     PeerMap peers;         // row p of the solved columns goes straight to its lambda rank's return buffer
     int rev_win;           // stage each chain's digit-reversal entries in shared memory (bulk copy)
     int hiocc;             // high-occupancy kernel variant (short columns: 64 registers, radices <= 8)
@@ -198,7 +202,8 @@ inline size_t lambda_smem_bytes(int L, int nhi, int nlo) {
     const size_t lpad = static_cast<size_t>((L / 256 + 1) * 256);
     return lpad * 16 + static_cast<size_t>(nhi + nlo) * 16 + static_cast<size_t>((L + 3) & ~3) * 4 + 32;
 }
-cudaError_t launch_theta(const ThetaParams& P, int nthr, size_t smem, cudaStream_t st);
+cudaError_t launch_theta(const ThetaParams& P, const CUtensorMap& cmap, const CUtensorMap& ctail, int nthr, size_t smem,
+                         cudaStream_t st);
 // lambda stages on row pairs inside one CTA (lambda_duo.cu); nthr = threads per row
 size_t lambda_duo_smem_bytes(int L, int nhi, int nlo);
 bool lambda_duo_ok(const LambdaParams& P, int nthr);

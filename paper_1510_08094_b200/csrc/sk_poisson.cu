@@ -168,7 +168,7 @@ void free_fft(DevFft& f) {
 // step > 1: the modes first, first + step, ... (count of them) of a spectrum
 // whose right-hand sides are rows * cols entries apart
 sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nrhs, int box_rows = 1, int step = 1,
-                        int first = 0, int count = 0) {
+                        int first = 0, int count = 0, int box_modes = 256) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -181,7 +181,7 @@ sk_status make_spec_map(CUtensorMap* map, void* base, int rows, int cols, int nr
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * rows), static_cast<cuuint64_t>(step > 1 ? count : cols),
                                 static_cast<cuuint64_t>(nrhs)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rows) * 16 * step, static_cast<cuuint64_t>(rows) * cols * 16};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * box_rows), 256, 1};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * box_rows), static_cast<cuuint32_t>(box_modes), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     base = static_cast<char*>(base) + static_cast<size_t>(first) * rows * 16;
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
@@ -316,6 +316,8 @@ struct sk_plan_s {
     int thr_theta = 0, thr_lambda = 0;
     size_t smem_theta = 0, smem_lambda = 0;
     double2* spec = nullptr;   // nrhs * cols * rows complex
+    double2* spec_rows = nullptr;  // nrhs * rows * cols complex: the row-major spectrum R[rhs][p][k] (fwd_rows)
+    int fwd_rows = 0;          // single-GPU solves on theta_kernel: lambda_fwd writes contiguous rows of R, theta gathers
     double* stats = nullptr;   // 4 * nrhs
     double2* z = nullptr;      // mean weights, M complex
     double* D = nullptr;       // coefficient solve: per-plan pivots d' (M x N), multipliers l behind them (M x N),
@@ -663,6 +665,11 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     if (const char* e = std::getenv("SK_LAMBDA_QUAD")) p->lambda_quad = std::atoi(e) != 0 ? 1 : 0;  // A/B
     if (const char* e = std::getenv("SK_LAMBDA_PAIR_INV")) p->lambda_pair_inv = std::atoi(e) != 0;  // opt-in A/B
     if (const char* e = std::getenv("SK_LAMBDA_DUO")) p->lambda_duo = std::atoi(e) != 0;  // A/B
+    // row-major forward spectrum + gathered theta columns (run_grid): on for large batches of short
+    // columns, where several theta CTAs per SM hide the gather (C4 2.48 -> 2.43 ms; C2 -0.8 %, C1 +1.4 %,
+    // C3's one-CTA-per-SM theta_sym +3 %: profiles/r2_phases_c3.md); SK_FWD_ROWS=0/1 forces it
+    p->fwd_rows = p->theta_hiocc && static_cast<size_t>(p->nrhs) * p->g.rows * p->g.cols >= (static_cast<size_t>(1) << 24);
+    if (const char* e = std::getenv("SK_FWD_ROWS")) p->fwd_rows = std::atoi(e) != 0;      // A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;
         p->grid_why = g_err;
@@ -765,6 +772,7 @@ sk_status sk_plan_destroy(sk_plan_t p) {
     free_fft(p->fm2);
     if (p->mp_w1) cudaFree(p->mp_w1);
     if (p->mp_w2) cudaFree(p->mp_w2);
+    if (p->spec_rows) cudaFree(p->spec_rows);
     for (void* q : {static_cast<void*>(p->spec), static_cast<void*>(p->stats), static_cast<void*>(p->z),
                     static_cast<void*>(p->D), static_cast<void*>(p->hF), static_cast<void*>(p->hX),
                     static_cast<void*>(p->hf), static_cast<void*>(p->hu), static_cast<void*>(p->rbuf),
@@ -878,6 +886,8 @@ sk_status sk_plan_info(sk_plan_t p, long long info[16]) {
         sk::lambda_duo_smem_bytes(p->g.Ll, p->fl.d.nhi, p->fl.d.nlo) <= 227 * 1024)
         info[13] |= 512;  // lambda stages on row pairs inside one CTA (lambda_duo_ok; the forward one for local stores)
     if (p->theta_sym) info[13] |= 64;  // theta_sym_kernel
+    if (p->fwd_rows && !p->theta_sym && !p->theta_q && !p->theta_mp && !p->lambda_split && !p->lambda_duo)
+        info[13] |= 1024;  // row-major forward spectrum, theta_kernel gathers its columns (single-GPU solves)
     if (p->theta_mp) info[13] |= 256;  // multi-pass theta stage (theta_mp.cu)
     if (p->grid_ok && p->lambda_quad != 0 && !p->lambda_split && !swz_l && !hi_l && p->nrhs == 1 &&
         p->thr_lambda <= 256 && p->N / 4 + 1 <= 12 * p->thr_lambda)
@@ -964,6 +974,15 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
     lp.pair = (p->lambda_pair ? 1 : 0) | ((p->lambda_quad == 1 || (p->lambda_quad < 0 && peers)) ? 4 : 0);
     lp.rows_local = rows_local;
     lp.nrhs = (sl.P == 1) ? p->nrhs : 1;
+    // row-major forward spectrum + gathered theta columns: whole single-GPU solves on theta_kernel
+    bool fwd_rows = false;
+    if (p->fwd_rows && sl.P == 1 && !peers && (stages & 3) == 3 && !p->theta_sym && !p->theta_q &&
+        !p->theta_mp && !p->lambda_split && !p->lambda_duo) {
+        const sk_status es =
+            ensure(reinterpret_cast<void**>(&p->spec_rows), sizeof(double2) * p->nrhs * p->g.rows * p->g.cols);
+        if (es != SK_OK) return es;
+        fwd_rows = true;
+    }
     if (stages & 1) {
         lp.in_rhs_stride = static_cast<long long>(rows_local) * p->N;
         lp.out_rhs_stride = static_cast<long long>(rows_local) * p->g.cols;
@@ -982,7 +1001,13 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
             CUtensorMap map;
             sk_status ms = make_spec_map(&map, spec, rows_local, p->g.cols, lp.nrhs);
             if (ms != SK_OK) return ms;
+            if (fwd_rows) {
+                lp.pair |= 8;
+                lp.spec = p->spec_rows;
+            }
             CU(sk::launch_lambda_fwd(lp, map, p->thr_lambda, p->smem_lambda, p->stream));
+            lp.pair &= ~8;
+            lp.spec = spec;
         }
         if (p->timing) {
             CU(cudaEventRecord(p->ev[1], p->stream));
@@ -1052,7 +1077,20 @@ static sk_status run_grid(sk_plan_t p, const sk::Slabs& sl, int rows_local, int 
         } else if (p->theta_sym) {
             CU(sk::launch_theta_sym(tp, p->thr_theta, p->smem_theta, p->stream));
         } else {
-            CU(sk::launch_theta(tp, p->thr_theta, p->smem_theta, p->stream));
+            CUtensorMap cmap{}, ctail{};
+            if (fwd_rows) {
+                // column k of R[rhs][p][k]: the fast dimension holds the N/2+1 modes, one box = 256 rows p
+                // (the tail box rounds M/2 + 1 up to theta_data_slots: every box lands 128-byte aligned)
+                tp.gather = 1;
+                tp.gather_nbox = p->g.rows / 256;
+                tp.gather_tail = sk::theta_data_slots(p->g.Lt) - tp.gather_nbox * 256;
+                sk_status ms = SK_OK;
+                if (tp.gather_nbox) ms = make_spec_map(&cmap, p->spec_rows, p->g.cols, p->g.rows, tp.nrhs);
+                if (ms == SK_OK && tp.gather_tail)
+                    ms = make_spec_map(&ctail, p->spec_rows, p->g.cols, p->g.rows, tp.nrhs, 1, 1, 0, 0, tp.gather_tail);
+                if (ms != SK_OK) return ms;
+            }
+            CU(sk::launch_theta(tp, cmap, ctail, p->thr_theta, p->smem_theta, p->stream));
         }
         if (p->timing) {
             CU(cudaEventRecord(p->ev[3], p->stream));

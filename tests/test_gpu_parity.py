@@ -368,6 +368,41 @@ def test_plan_kernel_variants(pkg, m, n, theta_hi, lambda_hi):
     assert bool(v & 1) == theta_hi and bool(v & 2) == lambda_hi, v
 
 
+@pytest.mark.parametrize("m,n,nrhs", [(512, 256, 1), (2048, 1024, 3), (60, 32, 2), (1000, 360, 1), (4096, 64, 2),
+                                        (500, 48, 1), (20, 24, 1), (1536, 40, 1)])
+def test_fwd_rows_gather_bitwise(pkg, oracle, reference, m, n, nrhs, monkeypatch):
+    """The row-major forward spectrum (lambda_fwd writes each row's modes
+    contiguously, theta_kernel gathers its raw column through two tensor maps:
+    boxes of 256 rows and the tail box; default for large batches of short
+    columns, C4) against the mode-major stores: the same values take another
+    route, so the solves agree bit for bit (several RHS, row counts with every
+    tail-box size, swizzled and unswizzled plans), and against the reference."""
+    f = np.stack([zero_mean_noise(oracle, m, n, 3 * m + n + r) for r in range(nrhs)])
+    fin = f if nrhs > 1 else f[0]
+    monkeypatch.setenv("SK_FWD_ROWS", "1")
+    with pkg.Plan(m, n, nrhs) as plan:
+        assert plan.info()["variants"] & 1024, plan.info()
+        u1 = plan.solve_grid(fin)
+    monkeypatch.setenv("SK_FWD_ROWS", "0")
+    with pkg.Plan(m, n, nrhs) as plan:
+        assert not plan.info()["variants"] & 1024
+        u0 = plan.solve_grid(fin)
+    assert np.array_equal(u0, u1)
+    _, _, u_ref = ref_grid(reference, f[0], m)
+    assert np.abs((u1[0] if nrhs > 1 else u1) - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+def test_fwd_rows_default_policy(pkg):
+    """On for large batches of short columns (C4: 64 RHS of 2048 x 1024), off
+    for a single small grid and for C3's theta_sym columns."""
+    with pkg.Plan(2048, 1024, 64) as plan:
+        assert plan.info()["variants"] & 1024
+    with pkg.Plan(2048, 1024) as plan:
+        assert not plan.info()["variants"] & 1024
+    with pkg.Plan(20000, 10000) as plan:
+        assert not plan.info()["variants"] & 1024
+
+
 @pytest.mark.parametrize("m,n", [(256, 1024), (128, 2048), (96, 512), (64, 4096)])
 def test_grid_pow2_rows_rough_data(pkg, oracle, reference, m, n):
     """Power-of-two lambda rows (N/2 = 256 .. 2048) run the lambda kernels on

@@ -665,10 +665,11 @@ sk_status sk_plan_create(int M, int N, int nrhs, int device, sk_plan_t* out) {
     if (const char* e = std::getenv("SK_LAMBDA_QUAD")) p->lambda_quad = std::atoi(e) != 0 ? 1 : 0;  // A/B
     if (const char* e = std::getenv("SK_LAMBDA_PAIR_INV")) p->lambda_pair_inv = std::atoi(e) != 0;  // opt-in A/B
     if (const char* e = std::getenv("SK_LAMBDA_DUO")) p->lambda_duo = std::atoi(e) != 0;  // A/B
-    // row-major forward spectrum + gathered theta columns (run_grid): on for large batches of short
-    // columns, where several theta CTAs per SM hide the gather (C4 2.48 -> 2.43 ms; C2 -0.8 %, C1 +1.4 %,
-    // C3's one-CTA-per-SM theta_sym +3 %: profiles/r2_phases_c3.md); SK_FWD_ROWS=0/1 forces it
-    p->fwd_rows = p->theta_hiocc && static_cast<size_t>(p->nrhs) * p->g.rows * p->g.cols >= (static_cast<size_t>(1) << 24);
+    // row-major forward spectrum + gathered theta columns (run_grid): on for theta_kernel solves of at
+    // least 2^23 spectral entries, where several theta CTAs per SM hide the gather (C4 2.48 -> 2.43 ms,
+    // 8 x 4096 x 2048 -3.1 %, 8192^2 -1.4 %; C2 -0.8 %, C1 +1.4 %, C3's one-CTA-per-SM theta_sym +3 %:
+    // profiles/r2_phases_c3.md); SK_FWD_ROWS=0/1 forces it
+    p->fwd_rows = static_cast<size_t>(p->nrhs) * p->g.rows * p->g.cols >= (static_cast<size_t>(1) << 23);
     if (const char* e = std::getenv("SK_FWD_ROWS")) p->fwd_rows = std::atoi(e) != 0;      // A/B
     if (p->grid_ok && (s = build_fft(Ll, p->thr_lambda, p->fl, odd_l, false, p->lambda_hiocc ? 8 : 25)) != SK_OK) {
         p->grid_ok = false;

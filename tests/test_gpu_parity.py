@@ -393,8 +393,9 @@ def test_fwd_rows_gather_bitwise(pkg, oracle, reference, m, n, nrhs, monkeypatch
 
 
 def test_fwd_rows_default_policy(pkg):
-    """On for large batches of short columns (C4: 64 RHS of 2048 x 1024), off
-    for a single small grid and for C3's theta_sym columns."""
+    """On for theta_kernel solves of at least 2^23 spectral entries (C4: 64
+    RHS of 2048 x 1024), off for a single small grid and for C3's theta_sym
+    columns."""
     with pkg.Plan(2048, 1024, 64) as plan:
         assert plan.info()["variants"] & 1024
     with pkg.Plan(2048, 1024) as plan:
